@@ -1,0 +1,360 @@
+/*
+ * qlm_oracle.c -- plain, slow, fp64 CPU oracle of QLM's RWT estimator
+ * evaluated over candidate queue orderings.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * (paper_2407_00047_b200/csrc); neither side includes the other.
+ *
+ * Citations: "P:Lx" = /root/reference/PAPER.md line x, "S:Lx" = SPEC.md.
+ * Every reading of a garbled or silent passage is listed in DESIGN.md
+ * ("Readings of the paper", R1..R14) and referenced here by its R-number.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared -o liboracle.so qlm_oracle.c -lm
+ * (-ffp-contract=off: no FMA contraction, so every + and * below is one IEEE
+ * round-to-nearest operation in source order.)
+ *
+ * Pins (tests/test_oracle_pins.py) -- every function below is pinned:
+ *   or_philox4x32_10   Random123 known-answer vectors.
+ *   or_enum_row        itertools.permutations lexicographic order (T <= 7).
+ *   or_random_row      permutation invariant + chi-square uniformity (T = 4).
+ *   or_estimate_row    SPEC worked examples S:L279/287/296/306/315, closed
+ *                      form for identical groups (Eq. 2/3), Insight-3
+ *                      transition arithmetic, textbook Phi-bar values.
+ *   or_score_row       SPEC S:L375 (-105 tie), X-Y-X example, C1 golden,
+ *                      SPT (min S2) and Moore-Hodgson (min S1) vs brute force.
+ *   or_mc_sample       closed form for constant tables, CLT normality test.
+ *   or_mc_count        deterministic-table special case == step function.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---- problem description (Table 3) ------------------ */
+typedef struct {
+    int32_t G, Q, D, M;
+    const int32_t *model;      /* [G] model of group i (Eq. 7)   */
+    const int32_t *n_req;      /* [G] requests in group i                    */
+    const double *slo;         /* [G] TTFT deadline, s (Eq. 8)   */
+    const double *mu;          /* [G] mean output tokens (Eq. 3)     */
+    const double *var;         /* [G] output-token variance (Eq. 3)          */
+    const int32_t *dist;       /* [G] MC length table id                     */
+    const int32_t *q_device;   /* [Q] device-type row                        */
+    const int32_t *q_resident; /* [Q] model loaded at t=0 (Def. 3)   */
+    const double *q_bmean;     /* [Q] pinned in-flight work, s (R12)         */
+    const double *q_bvar;      /* [Q]                                        */
+    const double *theta;       /* [D][M] tokens/s (Eq. 2)            */
+    const double *prefill;     /* [D][M] P (Eq. 1)               */
+    const double *eps;         /* [D][M] epsilon (Eq. 4)         */
+    const double *dtok;        /* [D][M] d (Eq. 4)                           */
+    const double *max_out;     /* [D][M] max output tokens (Eq. 4 bound)     */
+    const double *swap;        /* [D][M][M] swap time from->to (S)   */
+    int32_t K, n_tables;       /* MC length tables                           */
+    const uint16_t *len;       /* [n_tables][K]                              */
+    double z_clamp;            /* R9: v := 0 / 1 beyond +-z_clamp            */
+    double alpha;              /* n_over threshold                           */
+} or_problem;
+
+/* ---- Philox4x32-10 (Salmon et al., SC'11; Random123 reference) ---------- */
+void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }   /* key bump */
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* ---- candidate rows (encoding of Eq. 6; R10) ----------------
+ * A candidate is a row of T = G+Q-1 tokens: a permutation of 0..T-1 where
+ * token < G is a request group and token >= G separates virtual queues.    */
+
+/* RANDOM(seed, c): forward Fisher-Yates driven by Philox words (R10).     */
+void or_random_row(uint64_t seed, uint64_t c, int32_t T, int32_t *row)
+{
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint32_t words[4];
+    for (int32_t k = 0; k < T; ++k) row[k] = k;
+    for (int32_t i = 0; i + 1 < T; ++i) {
+        if (i % 4 == 0) {            /* one Philox block yields words 4b..4b+3 */
+            uint32_t ctr[4] = { (uint32_t)(i / 4), (uint32_t)c, (uint32_t)(c >> 32), 0x514C4D00u };
+            or_philox4x32_10(ctr, key, words);
+        }
+        uint32_t u = words[i % 4];
+        int32_t j = i + (int32_t)(((uint64_t)u * (uint64_t)(T - i)) >> 32);
+        int32_t t = row[i]; row[i] = row[j]; row[j] = t;
+    }
+}
+
+/* ENUM(c): Lehmer unranking, lexicographic order, c < T! (T <= 20).       */
+void or_enum_row(uint64_t c, int32_t T, int32_t *row)
+{
+    int32_t avail[64];
+    uint64_t fact[21];
+    fact[0] = 1;
+    for (int k = 1; k <= 20; ++k) fact[k] = fact[k - 1] * (uint64_t)k;
+    for (int32_t k = 0; k < T; ++k) avail[k] = k;
+    int32_t left = T;
+    for (int32_t pos = 0; pos < T; ++pos) {
+        uint64_t f = fact[T - 1 - pos];
+        int32_t k = (int32_t)(c / f);
+        c = c % f;
+        row[pos] = avail[k];
+        for (int32_t m = k; m + 1 < left; ++m) avail[m] = avail[m + 1];
+        --left;
+    }
+}
+
+/* ---- RWT estimator over one ordering ------------------------------------ */
+
+/* C - W for a group of model m on device d: P + D with D = max_out*eps*d
+ * (Eq. 1, Eq. 4 P:L632-648 with O_q := max output, Eq. 5 R3). */
+static double tail_of(const or_problem *p, int32_t d, int32_t m)
+{
+    int32_t k = d * p->M + m;
+    return p->prefill[k] + p->max_out[k] * p->eps[k] * p->dtok[k];
+}
+
+/* Per-group waiting time wt_i (mean, Eq. 2/10) and variance V_i (Eq. 3),
+ * plus its queue index and position.  Reading of Eq. 10 (P:L741-746 and the
+ * prose of P:L705): walking a queue in order, an exclusive accumulator A
+ * holds the expected time until the slot can start, B its variance.
+ *   - on a model change into the slot (Eq. 9, m_{-1} = resident model, R4):
+ *       A += tail(previous model)   [the group before the boundary contributes
+ *                                    its completion C = W + P + D, R1]
+ *            (skipped at the queue's first slot unless a backlog is pinned, R4/R12)
+ *       A += swap[prev][m]          [Eq. 10 2nd term, incl. slot's own switch, R2]
+ *   - wt = A, V = B                 [exclusive: groups ahead only, R5]
+ *   - A += n*mu/Theta, B += n*var/Theta^2   [Eq. 2/3, each group its own stats, R6/R7]
+ * Returns 0, or -1 if the row is not a permutation of 0..T-1 (Eq. 6).     */
+int or_estimate_row(const or_problem *p, const int32_t *row,
+                    double *wt, double *V, int32_t *queue_of, int32_t *pos_of)
+{
+    int32_t T = p->G + p->Q - 1;
+    char seen[4096];
+    if (T > 4096) return -1;
+    memset(seen, 0, (size_t)T);
+    for (int32_t s = 0; s < T; ++s) {
+        if (row[s] < 0 || row[s] >= T || seen[row[s]]) return -1;
+        seen[row[s]] = 1;
+    }
+    int32_t q = 0;
+    int32_t d = p->q_device[0], prev = p->q_resident[0], first = 1, pos = 0;
+    double A = p->q_bmean[0], B = p->q_bvar[0];
+    for (int32_t s = 0; s < T; ++s) {
+        int32_t tok = row[s];
+        if (tok >= p->G) {                       /* queue separator */
+            ++q;
+            d = p->q_device[q]; prev = p->q_resident[q]; first = 1; pos = 0;
+            A = p->q_bmean[q]; B = p->q_bvar[q];
+            continue;
+        }
+        int32_t i = tok, m = p->model[i];
+        if (m != prev) {                                     /* t = 1, Eq. 9 */
+            int backlog = p->q_bmean[q] > 0.0;
+            if (!first || backlog) A = A + tail_of(p, d, prev);
+            A = A + p->swap[(d * p->M + prev) * p->M + m];
+        }
+        wt[i] = A;
+        V[i] = B;
+        if (queue_of) queue_of[i] = q;
+        if (pos_of) pos_of[i] = pos;
+        double th = p->theta[d * p->M + m];
+        A = A + ((double)p->n_req[i] * p->mu[i]) / th;
+        B = B + ((double)p->n_req[i] * p->var[i]) / (th * th);
+        prev = m; first = 0; ++pos;
+    }
+    return 0;
+}
+
+/* SLO-violation probability of one group: P(wt_true > slo) under the CLT
+ * Normal N(wt, V) of Eq. 3, R8; V = 0 -> step, met iff
+ * wt <= slo, R9; clamp beyond +-z_clamp, R9.                    */
+double or_violation(double wt, double V, double slo, double z_clamp)
+{
+    if (V > 0.0) {
+        double z = (slo - wt) / sqrt(V);
+        if (z >= z_clamp) return 0.0;
+        if (z <= -z_clamp) return 1.0;
+        return 0.5 * erfc(z / sqrt(2.0));
+    }
+    return wt > slo ? 1.0 : 0.0;
+}
+
+/* Per-candidate objective (R11): S1 = sum n_i v_i / sum n_i (expected
+ * fraction of violating requests, relaxation of p <= 0);
+ * S2 = sum_i p_i with p_i = wt_i - slo_i (Eq. 11, objective
+ * P:L761-767), both summed in row order; n_over = #{v_i > alpha}.          */
+int or_score_row(const or_problem *p, const int32_t *row, double *s1, double *s2, int32_t *n_over)
+{
+    int32_t G = p->G, T = p->G + p->Q - 1;
+    double *wt = (double *)malloc(sizeof(double) * (size_t)G);
+    double *V = (double *)malloc(sizeof(double) * (size_t)G);
+    int rc = or_estimate_row(p, row, wt, V, NULL, NULL);
+    if (rc == 0) {
+        double num = 0.0, den = 0.0, pen = 0.0;
+        int32_t over = 0;
+        for (int32_t s = 0; s < T; ++s) {
+            int32_t i = row[s];
+            if (i >= G) continue;
+            double v = or_violation(wt[i], V[i], p->slo[i], p->z_clamp);
+            num = num + (double)p->n_req[i] * v;
+            den = den + (double)p->n_req[i];
+            pen = pen + (wt[i] - p->slo[i]);
+            if (v > p->alpha) ++over;
+        }
+        *s1 = num / den;
+        *s2 = pen;
+        if (n_over) *n_over = over;
+    }
+    free(wt); free(V);
+    return rc;
+}
+
+/* ---- candidate ranges ---------------------------------------------------- */
+enum { OR_EXPLICIT = 0, OR_RANDOM = 1, OR_ENUM = 2 };
+
+static void get_row(int kind, const void *rows, int32_t token_bytes, int64_t stride,
+                    uint64_t seed, uint64_t c, int64_t local, int32_t T, int32_t *row)
+{
+    if (kind == OR_RANDOM) { or_random_row(seed, c, T, row); return; }
+    if (kind == OR_ENUM) { or_enum_row(c, T, row); return; }
+    const uint8_t *base = (const uint8_t *)rows + local * stride;
+    for (int32_t s = 0; s < T; ++s)
+        row[s] = token_bytes == 1 ? base[s] : ((const uint16_t *)base)[s];
+}
+
+/* Scores of candidates first..first+count-1.  Returns #invalid rows.      */
+int64_t or_score_range(const or_problem *p, int kind, const void *rows, int32_t token_bytes,
+                       int64_t stride, uint64_t seed, uint64_t first, int64_t count,
+                       double *s1, double *s2, int32_t *n_over)
+{
+    int32_t T = p->G + p->Q - 1;
+    int32_t *row = (int32_t *)malloc(sizeof(int32_t) * (size_t)T);
+    int64_t bad = 0;
+    for (int64_t k = 0; k < count; ++k) {
+        get_row(kind, rows, token_bytes, stride, seed, first + (uint64_t)k, k, T, row);
+        if (or_score_row(p, row, &s1[k], &s2[k], n_over ? &n_over[k] : NULL) != 0) {
+            s1[k] = NAN; s2[k] = NAN; ++bad;
+        }
+    }
+    free(row);
+    return bad;
+}
+
+/* Per-group estimates of candidates first..first+count-1, each [count][G]:
+ * wt (mean), sd = sqrt(V), v.                                               */
+int64_t or_estimate_range(const or_problem *p, int kind, const void *rows, int32_t token_bytes,
+                          int64_t stride, uint64_t seed, uint64_t first, int64_t count,
+                          double *wt, double *sd, double *v)
+{
+    int32_t G = p->G, T = p->G + p->Q - 1;
+    int32_t *row = (int32_t *)malloc(sizeof(int32_t) * (size_t)T);
+    double *V = (double *)malloc(sizeof(double) * (size_t)G);
+    int64_t bad = 0;
+    for (int64_t k = 0; k < count; ++k) {
+        get_row(kind, rows, token_bytes, stride, seed, first + (uint64_t)k, k, T, row);
+        double *w = wt + k * G;
+        if (or_estimate_row(p, row, w, V, NULL, NULL) != 0) { ++bad; continue; }
+        for (int32_t i = 0; i < G; ++i) {
+            sd[k * G + i] = sqrt(V[i]);
+            v[k * G + i] = or_violation(w[i], V[i], p->slo[i], p->z_clamp);
+        }
+    }
+    free(row); free(V);
+    return bad;
+}
+
+/* ---- Monte-Carlo mode (R13) ----------------------------------------------
+ * Output lengths are sampled per request: for trial t, group k, request r,
+ *   word = Philox4x32-10(key = mc_seed, ctr = (r/4, k, t, 0x4D430000))[r%4]
+ *   O    = len[dist_k][word >> (32 - log2 K)]
+ * X[t][k] = sum_r O (exact integer), the group's total output tokens.      */
+void or_mc_sample(const or_problem *p, uint64_t mc_seed, int64_t trial_first,
+                  int64_t trial_count, uint32_t *X /* [trial_count][G] */)
+{
+    int32_t shift = 32;
+    for (int32_t k = p->K; k > 1; k >>= 1) --shift;
+    uint32_t key[2] = { (uint32_t)mc_seed, (uint32_t)(mc_seed >> 32) };
+    uint32_t words[4];
+    for (int64_t tt = 0; tt < trial_count; ++tt) {
+        uint32_t t = (uint32_t)(trial_first + tt);
+        for (int32_t k = 0; k < p->G; ++k) {
+            const uint16_t *tab = p->len + (int64_t)p->dist[k] * p->K;
+            uint32_t sum = 0;
+            for (int32_t r = 0; r < p->n_req[k]; ++r) {
+                if (r % 4 == 0) {
+                    uint32_t ctr[4] = { (uint32_t)(r / 4), (uint32_t)k, t, 0x4D430000u };
+                    or_philox4x32_10(ctr, key, words);
+                }
+                sum += tab[words[r % 4] >> shift];
+            }
+            X[tt * p->G + k] = sum;
+        }
+    }
+}
+
+/* For each candidate row and trial: the Eq. 10 walk of or_estimate_row with
+ * the sampled X/Theta in place of n*mu/Theta (Eq. 2 with the realised token
+ * count); counts[c][k] += (W_k > slo_k).  Returns #invalid rows.           */
+int64_t or_mc_count(const or_problem *p, int kind, const void *rows, int32_t token_bytes,
+                    int64_t stride, uint64_t seed, uint64_t first, int64_t count,
+                    const uint32_t *X, int64_t trial_count, uint32_t *counts /* [count][G] */)
+{
+    int32_t G = p->G, T = p->G + p->Q - 1;
+    int32_t *row = (int32_t *)malloc(sizeof(int32_t) * (size_t)T);
+    int64_t bad = 0;
+    for (int64_t c = 0; c < count; ++c) {
+        get_row(kind, rows, token_bytes, stride, seed, first + (uint64_t)c, c, T, row);
+        uint32_t *cnt = counts + c * G;
+        for (int32_t i = 0; i < G; ++i) cnt[i] = 0;
+        char seen[4096];
+        int ok = T <= 4096;
+        if (ok) {
+            memset(seen, 0, (size_t)T);
+            for (int32_t s = 0; s < T; ++s) {
+                if (row[s] < 0 || row[s] >= T || seen[row[s]]) { ok = 0; break; }
+                seen[row[s]] = 1;
+            }
+        }
+        if (!ok) { ++bad; continue; }
+        for (int64_t t = 0; t < trial_count; ++t) {
+            const uint32_t *x = X + t * G;
+            int32_t q = 0;
+            int32_t d = p->q_device[0], prev = p->q_resident[0], first_slot = 1;
+            double A = p->q_bmean[0];
+            for (int32_t s = 0; s < T; ++s) {
+                int32_t tok = row[s];
+                if (tok >= G) {
+                    ++q;
+                    d = p->q_device[q]; prev = p->q_resident[q]; first_slot = 1;
+                    A = p->q_bmean[q];
+                    continue;
+                }
+                int32_t i = tok, m = p->model[i];
+                if (m != prev) {
+                    int backlog = p->q_bmean[q] > 0.0;
+                    if (!first_slot || backlog) A = A + tail_of(p, d, prev);
+                    A = A + p->swap[(d * p->M + prev) * p->M + m];
+                }
+                if (A > p->slo[i]) cnt[i] += 1;
+                A = A + (double)x[i] / p->theta[d * p->M + m];
+                prev = m; first_slot = 0;
+            }
+        }
+    }
+    free(row);
+    return bad;
+}

@@ -1,0 +1,419 @@
+"""Pins of the CPU oracle against what the paper / SPEC / mathematics fix.
+
+None of these re-types the oracle's formulas: each expected value comes from
+a SPEC worked example, a hand derivation stored under tests/golden/ (with its
+citation), a closed form, a textbook algorithm (SPT, Moore-Hodgson), a
+library-defined order (itertools), published known-answer vectors (Random123)
+or a statistical law (CLT).  See DESIGN.md "Oracle pins".
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import stats
+
+import oracle as O
+from tests.handmade import hand_problem, rank_of
+from workloads.synth import make_config, make_problem, make_random_problem, balanced_row
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------- Philox (P13)
+def test_philox_random123_kat():
+    # Random123 kat_vectors, philox4x32_10 (Salmon et al. SC'11).
+    kat = [
+        ((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+        ((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2, (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+        ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+         (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
+    ]
+    for ctr, key, want in kat:
+        assert tuple(int(x) for x in O.philox4x32_10(ctr, key)) == want
+
+
+# ---------------------------------------------------------------- rows (Eq. 6)
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 6, 7])
+def test_enum_rows_are_lexicographic_permutations(T):
+    for c, perm in enumerate(itertools.permutations(range(T))):
+        assert tuple(O.enum_row(c, T)) == perm
+
+
+@pytest.mark.parametrize("T", [1, 2, 5, 71, 300, 1055])
+def test_random_rows_are_permutations(T):
+    for c in [0, 1, 2, 12345, 2**33 + 7]:
+        row = O.random_row(1, c, T)
+        assert sorted(row.tolist()) == list(range(T))
+
+
+def test_random_rows_uniform_over_permutations():
+    # Fisher-Yates with independent uniform indices gives every permutation
+    # probability 1/T!; chi-square over the 24 permutations of T = 4.
+    T, N = 4, 24000
+    counts = {}
+    for c in range(N):
+        key = tuple(O.random_row(7, c, T))
+        counts[key] = counts.get(key, 0) + 1
+    assert len(counts) == 24
+    chi2 = sum((v - N / 24) ** 2 / (N / 24) for v in counts.values())
+    assert stats.chi2.sf(chi2, 23) > 1e-3
+    # the seed changes the stream
+    assert [tuple(O.random_row(1, c, 20)) for c in range(5)] != \
+           [tuple(O.random_row(2, c, 20)) for c in range(5)]
+
+
+# ---------------------------------------------------------------- SPEC worked examples
+def test_wait_mean_and_std_S279():
+    g = gold("spec_examples.json")["wait_S279"]
+    # group A (25 requests) ahead of group B, same model = resident, one queue
+    p = hand_problem([0, 0], [g["requests_ahead"], 1], g["mu"], g["sigma"] ** 2, [1e9, 5.5],
+                     theta=g["theta"])
+    o = O.Oracle(p)
+    e = o.estimate([0, 1])
+    assert e["wt"][1] == pytest.approx(g["mean"], abs=1e-12)
+    assert math.sqrt(e["V"][1]) == pytest.approx(g["std"], abs=1e-12)
+    assert e["wt"][0] == 0.0 and e["V"][0] == 0.0       # empty queue ahead
+    # slo = mean + 1 std -> Phi-bar(1) (textbook)
+    tb = dict((z, v) for z, v in gold("phibar_textbook.json")["values"])
+    s1, s2, _ = o.score([0, 1])
+    assert s1 * 26 == pytest.approx(tb[1.0], abs=1e-14)   # n_B = 1 of 26 requests
+
+
+def test_serve_time_S306():
+    g = gold("spec_examples.json")["serve_S306"]
+    p = hand_problem([0, 0], [g["n"], 1], g["mu"], 0.0, 100.0, theta=g["theta"])
+    assert O.Oracle(p).estimate([0, 1])["wt"][1] == pytest.approx(g["serve_time"], abs=1e-12)
+
+
+def test_transition_tail_S287_S296():
+    g1 = gold("spec_examples.json")["decode_S287"]
+    g2 = gold("spec_examples.json")["completion_S296"]
+    # X group (8 s of work) then a Y group: the Y group waits W_X + C_X - W_X + swap
+    # = 8 + P + max_out*eps*d + S  (Eq. 1/4/10, readings R1/R2)
+    S = 20.0
+    p = hand_problem([0, 1], [40, 1], 200.0, 0.0, 1000.0, theta=1000.0, prefill=g2["prefill"],
+                     eps=g1["eps"], dtok=g1["d"], max_out=g1["max_out"], swap=S, M=2)
+    e = O.Oracle(p).estimate([0, 1])
+    assert e["wt"][1] == pytest.approx(8.0 + g2["completion"] + S, abs=1e-9)
+    assert g2["completion"] == pytest.approx(g2["prefill"] + g1["decode"])
+    # reverse order: the Y group is first in a queue whose resident is X -> swap only (R4)
+    e = O.Oracle(p).estimate([1, 0])
+    assert e["wt"][1] == pytest.approx(S, abs=0)
+    # and the X group behind it pays Y's tail + swap back
+    assert e["wt"][0] == pytest.approx(S + 1 * 200.0 / 1000.0 + g2["completion"] + S,
+                                       abs=1e-9)
+
+
+def test_slack_and_step_violation_S315():
+    g = gold("spec_examples.json")["slack_S315"]
+    # A: 8 s of work (n=40, mu=200, Theta=1000), sigma = 0 -> V = 0 -> step function
+    p = hand_problem([0, 0], [40, 10], 200.0, 0.0, [g["slo_A"], g["slo_B"]], theta=1000.0)
+    o = O.Oracle(p)
+    e = o.estimate([0, 1])
+    assert e["wt"][1] == g["predicted_B"]
+    assert g["slo_B"] - e["wt"][1] == g["slack_B"]
+    s1, s2, n_over = o.score([0, 1])
+    assert s1 == 10 / 50 and n_over == 1
+    assert s2 == (0 - g["slo_A"]) + (g["predicted_B"] - g["slo_B"])
+    # boundary: ttft == slo is met
+    p2 = hand_problem([0, 0], [40, 10], 200.0, 0.0, [10.0, 8.0], theta=1000.0)
+    assert O.Oracle(p2).score([0, 1])[0] == 0.0
+
+
+def test_objective_tie_S375():
+    g = gold("spec_examples.json")["tie_S375"]
+    # serve 5 s each: n = 25, mu = 200, Theta = 1000, sigma = 0
+    p = hand_problem([0, 0], [25, 25], 200.0, 0.0, g["slos"], theta=1000.0)
+    o = O.Oracle(p)
+    r = o.score_range(O.ENUM, 0, 2)
+    assert list(r["s2"]) == [g["objective"], g["objective"]]
+    assert O.argmin_key(r["s1"], r["s2"]) == 0          # tie -> lowest index (tighter first)
+    e = o.estimate([0, 1])
+    assert list(e["wt"] - np.asarray(g["slos"])) == g["penalties_tighter_first"]
+
+
+# ---------------------------------------------------------------- hand-derived goldens
+def test_xyx_example_P6():
+    g = gold("p6_xyx.json")
+    p = hand_problem([0, 1, 0], 25, 200.0, 0.0, 100.0, theta=1000.0, prefill=0.5, eps=1.0,
+                     dtok=0.5, max_out=1.0, swap=20.0, M=2)
+    o = O.Oracle(p)
+    r = o.score_range(O.ENUM, 0, 6)
+    for k, want in g["orders"].items():
+        k = int(k)
+        assert rank_of(want["order"]) == k
+        assert list(o.estimate(want["order"])["wt"]) == want["wt_by_group"]
+        assert r["s2"][k] == want["S2"]
+        assert r["s1"][k] == 0.0
+    assert O.argmin_key(r["s1"], r["s2"]) == g["argmin"]
+
+
+def test_c1_golden_P7():
+    g = gold("p7_c1.json")
+    p = make_config("C1")
+    o = O.Oracle(p)
+    r = o.score_range(O.ENUM, 0, 24)
+    assert O.argmin_key(r["s1"], r["s2"]) == g["argmin"] == rank_of(g["argmin_order"])
+    e = o.estimate(g["argmin_order"])
+    np.testing.assert_allclose(e["wt"], g["argmin_wt_by_group"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(e["V"], g["argmin_V_by_group"], rtol=0, atol=1e-12)
+    assert r["s1"][12] == g["argmin_S1"]
+    assert r["s2"][12] == pytest.approx(g["argmin_S2"], abs=1e-12)
+    assert rank_of(g["runner_up_order"]) == g["runner_up"]
+    s1_ru = 40 * 0.5 * math.erfc(3 / math.sqrt(0.85) / math.sqrt(2)) / 125
+    assert r["s1"][13] == pytest.approx(s1_ru, rel=1e-12)
+    assert r["s2"][13] == pytest.approx(g["runner_up_S2"], abs=1e-12)
+    assert r["s1"].max() == pytest.approx(g["worst_S1"], abs=1e-15)
+    assert r["s1"][rank_of(g["worst_order"])] == pytest.approx(g["worst_S1"], abs=1e-15)
+
+
+def test_phibar_textbook_P16():
+    for z, want in gold("phibar_textbook.json")["values"]:
+        assert O.violation(0.0, 1.0, z) == pytest.approx(want, abs=2e-16 + 1e-14 * want)
+        # scale invariance: only the z-score matters
+        assert O.violation(100.0, 4.0, 100.0 + 2 * z) == pytest.approx(want, abs=1e-14)
+    assert O.violation(0.0, 1.0, 8.5) == 0.0          # clamp (R9)
+    assert O.violation(0.0, 1.0, -8.5) == 1.0
+    assert 0.0 < O.violation(0.0, 1.0, 7.9) < 1e-14
+    assert O.violation(5.0, 0.0, 5.0) == 0.0          # V = 0: met iff wt <= slo
+    assert O.violation(5.0, 0.0, 4.999) == 1.0
+
+
+# ---------------------------------------------------------------- closed forms
+def test_identical_groups_closed_form_P8():
+    # Eq. 2/3 with q-1 identical groups ahead: wt = s*n*mu/Theta, V = s*n*sigma^2/Theta^2
+    G, n, mu, var, th = 40, 37, 311.0, 5000.0, 1700.0
+    p = hand_problem([0] * G, n, mu, var, 1e6, theta=th)
+    rng = np.random.default_rng(3)
+    order = rng.permutation(G)
+    e = O.Oracle(p).estimate(order)
+    for s, i in enumerate(order):
+        assert e["wt"][i] == pytest.approx(s * n * mu / th, rel=1e-13, abs=0)
+        assert e["V"][i] == pytest.approx(s * n * var / th**2, rel=1e-13, abs=0)
+        assert e["pos"][i] == s and e["queue"][i] == 0
+
+
+def test_insight3_interleaving_costs_extra_transitions():
+    # PAPER.md L351-357 / SPEC.md L316: interleaved X,Y,X,Y vs grouped X,X,Y,Y.
+    tail, S = 1.0, 20.0
+    p = hand_problem([0, 1, 0, 1], 25, 200.0, 0.0, 1e4, theta=1000.0, prefill=0.5, eps=1.0,
+                     dtok=0.5, max_out=1.0, swap=S, M=2)
+    o = O.Oracle(p)
+    inter = o.estimate([0, 1, 2, 3])["wt"]   # X1 Y1 X2 Y2: 3 transitions
+    group = o.estimate([0, 2, 1, 3])["wt"]   # X1 X2 Y1 Y2: 1 transition
+    assert inter[3] - group[3] == pytest.approx(2 * (tail + S), abs=1e-12)
+    assert inter.sum() - group.sum() == pytest.approx(4 * (tail + S), abs=1e-12)
+
+
+def _brute(o, G):
+    return o.score_range(O.ENUM, 0, math.factorial(G))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_spt_minimises_total_penalty_P9(seed):
+    # sigma = 0, one queue, one model: S2 = sum_j wt_j - sum slo is total start time,
+    # minimised by shortest-processing-time order (textbook 1||sum C_j).
+    rng = np.random.default_rng(100 + seed)
+    G = int(rng.integers(2, 8))
+    n = rng.integers(1, 300, G)
+    mu = rng.uniform(10, 500, G)
+    slo = rng.uniform(1, 100, G)
+    p = hand_problem([0] * G, n, mu, 0.0, slo, theta=1234.0)
+    a = np.sort(n * mu / 1234.0)
+    spt = sum(a[k] * (G - 1 - k) for k in range(G)) - slo.sum()
+    r = _brute(O.Oracle(p), G)
+    assert r["s2"].min() == pytest.approx(spt, rel=1e-12, abs=1e-9)
+
+
+def _moore_hodgson(p_times, due):
+    order = np.argsort(due, kind="stable")
+    sched, t, late = [], 0.0, 0
+    for j in order:
+        sched.append(j)
+        t += p_times[j]
+        if t > due[j]:
+            k = max(sched, key=lambda x: p_times[x])
+            sched.remove(k)
+            t -= p_times[k]
+            late += 1
+    return late
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_moore_hodgson_minimises_violations_P10(seed):
+    # sigma = 0, equal n: S1 * G = #late; late iff start > slo iff C > slo + W
+    # (due dates slo + W, textbook 1||sum U_j).
+    rng = np.random.default_rng(200 + seed)
+    G = int(rng.integers(2, 8))
+    mu = rng.uniform(10, 500, G)
+    p_times = 50 * mu / 1000.0
+    slo = rng.uniform(0.5, 1.0, G) * p_times.sum() * rng.uniform(0.2, 1.0)
+    p = hand_problem([0] * G, 50, mu, 0.0, slo, theta=1000.0)
+    r = _brute(O.Oracle(p), G)
+    assert round(r["s1"].min() * G, 9) == _moore_hodgson(p_times, slo + p_times)
+
+
+# ---------------------------------------------------------------- invariants (P11)
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_invariants_app_b(cfg):
+    p = make_config(cfg)
+    o = O.Oracle(p)
+    for c in range(40):
+        row = O.random_row(1, c, p.T)
+        e = o.estimate(row)
+        for q in range(p.Q):
+            idx = np.where(e["queue"] == q)[0]
+            idx = idx[np.argsort(e["pos"][idx])]
+            assert np.all(np.diff(e["wt"][idx]) >= 0)          # monotone wt
+            assert np.all(np.diff(e["V"][idx]) >= 0)
+        s1, s2, _ = o.score(row)
+        assert 0.0 <= s1 <= 1.0
+        assert s2 == pytest.approx((e["wt"] - p.slo).sum(), rel=1e-12)
+        # expected-violation mass is an integer when every v is 0 or 1
+        v = np.array([O.violation(e["wt"][i], e["V"][i], p.slo[i]) for i in range(p.G)])
+        if np.all((v == 0) | (v == 1)):
+            assert (s1 * p.n_req.sum()) == pytest.approx(round(s1 * p.n_req.sum()), abs=1e-9)
+
+
+def test_zero_swap_within_one_model_and_separability():
+    rng = np.random.default_rng(5)
+    # all groups of the resident model: no transition cost anywhere
+    p = hand_problem([0] * 9, rng.integers(1, 100, 9), rng.uniform(50, 300, 9),
+                     rng.uniform(0, 1e4, 9), 50.0, Q=3, swap=1e6, prefill=1e6)
+    o = O.Oracle(p)
+    row = O.random_row(3, 11, p.T)
+    e = o.estimate(row)
+    a = p.n_req * p.mu / 1000.0
+    for q in range(3):
+        idx = np.where(e["queue"] == q)[0]
+        idx = idx[np.argsort(e["pos"][idx])]
+        if len(idx) == 0:
+            continue
+        np.testing.assert_allclose(e["wt"][idx], np.concatenate([[0], np.cumsum(a[idx])[:-1]]),
+                                   rtol=1e-13, atol=0)
+    # separability: S2 of the row = sum over queues of each queue scored alone
+    pr = make_config("C2")
+    o2 = O.Oracle(pr)
+    row = O.random_row(1, 5, pr.T)
+    s1, s2, _ = o2.score(row)
+    e = o2.estimate(row)
+    tot = 0.0
+    for q in range(pr.Q):
+        idx = np.where(e["queue"] == q)[0]
+        tot += (e["wt"][idx] - pr.slo[idx]).sum()
+    assert s2 == pytest.approx(tot, rel=1e-12)
+
+
+def test_queue_label_symmetry():
+    # two queues with identical (device, resident, backlog): swapping their contents
+    # leaves the multiset of (wt, V) and both scores unchanged.
+    rng = np.random.default_rng(9)
+    p = make_random_problem(rng, 10, 2, 3, 1)
+    p.q_resident[:] = 1
+    p.q_device[:] = 0
+    o = O.Oracle(p)
+    row = O.random_row(4, 1, p.T)
+    bar = int(np.where(row >= p.G)[0][0])
+    swapped = np.concatenate([row[bar + 1:], [row[bar]], row[:bar]])
+    a, b = o.score(row), o.score(swapped)
+    assert a[0] == pytest.approx(b[0], abs=1e-15)
+    assert a[1] == pytest.approx(b[1], rel=1e-12)
+    ea, eb = o.estimate(row), o.estimate(swapped)
+    np.testing.assert_array_equal(ea["wt"], eb["wt"])
+    np.testing.assert_array_equal(ea["V"], eb["V"])
+
+
+def test_backlog_makes_first_switch_pay_tail():
+    # R12: a pinned in-flight backlog of the resident model must drain (its tail)
+    # before a different model can be swapped in.
+    p = hand_problem([1], 10, 100.0, 0.0, 1e3, M=2, theta=1000.0, prefill=0.5, eps=1.0,
+                     dtok=0.5, max_out=1.0, swap=7.0, backlog_mean=[3.0], backlog_var=[0.25])
+    e = O.Oracle(p).estimate([0])
+    assert e["wt"][0] == 3.0 + 1.0 + 7.0 and e["V"][0] == 0.25
+
+
+def test_invalid_rows_rejected():
+    p = make_config("C1")
+    o = O.Oracle(p)
+    with pytest.raises(ValueError):
+        o.estimate([0, 1, 1, 3])
+    with pytest.raises(ValueError):
+        o.estimate([0, 1, 2, 4])
+
+
+# ---------------------------------------------------------------- Monte-Carlo (P14/P15)
+def test_mc_constant_table_closed_form():
+    L = 123
+    tabs = np.full((2, 256), L, np.uint16)
+    tabs[1] = 7
+    p = hand_problem([0, 0, 0], [5, 17, 300], 123.0, 0.0, [1.0, 3.0, 4.0], theta=1000.0,
+                     len_tables=tabs, dist=[0, 1, 0])
+    X = O.Oracle(p).mc_sample(2, 0, 5)
+    assert np.all(X[:, 0] == 5 * L) and np.all(X[:, 1] == 17 * 7) and np.all(X[:, 2] == 300 * L)
+
+
+def test_mc_two_value_table_parity_and_mean():
+    tab = np.array([[1] * 512 + [3] * 512], np.uint16)
+    n = 400
+    p = hand_problem([0], n, 2.0, 1.0, 1.0, len_tables=tab, dist=[0])
+    X = O.Oracle(p).mc_sample(9, 0, 2000)[:, 0].astype(np.int64)
+    assert np.all((X - n) % 2 == 0) and X.min() >= n and X.max() <= 3 * n
+    # Binomial(n, 1/2) upper-half draws: mean 2n, sd = 2*sqrt(n/4) = sqrt(n)
+    assert abs(X.mean() - 2 * n) < 5 * math.sqrt(n) / math.sqrt(2000)
+
+
+def test_mc_clt_normality_P15():
+    # Appendix A: sums of n i.i.d. table draws are ~Normal.
+    p = make_config("C4")
+    tab = p.len_tables[int(p.dist[0])].astype(np.float64)
+    mu, var = tab.mean(), tab.var()
+    n = 200
+    q = hand_problem([0], n, mu, var, 1.0, len_tables=p.len_tables, dist=[p.dist[0]])
+    X = O.Oracle(q).mc_sample(2, 0, 3000)[:, 0].astype(np.float64)
+    z = (X - n * mu) / math.sqrt(n * var)
+    assert abs(z.mean()) < 4 / math.sqrt(3000)
+    assert abs(z.std() - 1) < 0.06
+    assert stats.kstest(z, "norm").pvalue > 0.01
+
+
+def test_mc_deterministic_table_is_step_function():
+    # constant lengths L: X/Theta is exactly n*L/Theta, so the MC walk equals the
+    # Gaussian walk with sigma = 0 and counts are T_mc * [wt > slo].
+    L = 64
+    tabs = np.full((1, 64), L, np.uint16)
+    rng = np.random.default_rng(1)
+    p = make_random_problem(rng, 12, 3, 2, 2, sigma_zero=True)
+    p.mu[:] = L
+    p.len_tables = tabs
+    p.dist = np.zeros(p.G, np.int32)
+    o = O.Oracle(p)
+    X = o.mc_sample(5, 0, 7)
+    for c in range(10):
+        row = O.random_row(1, c, p.T)
+        e = o.estimate(row)
+        cnt = o.mc_count(O.EXPLICIT, 0, 1, X, rows=row[None, :].astype(np.uint8))[0]
+        np.testing.assert_array_equal(cnt, 7 * (e["wt"] > p.slo))
+
+
+def test_mc_vs_gaussian_within_clt_scale():
+    # statistical sanity (not parity): MC violation frequency vs the Gaussian
+    # estimate on the C4 balanced ordering, within Edgeworth scale + 5 s.e.
+    p = make_config("C4")
+    o = O.Oracle(p)
+    row = balanced_row(p.G, p.Q)
+    T_mc = 400
+    X = o.mc_sample(2, 0, T_mc)
+    cnt = o.mc_count(O.EXPLICIT, 0, 1, X, rows=row[None, :])[0]
+    e = o.estimate(row.astype(np.int32))
+    v = np.array([O.violation(e["wt"][i], e["V"][i], p.slo[i]) for i in range(p.G)])
+    vmc = cnt / T_mc
+    se = np.sqrt(np.maximum(v * (1 - v), 1e-4) / T_mc)
+    assert np.all(np.abs(vmc - v) <= 0.03 + 5 * se)
