@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Bench: RWT-scored queue orderings / s on 1..8 B200 (BASELINE.json metric).
+
+One step = one pass of the whole hot path over one batch of
+C3 (64 groups, 4 models, 8 virtual queues) on every GPU:
+  a1-a5,a7  qlm_best_ordering_async: 1e6 RANDOM candidates generated on the
+            device, Eq. 10 scan, violation probabilities, S1/S2, argmin
+  a8        global min-loc: NCCL all-gather of 16-B records + reduce kernel
+  a6        qlm_rwt_estimate: per-(candidate, group) wt / sd / v for the same
+            1e6 candidates (768 MB of fp32 written to HBM)
+  a9        decode of the global winner (queue, position per group)
+  a10-a12   qlm_mc_estimate of the winner: 1221 Philox trials per GPU,
+            counts summed with one NCCL all-reduce
+Weak scaling: rank r scores global indices [r*1e6, (r+1)*1e6).
+
+`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample
+of the same step on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = "C3"
+N_PER_GPU = 1_000_000
+MC_TRIALS = 1221
+METRIC = "RWT-scored queue orderings/sec"
+UNIT = "orderings/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(world):
+    return {
+        "workload": f"{CFG}: 64 request groups, 4 models (7B/13B/70B-like), 8 virtual queues "
+                    f"(A100-like profile, App. B); per GPU per step {N_PER_GPU:.0e} RANDOM candidate "
+                    f"orderings scored + argmin, bulk per-group wt/sd/v for all of them, "
+                    f"MC ({MC_TRIALS} trials) of the global winner",
+        "groups": 64, "queues": 8, "models": 4, "candidates_per_gpu": N_PER_GPU,
+        "mc_trials_per_gpu": MC_TRIALS, "parallelism": f"dp{world}",
+        "l2": "not flushed explicitly: every step writes 768 MB of bulk estimates per GPU "
+              "(>6x the 126 MB L2), evicting it between steps",
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML while the timed region runs."""
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            names = {N.nvmlClocksThrottleReasonHwSlowdown: "hw_slowdown",
+                     N.nvmlClocksThrottleReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                     N.nvmlClocksThrottleReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                     N.nvmlClocksThrottleReasonSwPowerCap: "sw_power_cap"}
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        for bit, name in names.items():
+                            if r & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # NVML missing: report that instead of a number
+            self.reasons.add(f"nvml_unavailable:{type(e).__name__}")
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- oracle leg
+def oracle_sample(n_cand: int, trials: int):
+    """One bounded sample of the step on the CPU oracle; returns seconds."""
+    import numpy as np
+    import oracle as O
+    from workloads.synth import make_config, CANDIDATE_SEED, MC_SEED
+    p = make_config(CFG)
+    o = O.Oracle(p)
+    t0 = time.perf_counter()
+    r = o.score_range(O.RANDOM, 0, n_cand, seed=CANDIDATE_SEED)
+    best = O.argmin_key(r["s1"], r["s2"])
+    o.estimate_range(O.RANDOM, 0, n_cand, seed=CANDIDATE_SEED)
+    row = O.random_row(CANDIDATE_SEED, best, p.T)
+    o.estimate(row)
+    if trials > 0:
+        X = o.mc_sample(MC_SEED, 0, trials)
+        o.mc_count(O.EXPLICIT, 0, 1, X, rows=row[None, :].astype(np.uint8))
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(budget_s: float = 15.0):
+    """Oracle on a bounded sample: ~budget_s of single-thread CPU work."""
+    t = oracle_sample(2000, 2)
+    n = int(max(2000, min(N_PER_GPU, 2000 * budget_s / max(t, 1e-6))))
+    trials = max(1, round(MC_TRIALS * n / N_PER_GPU))
+    t = oracle_sample(n, trials)
+    return {"value": n / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} of the {N_PER_GPU} C3 candidates of one step (score+argmin, bulk "
+                      f"estimates) + MC {trials} of {MC_TRIALS} trials, single-threaded plain C fp64 "
+                      f"(-O2 -ffp-contract=off), {t:.2f} s; value = sampled candidates / s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    per = None
+    # calibrate the per-step sample so that steps+warmup finish in ~120 s
+    t = oracle_sample(2000, 2)
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    n = int(max(200, min(N_PER_GPU, 2000 * budget / max(t, 1e-6))))
+    trials = max(1, round(MC_TRIALS * n / N_PER_GPU))
+    for _ in range(args.warmup):
+        oracle_sample(n, trials)
+    ts = [oracle_sample(n, trials) for _ in range(args.steps)]
+    tot = sum(ts)
+    per = tot / args.steps
+    value = n / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"each step: {n} of the {N_PER_GPU} C3 candidates (score+argmin, "
+                                   f"bulk estimates) + MC {trials} of {MC_TRIALS} trials; plain C "
+                                   f"fp64 oracle, single thread"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our leg
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__
+    from paper_2407_00047_b200 import RwtEstimator, kernel_launches, groups_array
+    from paper_2407_00047_b200.dist import global_best, sum_counts
+    from workloads.synth import make_config, CANDIDATE_SEED, MC_SEED
+
+    __graft_entry__.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    p = make_config(CFG)
+    est = RwtEstimator(p, device=local_rank)
+    G = p.G
+    stream = torch.cuda.current_stream(dev)
+    cand = est.random(first=rank * N_PER_GPU, count=N_PER_GPU, seed=CANDIDATE_SEED)
+    rec = torch.empty(2, dtype=torch.int64, device=dev)
+    bulk = {k: torch.empty((N_PER_GPU, G), dtype=torch.float32, device=dev) for k in ("wt", "sd", "v")}
+    counts = torch.empty((1, G), dtype=torch.int32, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(kt=None, groups_host=None, out_host=None):
+        if groups_host is not None:
+            est.update_groups(groups_host)                       # H2D of the step's inputs
+        if kt:
+            kt[0].record(stream)
+        r = est.best_ordering_async(cand, rec)
+        if kt:
+            kt[1].record(stream)
+        g = global_best(r, est.reduce_records)
+        if kt:
+            kt[2].record(stream)
+        est.rwt_estimate(cand, out=bulk)
+        if kt:
+            kt[3].record(stream)
+        win = est.from_record(g, seed=CANDIDATE_SEED)
+        qo, po = est.decode(win)
+        est.mc_estimate(win, mc_seed=MC_SEED, trials=MC_TRIALS, trial_first=rank * MC_TRIALS,
+                        counts=counts)
+        sum_counts(counts)
+        if out_host is not None:                                 # D2H of the step's result
+            out_host["rec"].copy_(g, non_blocking=True)
+            out_host["qo"].copy_(qo.view(-1), non_blocking=True)
+            out_host["po"].copy_(po.view(-1), non_blocking=True)
+            out_host["cnt"].copy_(counts.view(-1), non_blocking=True)
+        return g
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region
+    K = args.steps
+    kts = [[ev() for _ in range(4)] for _ in range(K)]
+    e0, e1 = ev(), ev()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = kernel_launches()
+    with ClockSampler(torch.cuda.get_device_properties(dev).index if hasattr(
+            torch.cuda.get_device_properties(dev), "index") else local_rank) as clk:
+        e0.record(stream)
+        for k in range(K):
+            step(kts[k])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = kernel_launches() - l0
+    t_ms = e0.elapsed_time(e1)
+    score_ms = sum(k[0].elapsed_time(k[1]) for k in kts) / K
+    bulk_ms = sum(k[2].elapsed_time(k[3]) for k in kts) / K
+    t = torch.tensor([t_ms, score_ms, bulk_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms, score_ms, bulk_ms = t.tolist()
+    ms_per_step = t_ms / K
+    value = N_PER_GPU * world / (ms_per_step / 1e3)
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        g_np = groups_array(p.model, p.n_req, p.slo, p.mu, p.var, p.dist)
+        groups_host = torch.from_numpy(g_np.view(np.uint8).copy()).pin_memory()
+        out_host = {"rec": torch.empty(2, dtype=torch.int64).pin_memory(),
+                    "qo": torch.empty(G, dtype=torch.int32).pin_memory(),
+                    "po": torch.empty(G, dtype=torch.int32).pin_memory(),
+                    "cnt": torch.empty(G, dtype=torch.int32).pin_memory()}
+        Ke = max(10, K // 5)
+        for _ in range(3):
+            step(groups_host=groups_host, out_host=out_host)
+            stream.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        x0, x1 = ev(), ev()
+        x0.record(stream)
+        for _ in range(Ke):
+            step(groups_host=groups_host, out_host=out_host)
+            stream.synchronize()                                  # the host reads the result
+            _ = int(out_host["rec"][1])
+        x1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([x0.elapsed_time(x1) / Ke], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": N_PER_GPU * world / (te.item() / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(groups_host.numel()),
+               "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in out_host.values())),
+               "ms_per_step": te.item(),
+               "note": "per step: pinned H2D of the 64 group records + table rebuild, the whole "
+                       "step, D2H of (record, decoded ordering, MC counts), host sync"}
+
+    if rank == 0:
+        peaks = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                peaks = json.load(f)
+        except Exception:
+            pass
+        hbm_peak = peaks.get("hbm_gbs")
+        peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if hbm_peak else \
+            "fallback 6650 GB/s (B200_PROFILING.md)"
+        hbm_peak = hbm_peak or 6650.0
+        bulk_bytes = N_PER_GPU * G * 3 * 4                     # algorithmic: outputs only (RANDOM)
+        bulk_gbs = bulk_bytes / (bulk_ms / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get(CFG, {}).get("bulk_kernel_dram_bytes_per_launch")
+        except Exception:
+            pass
+        roofline = {"kernel": "bulk_kernel (qlm_rwt_estimate)", "bound": "hbm",
+                    "achieved": bulk_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": bulk_gbs / hbm_peak, "traffic": traffic,
+                    "algorithmic_bytes_per_launch": bulk_bytes,
+                    "bytes_per_unit": G * 12, "units_per_launch": N_PER_GPU,
+                    "kernel_ms": bulk_ms, "peak_source": peak_src}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(world),
+            "roofline": roofline,
+            "kernels": {"score_argmin_ms": score_ms, "bulk_estimate_ms": bulk_ms,
+                        "score_argmin_orderings_per_s": N_PER_GPU / (score_ms / 1e3),
+                        "share_of_step": {"score_argmin": score_ms / ms_per_step,
+                                          "bulk_estimate": bulk_ms / ms_per_step}},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,213 @@
+/*
+ * qlm.h -- C ABI of the B200 bulk RWT-scoring library (libqlm.so).
+ *
+ * The library evaluates QLM's Request Waiting Time (RWT) estimator
+ * (Sec. 6, Eqs. 1-5) in bulk over candidate orderings of
+ * request groups into virtual queues, scores each ordering with the global
+ * scheduler's objective (Sec. 7, Eqs. 6-11 + objective, L665-767) and picks
+ * the best one.  "P:Lx" cites /root/reference/PAPER.md line x, "S:Lx"
+ * SPEC.md line x; R-numbers are the readings listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Return an int status (qlm_status); 0 = QLM_OK.  No exception or abort
+ *    crosses the ABI.  On error, qlm_last_error() returns a thread-local
+ *    message naming the offending field and index.
+ *  - Host arrays passed to qlm_create / qlm_update_groups are deep-copied;
+ *    the caller may free them on return.
+ *  - Device arrays (candidate rows, outputs) are caller-owned device memory
+ *    (e.g. torch tensors' data_ptr) on the context's device, 16-byte
+ *    aligned where stated.  The context owns its tables and scratch.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Bulk calls
+ *    are asynchronous on it; calls on one context must be stream-ordered
+ *    (a context is not thread-safe).
+ *  - No CPU fallback: if the device is not an sm_100 part, qlm_create fails
+ *    with QLM_ECUDA.
+ */
+#ifndef QLM_H
+#define QLM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QLM_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define QLM_API __attribute__((visibility("default")))
+#else
+#define QLM_API
+#endif
+
+typedef enum {
+    QLM_OK = 0,
+    QLM_EINVAL = 1,     /* invalid argument; qlm_last_error names it           */
+    QLM_ENOMEM = 2,     /* device allocation failed                             */
+    QLM_ECUDA = 3,      /* CUDA runtime error / unsupported device              */
+    QLM_EBADORDER = 5,  /* a row is not a permutation of 0..T-1 (Eq. 6)         */
+    QLM_ERANGE = 6      /* T > 65535, ENUM index >= T!, index overflow          */
+} qlm_status;
+
+typedef struct qlm_ctx qlm_ctx;
+
+/* A request group (Def. P:L443-447): homogeneous in model and SLO.        */
+typedef struct {
+    int32_t model;     /* [0, M): model served (m_i of Eq. 7)          */
+    int32_t n_req;     /* >= 1 requests in the group (<= 65536 if dist_id >= 0)     */
+    double slo_s;      /* > 0, finite: TTFT deadline in seconds (Def. 2) */
+    double mu_out;     /* > 0: mean output tokens per request (Eq. 3)        */
+    double var_out;    /* >= 0: variance of output tokens per request (Eq. 3)        */
+    int32_t dist_id;   /* MC length table of the group, or -1 (Gaussian only)        */
+    int32_t reserved;  /* must be 0                                                   */
+} qlm_group;           /* 40 bytes */
+
+/* A virtual queue = one serving instance (Def. P:L449-453, Def. 3). */
+typedef struct {
+    int32_t device;          /* [0, D): row of the per-device profile tables        */
+    int32_t resident_model;  /* [0, M): model loaded at t = 0 (m_{g,-1}, R4)        */
+    double backlog_mean_s;   /* >= 0: expected in-flight work pinned ahead (R12)     */
+    double backlog_var_s2;   /* >= 0: its variance                                    */
+} qlm_queue;                 /* 24 bytes */
+
+/* Offline-profiled constants per (device type, model).
+ * Row-major [D][M] unless stated.  The library derives, per (d, m):
+ *   tail = prefill + max_out * eps * decode   (C - W, Eq. 1 + Eq. 4, R3)    */
+typedef struct {
+    int32_t D, M;            /* >= 1 device types, >= 1 models                     */
+    const double *theta;     /* > 0 output tokens/s (Theta, Eq. 2)         */
+    const double *prefill_s; /* >= 0 prefill time P (Eq. 1)             */
+    const double *eps;       /* > 0 inefficiency factor epsilon (Eq. 4)             */
+    const double *decode_s;  /* >= 0 decode time per token d (Eq. 4)                */
+    const double *max_out;   /* >= 0 max output tokens O_q (Eq. 4)          */
+    const double *swap_s;    /* [D][M][M] >= 0 swap time from->to, diagonal 0 (S)   */
+} qlm_profile;
+
+/* Output-length quantile tables for the Monte-Carlo mode (R13).           */
+typedef struct {
+    int32_t K;               /* power of two in [2, 65536]                          */
+    int32_t n_tables;        /* >= 1                                                */
+    const uint16_t *len;     /* [n_tables][K] output lengths in tokens              */
+} qlm_len_tables;
+
+typedef struct {
+    double z_clamp;          /* > 0, default 8: v := 0/1 beyond +-z_clamp (R9)      */
+    double alpha;            /* [0, 1), default 0.01 (p99): n_over = #{v > alpha} */
+    int32_t device;          /* CUDA ordinal                                         */
+    int32_t reserved;        /* must be 0                                            */
+} qlm_options;
+
+/* Candidate orderings (encoding of Eq. 6, R10): a row of T = G+Q-1 tokens,
+ * a permutation of 0..T-1; token < G is a request group, token >= G a
+ * queue separator.  Queue q holds the groups between the q-th and the
+ * (q+1)-th separator, in order (position j of Eq. 6).                       */
+enum { QLM_CAND_EXPLICIT = 0, QLM_CAND_RANDOM = 1, QLM_CAND_ENUM = 2 };
+
+/* Best-candidate record, device-resident (16 bytes).  key orders
+ * candidates lexicographically by (fp32 S1, fp32 S2) (R11); ties go to the
+ * lowest index (R14).  key = UINT64_MAX / index = -1 means "none".          */
+typedef struct {
+    uint64_t key;    /* fp32bits(S1) << 32 | ord32(fp32 S2)                        */
+    int64_t index;   /* global candidate index                                      */
+} qlm_record;
+
+typedef struct {
+    int32_t kind;          /* QLM_CAND_*                                             */
+    int32_t token_bytes;   /* EXPLICIT: 1 (needs T <= 256) or 2                       */
+    const void *rows;      /* EXPLICIT: device [count][stride] bytes, 16-B aligned   */
+    int64_t stride;        /* EXPLICIT: bytes per row, multiple of 16, >= T*token_bytes */
+    uint64_t seed;         /* RANDOM: Philox key                                      */
+    int64_t first;         /* global index of the first candidate (RANDOM/ENUM)      */
+    int64_t count;         /* number of candidates, >= 0                              */
+    const qlm_record *first_from; /* optional device record: if non-NULL, count must be
+                              1 and the candidate index is read on the device from
+                              first_from->index at kernel time (no host sync); an
+                              index < 0 makes the call a no-op on the device.        */
+} qlm_candidates;
+
+typedef struct {
+    int64_t index;         /* winner's global candidate index (-1 if count == 0)     */
+    float s1, s2;          /* its objective (R11)                                    */
+    int32_t n_over;        /* #{groups with v > alpha}                               */
+    int32_t reserved;
+} qlm_best;
+
+/* ---- lifetime --------------------------------------------------------- */
+
+/* Validate, deep-copy and upload the problem, build the derived tables on
+ * the device (per-(d,g) W = n*mu/Theta and n*var/Theta^2, per-(d,m) tail),
+ * and synchronise.  `tabs` may be NULL (then every dist_id must be -1);
+ * `opt` may be NULL (defaults).  Errors: QLM_EINVAL (named field), QLM_ERANGE
+ * (T > 65535), QLM_ECUDA (no sm_100 device), QLM_ENOMEM.                     */
+QLM_API int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int32_t Q,
+               const qlm_profile *prof, const qlm_len_tables *tabs, const qlm_options *opt,
+               qlm_ctx **out);
+QLM_API void qlm_destroy(qlm_ctx *ctx);
+QLM_API const char *qlm_last_error(void);
+
+/* Replace all G group records (same G) from host memory: validated on the
+ * host, copied H2D on `stream` and the derived tables rebuilt there
+ * (asynchronous).  The host array must stay valid until the stream reaches
+ * the copy (pinned memory recommended).  A new request arriving in a group
+ * is this call.                                                */
+QLM_API int qlm_update_groups(qlm_ctx *ctx, const qlm_group *groups, void *stream);
+
+/* ---- the hot path -------------------------------------------------------- */
+
+/* Per-candidate scores (Gaussian): s1[k], s2[k] (device fp32 [count]) and
+ * optionally n_over[k] (device int32 [count], nullable) for candidate
+ * first + k.                                                                */
+QLM_API int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, float *s2,
+                        int32_t *n_over, void *stream);
+
+/* Argmin over the candidates on this device: writes one qlm_record to
+ * `rec` (device memory).  Asynchronous; no host sync.                       */
+QLM_API int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record *rec,
+                            void *stream);
+
+/* Lexicographic min over n device records (e.g. all-gathered from every
+ * rank) -> *out (device).  Asynchronous.                                    */
+QLM_API int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, qlm_record *out,
+                       void *stream);
+
+/* Synchronous convenience: argmin + decode of the winner into host arrays
+ * queue_of_group[G] / pos_of_group[G] (both nullable).                      */
+QLM_API int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
+                      int32_t *queue_of_group, int32_t *pos_of_group, void *stream);
+
+/* Bulk per-group estimates for every candidate (Eq. 2/3/10): device fp32
+ * [count][G] arrays, row k = candidate first + k, column = group id, each
+ * nullable:  wt_mean = expected waiting time (s), wt_std = sqrt(variance),
+ * viol = SLO-violation probability (R8, R9).                                */
+QLM_API int qlm_rwt_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean, float *wt_std,
+                     float *viol, void *stream);
+
+/* Monte-Carlo estimate (R13): samples trials [trial_first, trial_first +
+ * trial_count) of every group's total output tokens with Philox (key =
+ * mc_seed), walks each candidate's queues with the sampled work and writes
+ * counts[k][g] = #{trials with W_g > slo_g} (device uint32 [count][G],
+ * overwritten).  Needs length tables.  trial_first + trial_count <= 2^32.    */
+QLM_API int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
+                    int64_t trial_first, int64_t trial_count, uint32_t *counts, void *stream);
+
+/* Decode candidates into per-group queue index and position (x_{g,i,j} of
+ * Eq. 6): device int32 [count][G] each (nullable).                         */
+QLM_API int qlm_decode(qlm_ctx *ctx, const qlm_candidates *cand, int32_t *queue_of_group,
+               int32_t *pos_of_group, void *stream);
+
+/* Materialise candidate rows as uint16 tokens: device [count][T].          */
+QLM_API int qlm_rows(qlm_ctx *ctx, const qlm_candidates *cand, uint16_t *rows_out, void *stream);
+
+/* Validate EXPLICIT rows (Eq. 6 bijection); synchronous.  *n_bad = number
+ * of rows that are not permutations of 0..T-1.                              */
+QLM_API int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, void *stream);
+
+/* ---- introspection --------------------------------------------------------- */
+QLM_API int qlm_dims(const qlm_ctx *ctx, int32_t *G, int32_t *Q, int32_t *T, int32_t *D, int32_t *M);
+QLM_API int64_t qlm_kernel_launches(void);   /* kernels launched by this process so far */
+QLM_API int qlm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QLM_H */

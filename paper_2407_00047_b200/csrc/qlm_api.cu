@@ -1,0 +1,559 @@
+// qlm_api.cu -- the C ABI (include/qlm.h): validation, context, device memory,
+// argument marshalling to the kernels in qlm_kernels.cu.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qlm_launch.h"
+
+using namespace qlm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    return fail(QLM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool is_fin(double x) { return std::isfinite(x); }
+
+}  // namespace
+
+struct qlm_ctx {
+    int device = 0;
+    Dims dm{};
+    double z_clamp = 8.0, zc2 = 64.0;
+    float alpha = 0.01f;
+    bool has_tables = false;
+    // raw uploads (one allocation)
+    void *d_raw = nullptr;
+    qlm_group *d_groups = nullptr;
+    qlm_queue *d_queues = nullptr;
+    double *d_theta = nullptr, *d_prefill = nullptr, *d_eps = nullptr, *d_dec = nullptr,
+           *d_maxo = nullptr, *d_swap = nullptr;
+    // derived tables (one allocation)
+    void *d_tab = nullptr;
+    Tables tb{};
+    // scratch
+    qlm_record *d_block_recs = nullptr;
+    unsigned int *d_counter = nullptr;
+    qlm_record *d_rec = nullptr;           // sync best_ordering
+    int32_t *d_dec_out = nullptr;          // [2][G] sync decode
+    unsigned long long *d_bad = nullptr;
+    int max_blocks = 0;
+    uint32_t *d_X = nullptr;
+    size_t X_cap = 0;
+    uint16_t *d_rows = nullptr;
+    size_t rows_cap = 0;
+    std::vector<qlm_group> groups;
+    std::vector<qlm_queue> queues;
+    std::vector<double> prof;              // theta|prefill|eps|dec|maxo [D*M] each, swap [D*M*M]
+};
+
+namespace {
+
+size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+int validate_groups(const qlm_group *g, int G, int M, int n_tables) {
+    for (int i = 0; i < G; ++i) {
+        const qlm_group &x = g[i];
+        if (x.model < 0 || x.model >= M)
+            return fail(QLM_EINVAL, "groups[%d].model=%d not in [0,M=%d)", i, x.model, M);
+        if (x.n_req < 1) return fail(QLM_EINVAL, "groups[%d].n_req=%d must be >= 1", i, x.n_req);
+        if (!(x.slo_s > 0.0) || !is_fin(x.slo_s))
+            return fail(QLM_EINVAL, "groups[%d].slo_s=%g must be > 0 and finite", i, x.slo_s);
+        if (!(x.mu_out > 0.0) || !is_fin(x.mu_out))
+            return fail(QLM_EINVAL, "groups[%d].mu_out=%g must be > 0 and finite", i, x.mu_out);
+        if (!(x.var_out >= 0.0) || !is_fin(x.var_out))
+            return fail(QLM_EINVAL, "groups[%d].var_out=%g must be >= 0 and finite", i, x.var_out);
+        if (x.dist_id < -1 || x.dist_id >= n_tables)
+            return fail(QLM_EINVAL, "groups[%d].dist_id=%d not in [-1,n_tables=%d)", i, x.dist_id,
+                        n_tables);
+        if (x.dist_id >= 0 && x.n_req > 65536)
+            return fail(QLM_EINVAL, "groups[%d].n_req=%d > 65536 with a length table", i, x.n_req);
+        if (x.reserved != 0) return fail(QLM_EINVAL, "groups[%d].reserved must be 0", i);
+    }
+    return QLM_OK;
+}
+
+int check_dev(qlm_ctx *ctx) {
+    cudaError_t e = cudaSetDevice(ctx->device);
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "cudaSetDevice");
+}
+
+int check_cand(const qlm_ctx *ctx, const qlm_candidates *c) {
+    if (!c) return fail(QLM_EINVAL, "cand is NULL");
+    const int T = ctx->dm.T;
+    if (c->count < 0) return fail(QLM_EINVAL, "cand.count=%lld < 0", (long long)c->count);
+    if (c->first_from && c->count != 1)
+        return fail(QLM_EINVAL, "cand.first_from requires cand.count == 1");
+    switch (c->kind) {
+    case QLM_CAND_EXPLICIT:
+        if (c->token_bytes != 1 && c->token_bytes != 2)
+            return fail(QLM_EINVAL, "cand.token_bytes=%d must be 1 or 2", c->token_bytes);
+        if (c->token_bytes == 1 && T > 256)
+            return fail(QLM_EINVAL, "cand.token_bytes=1 needs T=%d <= 256", T);
+        if (c->count > 0 && !c->rows) return fail(QLM_EINVAL, "cand.rows is NULL");
+        if (((uintptr_t)c->rows & 15) != 0) return fail(QLM_EINVAL, "cand.rows not 16-B aligned");
+        if (c->stride % 16 != 0 || c->stride < (int64_t)T * c->token_bytes)
+            return fail(QLM_EINVAL, "cand.stride=%lld must be a multiple of 16 and >= T*token_bytes=%d",
+                        (long long)c->stride, T * c->token_bytes);
+        if (c->first_from) return fail(QLM_EINVAL, "cand.first_from not supported for EXPLICIT");
+        break;
+    case QLM_CAND_RANDOM:
+        if (c->first < 0) return fail(QLM_EINVAL, "cand.first=%lld < 0", (long long)c->first);
+        if (c->count > 0 && c->first > INT64_MAX - c->count)
+            return fail(QLM_ERANGE, "cand.first + cand.count overflows");
+        break;
+    case QLM_CAND_ENUM: {
+        if (T > 20) return fail(QLM_ERANGE, "ENUM needs T=%d <= 20", T);
+        uint64_t f = 1;
+        for (int k = 2; k <= T; ++k) f *= (uint64_t)k;
+        if (c->first < 0) return fail(QLM_EINVAL, "cand.first=%lld < 0", (long long)c->first);
+        if (!c->first_from && (uint64_t)c->first + (uint64_t)c->count > f)
+            return fail(QLM_ERANGE, "ENUM range [%lld, %lld) exceeds T!=%llu", (long long)c->first,
+                        (long long)(c->first + c->count), (unsigned long long)f);
+        break;
+    }
+    default:
+        return fail(QLM_EINVAL, "cand.kind=%d unknown", c->kind);
+    }
+    return QLM_OK;
+}
+
+Cand to_cand(const qlm_candidates *c) {
+    Cand d;
+    d.kind = c->kind;
+    d.tb = c->token_bytes;
+    d.rows = static_cast<const uint8_t *>(c->rows);
+    d.stride = c->stride;
+    d.seed = c->seed;
+    d.first = c->first;
+    d.count = c->count;
+    d.first_from = c->first_from;
+    return d;
+}
+
+ScanParams base_params(const qlm_ctx *ctx, const qlm_candidates *c) {
+    ScanParams p;
+    memset(&p, 0, sizeof p);
+    p.dm = ctx->dm;
+    p.tb = ctx->tb;
+    p.cd = to_cand(c);
+    p.block_recs = ctx->d_block_recs;
+    p.counter = ctx->d_counter;
+    p.max_blocks = ctx->max_blocks;
+    p.zc2 = ctx->zc2;
+    p.alpha = ctx->alpha;
+    return p;
+}
+
+int rebuild(qlm_ctx *ctx, cudaStream_t st) {
+    cudaError_t e = launch_build(ctx->dm, ctx->d_groups, ctx->d_queues, ctx->d_theta,
+                                 ctx->d_prefill, ctx->d_eps, ctx->d_dec, ctx->d_maxo, ctx->d_swap,
+                                 ctx->tb, st);
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "build_tables");
+}
+
+int ensure_rows(qlm_ctx *ctx, int64_t count) {
+    const size_t need = (size_t)count * ctx->dm.T * sizeof(uint16_t);
+    if (need <= ctx->rows_cap) return QLM_OK;
+    if (ctx->d_rows) cudaFree(ctx->d_rows);
+    ctx->d_rows = nullptr;
+    ctx->rows_cap = 0;
+    if (cudaMalloc(&ctx->d_rows, need) != cudaSuccess)
+        return fail(QLM_ENOMEM, "rows scratch of %zu bytes", need);
+    ctx->rows_cap = need;
+    return QLM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qlm_abi_version(void) { return QLM_ABI_VERSION; }
+
+const char *qlm_last_error(void) { return g_err.c_str(); }
+
+int64_t qlm_kernel_launches(void) { return g_launches.load(); }
+
+int qlm_dims(const qlm_ctx *ctx, int32_t *G, int32_t *Q, int32_t *T, int32_t *D, int32_t *M) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    if (G) *G = ctx->dm.G;
+    if (Q) *Q = ctx->dm.Q;
+    if (T) *T = ctx->dm.T;
+    if (D) *D = ctx->dm.D;
+    if (M) *M = ctx->dm.M;
+    return QLM_OK;
+}
+
+int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int32_t Q,
+               const qlm_profile *prof, const qlm_len_tables *tabs, const qlm_options *opt,
+               qlm_ctx **out) {
+    if (!out) return fail(QLM_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!groups || G < 1) return fail(QLM_EINVAL, "G=%d must be >= 1 with non-NULL groups", G);
+    if (!queues || Q < 1) return fail(QLM_EINVAL, "Q=%d must be >= 1 with non-NULL queues", Q);
+    if ((int64_t)G + Q - 1 > 65535) return fail(QLM_ERANGE, "T=G+Q-1=%lld > 65535", (long long)G + Q - 1);
+    if (!prof) return fail(QLM_EINVAL, "prof is NULL");
+    const int D = prof->D, M = prof->M;
+    if (D < 1 || M < 1 || D > 64 || M > 64)
+        return fail(QLM_EINVAL, "profile D=%d, M=%d must be in [1,64]", D, M);
+    const double *arr[6] = {prof->theta, prof->prefill_s, prof->eps, prof->decode_s, prof->max_out,
+                            prof->swap_s};
+    const char *names[6] = {"theta", "prefill_s", "eps", "decode_s", "max_out", "swap_s"};
+    for (int a = 0; a < 6; ++a)
+        if (!arr[a]) return fail(QLM_EINVAL, "prof.%s is NULL", names[a]);
+    for (int k = 0; k < D * M; ++k) {
+        const int d = k / M, m = k % M;
+        if (!(prof->theta[k] > 0.0) || !is_fin(prof->theta[k]))
+            return fail(QLM_EINVAL, "prof.theta[%d][%d]=%g must be > 0 and finite", d, m, prof->theta[k]);
+        if (!(prof->prefill_s[k] >= 0.0) || !is_fin(prof->prefill_s[k]))
+            return fail(QLM_EINVAL, "prof.prefill_s[%d][%d]=%g must be >= 0", d, m, prof->prefill_s[k]);
+        if (!(prof->eps[k] > 0.0) || !is_fin(prof->eps[k]))
+            return fail(QLM_EINVAL, "prof.eps[%d][%d]=%g must be > 0", d, m, prof->eps[k]);
+        if (!(prof->decode_s[k] >= 0.0) || !is_fin(prof->decode_s[k]))
+            return fail(QLM_EINVAL, "prof.decode_s[%d][%d]=%g must be >= 0", d, m, prof->decode_s[k]);
+        if (!(prof->max_out[k] >= 0.0) || !is_fin(prof->max_out[k]))
+            return fail(QLM_EINVAL, "prof.max_out[%d][%d]=%g must be >= 0", d, m, prof->max_out[k]);
+    }
+    for (int k = 0; k < D * M * M; ++k) {
+        const int d = k / (M * M), a = (k / M) % M, b = k % M;
+        const double s = prof->swap_s[k];
+        if (!(s >= 0.0) || !is_fin(s))
+            return fail(QLM_EINVAL, "prof.swap_s[%d][%d][%d]=%g must be >= 0 and finite", d, a, b, s);
+        if (a == b && s != 0.0)
+            return fail(QLM_EINVAL, "prof.swap_s[%d][%d][%d]=%g: diagonal must be 0", d, a, b, s);
+    }
+    int n_tables = 0, K = 0;
+    if (tabs) {
+        K = tabs->K;
+        n_tables = tabs->n_tables;
+        if (K < 2 || K > 65536 || (K & (K - 1)))
+            return fail(QLM_EINVAL, "tabs.K=%d must be a power of two in [2,65536]", K);
+        if (n_tables < 1 || !tabs->len)
+            return fail(QLM_EINVAL, "tabs.n_tables=%d must be >= 1 with non-NULL len", n_tables);
+    }
+    int rc = validate_groups(groups, G, M, n_tables);
+    if (rc) return rc;
+    for (int q = 0; q < Q; ++q) {
+        const qlm_queue &u = queues[q];
+        if (u.device < 0 || u.device >= D)
+            return fail(QLM_EINVAL, "queues[%d].device=%d not in [0,D=%d)", q, u.device, D);
+        if (u.resident_model < 0 || u.resident_model >= M)
+            return fail(QLM_EINVAL, "queues[%d].resident_model=%d not in [0,M=%d)", q,
+                        u.resident_model, M);
+        if (!(u.backlog_mean_s >= 0.0) || !is_fin(u.backlog_mean_s))
+            return fail(QLM_EINVAL, "queues[%d].backlog_mean_s=%g must be >= 0", q, u.backlog_mean_s);
+        if (!(u.backlog_var_s2 >= 0.0) || !is_fin(u.backlog_var_s2))
+            return fail(QLM_EINVAL, "queues[%d].backlog_var_s2=%g must be >= 0", q, u.backlog_var_s2);
+    }
+    double z_clamp = 8.0, alpha = 0.01;
+    int device = 0;
+    if (opt) {
+        z_clamp = opt->z_clamp;
+        alpha = opt->alpha;
+        device = opt->device;
+        if (!(z_clamp > 0.0) || !is_fin(z_clamp))
+            return fail(QLM_EINVAL, "opt.z_clamp=%g must be > 0", z_clamp);
+        if (!(alpha >= 0.0 && alpha < 1.0)) return fail(QLM_EINVAL, "opt.alpha=%g not in [0,1)", alpha);
+        if (opt->reserved != 0) return fail(QLM_EINVAL, "opt.reserved must be 0");
+    }
+    // device: must be sm_100 (no CPU fallback, no other arch path)
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) return fail(QLM_ECUDA, "no CUDA device (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(QLM_EINVAL, "opt.device=%d not in [0,%d)", device, ndev);
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(QLM_ECUDA, "device %d is sm_%d%d; libqlm is built for sm_100a only", device,
+                    prop.major, prop.minor);
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+
+    qlm_ctx *ctx = new qlm_ctx();
+    ctx->device = device;
+    ctx->dm.G = G; ctx->dm.Q = Q; ctx->dm.D = D; ctx->dm.M = M; ctx->dm.T = G + Q - 1;
+    ctx->dm.K = K; ctx->dm.n_tables = n_tables;
+    int lg = 0;
+    while ((1 << lg) < K) ++lg;
+    ctx->dm.shift = 32 - lg;
+    ctx->z_clamp = z_clamp;
+    ctx->zc2 = z_clamp * z_clamp;
+    ctx->alpha = (float)alpha;
+    ctx->has_tables = tabs != nullptr;
+    ctx->groups.assign(groups, groups + G);
+    ctx->queues.assign(queues, queues + Q);
+    const size_t DM = (size_t)D * M;
+    ctx->prof.resize(5 * DM + DM * M);
+    for (int a = 0; a < 5; ++a) memcpy(&ctx->prof[a * DM], arr[a], DM * sizeof(double));
+    memcpy(&ctx->prof[5 * DM], prof->swap_s, DM * M * sizeof(double));
+
+    // raw region
+    const size_t o_g = 0, o_q = a16(o_g + G * sizeof(qlm_group)),
+                 o_p = a16(o_q + Q * sizeof(qlm_queue)),
+                 raw_bytes = a16(o_p + ctx->prof.size() * sizeof(double));
+    // table region
+    const size_t t_grec = 0, t_ab = a16(t_grec + G * sizeof(GRec)),
+                 t_q = a16(t_ab + (size_t)D * G * sizeof(double2)),
+                 t_tail = a16(t_q + Q * sizeof(QRec)), t_swap = a16(t_tail + DM * 8),
+                 t_theta = a16(t_swap + DM * M * 8), t_dist = a16(t_theta + DM * 8),
+                 t_den = a16(t_dist + G * 4), t_len = a16(t_den + 8),
+                 tab_bytes = a16(t_len + (size_t)n_tables * K * 2);
+    ctx->max_blocks = sm_count() * 32;
+    if (cudaMalloc(&ctx->d_raw, raw_bytes) != cudaSuccess ||
+        cudaMalloc(&ctx->d_tab, tab_bytes) != cudaSuccess ||
+        cudaMalloc(&ctx->d_block_recs, ctx->max_blocks * sizeof(qlm_record)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_counter, 64) != cudaSuccess ||
+        cudaMalloc(&ctx->d_rec, 64) != cudaSuccess ||
+        cudaMalloc(&ctx->d_dec_out, 2 * (size_t)G * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_bad, 64) != cudaSuccess) {
+        qlm_destroy(ctx);
+        return fail(QLM_ENOMEM, "device allocation failed");
+    }
+    uint8_t *raw = static_cast<uint8_t *>(ctx->d_raw);
+    ctx->d_groups = reinterpret_cast<qlm_group *>(raw + o_g);
+    ctx->d_queues = reinterpret_cast<qlm_queue *>(raw + o_q);
+    double *pp = reinterpret_cast<double *>(raw + o_p);
+    ctx->d_theta = pp; ctx->d_prefill = pp + DM; ctx->d_eps = pp + 2 * DM; ctx->d_dec = pp + 3 * DM;
+    ctx->d_maxo = pp + 4 * DM; ctx->d_swap = pp + 5 * DM;
+    uint8_t *tab = static_cast<uint8_t *>(ctx->d_tab);
+    ctx->tb.grec = reinterpret_cast<GRec *>(tab + t_grec);
+    ctx->tb.ab = reinterpret_cast<double2 *>(tab + t_ab);
+    ctx->tb.qrec = reinterpret_cast<QRec *>(tab + t_q);
+    ctx->tb.tail = reinterpret_cast<double *>(tab + t_tail);
+    ctx->tb.swap = reinterpret_cast<double *>(tab + t_swap);
+    ctx->tb.theta = reinterpret_cast<double *>(tab + t_theta);
+    ctx->tb.dist = reinterpret_cast<int32_t *>(tab + t_dist);
+    ctx->tb.den = reinterpret_cast<double *>(tab + t_den);
+    ctx->tb.len = reinterpret_cast<uint16_t *>(tab + t_len);
+
+    if ((e = cudaMemcpy(ctx->d_groups, groups, G * sizeof(qlm_group), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(ctx->d_queues, queues, Q * sizeof(qlm_queue), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemcpy(pp, ctx->prof.data(), ctx->prof.size() * sizeof(double), cudaMemcpyHostToDevice)) ||
+        (e = cudaMemset(ctx->d_counter, 0, 64))) {
+        qlm_destroy(ctx);
+        return cuda_fail(e, "upload");
+    }
+    if (tabs && (e = cudaMemcpy(ctx->tb.len, tabs->len, (size_t)n_tables * K * 2, cudaMemcpyHostToDevice))) {
+        qlm_destroy(ctx);
+        return cuda_fail(e, "upload length tables");
+    }
+    rc = rebuild(ctx, nullptr);
+    if (!rc && (e = cudaDeviceSynchronize()) != cudaSuccess) rc = cuda_fail(e, "build_tables");
+    if (rc) {
+        qlm_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return QLM_OK;
+}
+
+void qlm_destroy(qlm_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    void *ptrs[] = {ctx->d_raw, ctx->d_tab, ctx->d_block_recs, ctx->d_counter, ctx->d_rec,
+                    ctx->d_dec_out, ctx->d_bad, ctx->d_X, ctx->d_rows};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    delete ctx;
+}
+
+int qlm_update_groups(qlm_ctx *ctx, const qlm_group *groups, void *stream) {
+    if (!ctx || !groups) return fail(QLM_EINVAL, "ctx or groups is NULL");
+    int rc = validate_groups(groups, ctx->dm.G, ctx->dm.M, ctx->dm.n_tables);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(ctx->d_groups, groups, ctx->dm.G * sizeof(qlm_group),
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "update_groups copy");
+    ctx->groups.assign(groups, groups + ctx->dm.G);
+    return rebuild(ctx, st);
+}
+
+int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, float *s2,
+                        int32_t *n_over, void *stream) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (cand->count > 0 && (!s1 || !s2)) return fail(QLM_EINVAL, "s1/s2 outputs are NULL");
+    if (cand->count == 0) return QLM_OK;
+    ScanParams p = base_params(ctx, cand);
+    p.s1 = s1; p.s2 = s2; p.n_over = n_over;
+    cudaError_t e = launch_score(p, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score kernel");
+}
+
+int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record *rec,
+                            void *stream) {
+    if (!ctx || !rec) return fail(QLM_EINVAL, "ctx or rec is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cand->count == 0) {
+        const qlm_record none = {~0ull, -1};
+        cudaError_t e = cudaMemcpyAsync(rec, &none, sizeof none, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e == cudaSuccess ? QLM_OK : cuda_fail(e, "empty record");
+    }
+    ScanParams p = base_params(ctx, cand);
+    p.out_rec = rec;
+    cudaError_t e = launch_score(p, st);
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score/argmin kernel");
+}
+
+int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, qlm_record *out,
+                       void *stream) {
+    if (!ctx || !recs || !out || n < 1) return fail(QLM_EINVAL, "reduce_records: bad arguments");
+    int rc = check_dev(ctx);
+    if (rc) return rc;
+    cudaError_t e = launch_reduce_records(recs, n, out, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "reduce_records");
+}
+
+int qlm_decode(qlm_ctx *ctx, const qlm_candidates *cand, int32_t *queue_of_group,
+               int32_t *pos_of_group, void *stream) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (cand->count == 0) return QLM_OK;
+    ScanParams p = base_params(ctx, cand);
+    cudaError_t e = launch_rows(p, nullptr, queue_of_group, pos_of_group,
+                                static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "decode kernel");
+}
+
+int qlm_rows(qlm_ctx *ctx, const qlm_candidates *cand, uint16_t *rows_out, void *stream) {
+    if (!ctx || !rows_out) return fail(QLM_EINVAL, "ctx or rows_out is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (cand->count == 0) return QLM_OK;
+    ScanParams p = base_params(ctx, cand);
+    cudaError_t e = launch_rows(p, rows_out, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "rows kernel");
+}
+
+int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
+                      int32_t *queue_of_group, int32_t *pos_of_group, void *stream) {
+    if (!ctx || !out) return fail(QLM_EINVAL, "ctx or out is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    memset(out, 0, sizeof *out);
+    out->index = -1;
+    if (cand->count == 0) return QLM_OK;
+    if ((rc = qlm_best_ordering_async(ctx, cand, ctx->d_rec, stream))) return rc;
+    qlm_record h;
+    cudaError_t e = cudaMemcpyAsync(&h, ctx->d_rec, sizeof h, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "best_ordering");
+    out->index = h.index;
+    if (h.index < 0) return QLM_OK;
+    // re-score and decode the winner on the device
+    qlm_candidates one = *cand;
+    one.first = h.index;
+    one.count = 1;
+    one.first_from = nullptr;
+    if (cand->kind == QLM_CAND_EXPLICIT)
+        one.rows = static_cast<const uint8_t *>(cand->rows) + (h.index - cand->first) * cand->stride;
+    float *d_s = reinterpret_cast<float *>(ctx->d_rec + 1);
+    int32_t *d_no = reinterpret_cast<int32_t *>(ctx->d_rec + 2);
+    if ((rc = qlm_score_orderings(ctx, &one, d_s, d_s + 1, d_no, stream))) return rc;
+    if ((rc = qlm_decode(ctx, &one, ctx->d_dec_out, ctx->d_dec_out + ctx->dm.G, stream))) return rc;
+    float s[2];
+    int32_t no = 0;
+    if ((e = cudaMemcpyAsync(s, d_s, sizeof s, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpyAsync(&no, d_no, sizeof no, cudaMemcpyDeviceToHost, st)) ||
+        (queue_of_group && (e = cudaMemcpyAsync(queue_of_group, ctx->d_dec_out,
+                                                ctx->dm.G * sizeof(int32_t), cudaMemcpyDeviceToHost, st))) ||
+        (pos_of_group && (e = cudaMemcpyAsync(pos_of_group, ctx->d_dec_out + ctx->dm.G,
+                                              ctx->dm.G * sizeof(int32_t), cudaMemcpyDeviceToHost, st))) ||
+        (e = cudaStreamSynchronize(st)))
+        return cuda_fail(e, "best_ordering readback");
+    out->s1 = s[0];
+    out->s2 = s[1];
+    out->n_over = no;
+    return QLM_OK;
+}
+
+int qlm_rwt_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean, float *wt_std,
+                     float *viol, void *stream) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (cand->count == 0 || (!wt_mean && !wt_std && !viol)) return QLM_OK;
+    ScanParams p = base_params(ctx, cand);
+    p.wt = wt_mean; p.sd = wt_std; p.vo = viol;
+    cudaError_t e = launch_bulk(p, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "bulk estimate kernel");
+}
+
+int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
+                    int64_t trial_first, int64_t trial_count, uint32_t *counts, void *stream) {
+    if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (!ctx->has_tables) return fail(QLM_EINVAL, "MC mode needs length tables at qlm_create");
+    for (int i = 0; i < ctx->dm.G; ++i)
+        if (ctx->groups[i].dist_id < 0)
+            return fail(QLM_EINVAL, "groups[%d].dist_id=-1: MC mode needs a length table", i);
+    if (trial_first < 0 || trial_count < 0 || trial_first + trial_count > (int64_t)1 << 32)
+        return fail(QLM_ERANGE, "trials [%lld, +%lld) must lie in [0, 2^32)", (long long)trial_first,
+                    (long long)trial_count);
+    if (cand->count > 65535) return fail(QLM_ERANGE, "MC: cand.count=%lld > 65535", (long long)cand->count);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (cand->count == 0) return QLM_OK;
+    if ((e = cudaMemsetAsync(counts, 0, (size_t)cand->count * ctx->dm.G * 4, st)) != cudaSuccess)
+        return cuda_fail(e, "counts memset");
+    if (trial_count == 0) return QLM_OK;
+    const size_t needX = (size_t)trial_count * ctx->dm.G * 4;
+    if (needX > ctx->X_cap) {
+        if (ctx->d_X) cudaFree(ctx->d_X);
+        ctx->d_X = nullptr;
+        ctx->X_cap = 0;
+        if (cudaMalloc(&ctx->d_X, needX) != cudaSuccess) return fail(QLM_ENOMEM, "MC scratch %zu B", needX);
+        ctx->X_cap = needX;
+    }
+    if ((rc = ensure_rows(ctx, cand->count))) return rc;
+    ScanParams p = base_params(ctx, cand);
+    if ((e = launch_rows(p, ctx->d_rows, nullptr, nullptr, st)) != cudaSuccess) return cuda_fail(e, "MC rows");
+    if ((e = launch_mc_sample(ctx->dm, ctx->tb, mc_seed, trial_first, trial_count, ctx->d_X, st)) != cudaSuccess)
+        return cuda_fail(e, "MC sample kernel");
+    if ((e = launch_mc_count(ctx->dm, ctx->tb, ctx->d_rows, cand->first_from, cand->count, ctx->d_X,
+                             trial_count, counts, st)) != cudaSuccess)
+        return cuda_fail(e, "MC count kernel");
+    return QLM_OK;
+}
+
+int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, void *stream) {
+    if (!ctx || !n_bad) return fail(QLM_EINVAL, "ctx or n_bad is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (cand->kind != QLM_CAND_EXPLICIT) { *n_bad = 0; return QLM_OK; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(ctx->d_bad, 0, 8, st);
+    if (e == cudaSuccess) e = launch_check_rows(to_cand(cand), ctx->dm.T, ctx->d_bad, st);
+    unsigned long long h = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, ctx->d_bad, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "check_rows");
+    *n_bad = (int64_t)h;
+    return QLM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,244 @@
+// qlm_device.cuh -- device data layout and primitives of libqlm (sm_100a).
+//
+// Shares nothing with oracle/: this is the product path.  Citations:
+// "P:Lx" = PAPER.md line x; R-numbers = readings in DESIGN.md.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qlm.h"
+
+namespace qlm {
+
+// ---- derived tables in HBM (built on the device by build_tables_kernel) ----
+// Per group, device-independent: deadline, request count, model (16 B).
+struct alignas(16) GRec {
+    double slo;     // slo_i (Eq. 8)
+    int32_t n;      // n_i
+    int32_t model;  // m_i (Eq. 7)
+};
+// Per queue (32 B): backlog (R12), device row, resident model (R4).
+struct alignas(16) QRec {
+    double bmean, bvar;
+    int32_t d, r, backlog, pad;
+};
+
+struct Dims {
+    int G, Q, D, M, T;      // T = G + Q - 1 tokens per row
+    int K, n_tables, shift; // MC tables; shift = 32 - log2(K)
+};
+
+struct Tables {             // device pointers, one allocation
+    GRec *grec;             // [G]
+    double2 *ab;            // [D][G]  {n mu / Theta, n var / Theta^2}  (Eq. 2/3)
+    QRec *qrec;             // [Q]
+    double *tail;           // [D][M]  P + max_out eps d  (Eq. 1/4, R3)
+    double *swap;           // [D][M][M]
+    double *theta;          // [D][M]
+    int32_t *dist;          // [G]
+    uint16_t *len;          // [n_tables][K]
+    double *den;            // [1] sum_i n_i
+};
+
+struct Cand {               // device view of qlm_candidates
+    int kind, tb;
+    const uint8_t *rows;
+    int64_t stride;
+    uint64_t seed;
+    int64_t first, count;
+    const qlm_record *first_from;
+};
+
+// ---- Philox4x32-10 (Salmon et al. SC'11) ------------------------------------
+__device__ __forceinline__ uint4 philox10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k.x += 0x9E3779B9u; k.y += 0xBB67AE85u; }
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint32_t pick4(uint4 w, int k) {
+    return k == 0 ? w.x : k == 1 ? w.y : k == 2 ? w.z : w.w;
+}
+
+// Candidate-row Philox stream (R10): key = seed, counter = (i/4, c_lo, c_hi, 'QLM\0').
+constexpr uint32_t kRowTag = 0x514C4D00u;
+// MC stream (R13): key = mc_seed, counter = (r/4, group, trial, 'MC\0\0').
+constexpr uint32_t kMcTag = 0x4D430000u;
+
+// ---- per-thread Fisher-Yates scratch in shared memory ----------------------
+// Element i of thread `tid` lives in 32-bit word (i / EPW) * blk + tid, byte
+// lane i % EPW: a warp touching any elements hits 32 distinct banks.
+template <typename TOK>
+__device__ __forceinline__ TOK *fy_elem(uint8_t *base, int i, int blk, int tid) {
+    constexpr int EPW = 4 / (int)sizeof(TOK);
+    return reinterpret_cast<TOK *>(base + ((size_t)((i / EPW) * blk + tid) << 2) +
+                                   (i % EPW) * sizeof(TOK));
+}
+
+// Forward Fisher-Yates over T tokens (R10); calls f(token) for positions
+// 0..T-1 in order, each as soon as it is final (fused generation + scan).
+template <typename TOK, typename F>
+__device__ __forceinline__ void tokens_random(uint8_t *scratch, int blk, int tid, int T,
+                                              uint64_t seed, uint64_t c, F &&f) {
+    constexpr int EPW = 4 / (int)sizeof(TOK);
+    uint32_t *w32 = reinterpret_cast<uint32_t *>(scratch);
+    const int nw = (T + EPW - 1) / EPW;
+    for (int w = 0; w < nw; ++w)
+        w32[w * blk + tid] = EPW == 4 ? 0x03020100u + 0x04040404u * (uint32_t)w
+                                      : 0x00010000u + 0x00020002u * (uint32_t)w;
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint32_t clo = (uint32_t)c, chi = (uint32_t)(c >> 32);
+    for (int i0 = 0; i0 < T; i0 += 4) {
+        uint4 wd = make_uint4(0u, 0u, 0u, 0u);
+        if (i0 < T - 1) wd = philox10(make_uint4((uint32_t)(i0 >> 2), clo, chi, kRowTag), key);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k;
+            if (i >= T) break;
+            TOK *pi = fy_elem<TOK>(scratch, i, blk, tid);
+            int tok;
+            if (i < T - 1) {
+                const int j = i + (int)__umulhi(pick4(wd, k), (uint32_t)(T - i));
+                TOK *pj = fy_elem<TOK>(scratch, j, blk, tid);
+                const TOK ti = *pi, tj = *pj;
+                *pj = ti;
+                tok = tj;
+            } else {
+                tok = *pi;
+            }
+            f(tok);
+        }
+    }
+}
+
+// EXPLICIT rows: 16-byte vector loads of the thread's own row.
+template <typename TOK, typename F>
+__device__ __forceinline__ void tokens_explicit(const uint8_t *row, int T, F &&f) {
+    constexpr int PER = 16 / (int)sizeof(TOK);
+    for (int s0 = 0; s0 < T; s0 += PER) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + (size_t)s0 * sizeof(TOK)));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            if (s0 + k >= T) break;
+            const int tok = sizeof(TOK) == 1 ? (int)((w[k >> 2] >> ((k & 3) * 8)) & 0xFFu)
+                                              : (int)((w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu);
+            f(tok);
+        }
+    }
+}
+
+// ENUM rows: Lehmer unranking in lexicographic order, T <= 20.
+template <typename F>
+__device__ __forceinline__ void tokens_enum(uint64_t c, int T, F &&f) {
+    uint32_t avail = T >= 32 ? 0xFFFFFFFFu : ((1u << T) - 1u);
+    uint64_t fact = 1;
+    for (int k = 2; k < T; ++k) fact *= (uint64_t)k;   // (T-1)!
+    for (int pos = 0; pos < T; ++pos) {
+        const int rem = T - 1 - pos;
+        const uint64_t k = c / fact;
+        c -= k * fact;
+        uint32_t a = avail;
+        for (uint64_t s = 0; s < k; ++s) a &= a - 1u;   // drop the k lowest available
+        const int tok = __ffs((int)a) - 1;
+        avail &= ~(1u << tok);
+        if (rem > 0) fact /= (uint64_t)rem;
+        f(tok);
+    }
+}
+
+// ---- one pass of the Eq. 2/3/10 recurrence over a row (R1-R7, R12) ---------
+// Tables are read from shared memory, replicated REP times and interleaved
+// so that lane l reads copy l % REP (REP = 8 makes 16-B reads conflict-free).
+template <int REP>
+struct Walker {
+    const GRec *sgrec;     // [G * REP]
+    const double2 *sab;    // [D * G * REP]
+    const QRec *sq;        // [Q]
+    const double *stail;   // [D * M]
+    const double *sswap;   // [D * M * M]
+    int G, Q, M, lrep;
+    double A, B;           // exclusive mean / variance accumulators
+    int q, d, prev, first, backlog;
+
+    __device__ __forceinline__ void start_queue(int qq) {
+        const QRec r = sq[qq];
+        A = r.bmean; B = r.bvar; d = r.d; prev = r.r; backlog = r.backlog; first = 1; q = qq;
+    }
+    // Returns false for a queue separator.  Otherwise (wt, V) of the group.
+    __device__ __forceinline__ bool step(int tok, double &wt, double &V, GRec &g) {
+        if (tok >= G) {                                   // separator: next queue
+            start_queue(q + 1 < Q ? q + 1 : Q - 1);
+            return false;
+        }
+        g = sgrec[tok * REP + lrep];
+        const double2 ab = sab[(d * G + tok) * REP + lrep];
+        const int m = g.model;
+        if (m != prev) {                                  // t = 1 (Eq. 9)
+            const double t = (first && !backlog) ? 0.0 : stail[d * M + prev];
+            A = __dadd_rn(A, t);                          // C - W of the group ahead (R1)
+            A = __dadd_rn(A, sswap[(d * M + prev) * M + m]);   // swap S (R2)
+        }
+        wt = A; V = B;                                    // exclusive (R5)
+        A = __dadd_rn(A, ab.x);
+        B = __dadd_rn(B, ab.y);
+        prev = m; first = 0;
+        return true;
+    }
+};
+
+// Violation probability (R8/R9): P(N(wt, V) > slo) = Phi-bar(slack / sqrt V),
+// 0/1 beyond |z| >= z_clamp (tested as slack^2 >= z_clamp^2 V, exact for V = 0).
+__device__ __forceinline__ float violation(double slack, double V, double zc2) {
+    const double c = fma(slack, slack, -zc2 * V);
+    if (c >= 0.0) return slack < 0.0 ? 1.0f : 0.0f;
+    const float z = (float)(slack * rsqrt(V));
+    return normcdff(-z);
+}
+
+__device__ __forceinline__ uint64_t make_key(float s1, float s2) {
+    s2 = s2 + 0.0f;                                       // -0 -> +0
+    uint32_t b2 = __float_as_uint(s2);
+    b2 = (b2 & 0x80000000u) ? ~b2 : (b2 | 0x80000000u);
+    return ((uint64_t)__float_as_uint(s1) << 32) | b2;
+}
+
+__device__ __forceinline__ bool better(uint64_t k1, int64_t i1, uint64_t k2, int64_t i2) {
+    return k1 < k2 || (k1 == k2 && (uint64_t)i1 < (uint64_t)i2);
+}
+
+__device__ __forceinline__ void warp_argmin(uint64_t &key, int64_t &idx) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(0xFFFFFFFFu, key, o);
+        const int64_t i2 = __shfl_xor_sync(0xFFFFFFFFu, idx, o);
+        if (better(k2, i2, key, idx)) { key = k2; idx = i2; }
+    }
+}
+
+// ---- bulk async copies (TMA engine, no tensor map) ----------------------------
+__device__ __forceinline__ void bulk_s2g(void *gdst, const void *ssrc, uint32_t bytes) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(gdst), "r"(s), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+}  // namespace qlm

@@ -1,0 +1,49 @@
+// qlm_launch.h -- launchers shared by qlm_api.cu and qlm_kernels.cu (internal).
+#pragma once
+
+#include <atomic>
+
+#include "qlm_device.cuh"
+
+namespace qlm {
+
+struct ScanParams {
+    Dims dm;
+    Tables tb;
+    Cand cd;
+    float *s1, *s2;            // score outputs [count] (nullable)
+    int32_t *n_over;
+    float *wt, *sd, *vo;       // bulk outputs [count][G] (nullable)
+    qlm_record *block_recs;    // [max_blocks] argmin scratch
+    unsigned int *counter;     // last-block ticket
+    qlm_record *out_rec;       // argmin result (nullable = no argmin)
+    int max_blocks;
+    double zc2;                // z_clamp^2
+    float alpha;
+    int blk;
+    int use_tma;
+    int off_grec, off_ab, off_q, off_tail, off_swap, off_scratch;
+    int off_stage_w, off_stage_s, off_stage_v;
+};
+
+extern std::atomic<int64_t> g_launches;
+int sm_count();
+
+cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
+                         const double *theta, const double *prefill, const double *eps,
+                         const double *dec, const double *maxo, const double *swp,
+                         const Tables &tb, cudaStream_t st);
+cudaError_t launch_score(const ScanParams &p, cudaStream_t st);
+cudaError_t launch_bulk(const ScanParams &p, cudaStream_t st);
+cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,
+                        cudaStream_t st);
+cudaError_t launch_reduce_records(const qlm_record *recs, int n, qlm_record *out,
+                                  cudaStream_t st);
+cudaError_t launch_check_rows(const Cand &cd, int T, unsigned long long *n_bad, cudaStream_t st);
+cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, int64_t t0,
+                             int64_t nt, uint32_t *X, cudaStream_t st);
+cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const uint16_t *rows,
+                            const qlm_record *first_from, int64_t count, const uint32_t *X,
+                            int64_t nt, uint32_t *counts, cudaStream_t st);
+
+}  // namespace qlm

@@ -1,0 +1,44 @@
+"""Data-parallel sharding of candidates and the cross-rank min-loc (a8, a12).
+
+Candidates are independent units: rank r of W scores the contiguous global
+index range shard_range(N, r, W) (weak scaling when every rank takes its own
+N).  The only exchange is the argmin: every rank all-gathers the W 16-byte
+best records (one NCCL call over NVLink) and reduces them with the
+lexicographic (key, index) rule -- on the GPU with qlm_reduce_records.  MC
+counts are summed with one all_reduce.  torch.distributed is plumbing only.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [first, first+count) of `total` candidates for `rank`."""
+    base, extra = divmod(total, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+def gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather each rank's int64[2] record -> int64[world*2] (same device)."""
+    world = dist.get_world_size(group)
+    out = torch.empty(world * 2, dtype=rec.dtype, device=rec.device)
+    dist.all_gather_into_tensor(out, rec.contiguous(), group=group)
+    return out
+
+
+def global_best(rec: torch.Tensor, reduce, group=None) -> torch.Tensor:
+    """Global min-loc: gather all ranks' records, then `reduce(records)`.
+
+    `reduce` is RwtEstimator.reduce_records on the GPU path.
+    """
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return rec
+    return reduce(gather_records(rec, group))
+
+
+def sum_counts(counts: torch.Tensor, group=None) -> torch.Tensor:
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    return counts

@@ -1,0 +1,213 @@
+"""Python binding of libqlm: bulk RWT estimation over candidate queue orderings.
+
+Thin marshalling over include/qlm.h -- every step of the path runs in the
+CUDA kernels of csrc/.  torch provides device memory and streams only.
+
+    est = RwtEstimator(problem, device=0)          # qlm_create (a0)
+    cand = est.random(first=0, count=10**6, seed=1)
+    best = est.best_ordering(cand)                  # a1-a5, a7, a9
+    wt, sd, v = est.rwt_estimate(cand)              # a6 bulk per-(candidate, group)
+    counts = est.mc_estimate(est.from_record(rec), mc_seed=2, trials=1221)   # a10-a11
+
+Citations: PAPER.md Sec. 6 (RWT estimator, L564-664) and Sec. 7 (global
+scheduler objective, L665-767); readings R1-R14 in DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+@dataclasses.dataclass
+class Cand:
+    """A set of candidate orderings (qlm_candidates, R10)."""
+    kind: int
+    first: int = 0
+    count: int = 0
+    seed: int = 0
+    rows: torch.Tensor | None = None        # EXPLICIT: uint8/int16 device [count, stride]
+    first_from: torch.Tensor | None = None  # device record (int64[2]); count must be 1
+
+    def c(self) -> L.Candidates:
+        tb, stride, rows = 1, 0, None
+        if self.kind == L.CAND_EXPLICIT:
+            r = self.rows
+            tb = r.element_size()
+            stride = r.stride(0) * tb
+            rows = r.data_ptr()
+        ff = None if self.first_from is None else self.first_from.data_ptr()
+        return L.Candidates(self.kind, tb, rows, stride, self.seed, self.first, self.count, ff)
+
+
+def groups_array(model, n_req, slo, mu, var, dist=None) -> np.ndarray:
+    G = len(model)
+    g = np.zeros(G, L.GROUP_DTYPE)
+    g["model"], g["n_req"], g["slo_s"], g["mu_out"], g["var_out"] = model, n_req, slo, mu, var
+    g["dist_id"] = -1 if dist is None else dist
+    return g
+
+
+def queues_array(device, resident, backlog_mean=None, backlog_var=None) -> np.ndarray:
+    Q = len(device)
+    q = np.zeros(Q, L.QUEUE_DTYPE)
+    q["device"], q["resident_model"] = device, resident
+    q["backlog_mean_s"] = 0.0 if backlog_mean is None else backlog_mean
+    q["backlog_var_s2"] = 0.0 if backlog_var is None else backlog_var
+    return q
+
+
+class RwtEstimator:
+    """One qlm_ctx: a scheduling problem resident on one sm_100a GPU."""
+
+    def __init__(self, problem, device: int = 0, z_clamp: float = 8.0, alpha: float = 0.01,
+                 with_tables: bool | None = None):
+        p = problem
+        self.device = torch.device("cuda", device)
+        self.groups = groups_array(p.model, p.n_req, p.slo, p.mu, p.var, p.dist)
+        self.queues = queues_array(p.q_device, p.q_resident, p.q_backlog_mean, p.q_backlog_var)
+        c = np.ascontiguousarray
+        self._prof_arrays = [c(a, np.float64) for a in
+                             (p.theta, p.prefill, p.eps, p.dtok, p.max_out, p.swap)]
+        D, M = self._prof_arrays[0].shape
+        prof = L.Profile(D, M, *[a.ctypes.data for a in self._prof_arrays])
+        tabs = None
+        use_tabs = p.len_tables is not None if with_tables is None else with_tables
+        if use_tabs:
+            self._len = c(p.len_tables, np.uint16)
+            tabs = L.LenTables(self._len.shape[1], self._len.shape[0], self._len.ctypes.data)
+        else:
+            self.groups["dist_id"] = -1
+        opt = L.Options(z_clamp, alpha, device, 0)
+        h = C.c_void_p()
+        L.check(L.lib().qlm_create(self.groups.ctypes.data, len(self.groups),
+                                   self.queues.ctypes.data, len(self.queues), C.byref(prof),
+                                   C.byref(tabs) if tabs is not None else None, C.byref(opt),
+                                   C.byref(h)), "qlm_create")
+        self._h = h
+        self.G, self.Q, self.D, self.M = len(self.groups), len(self.queues), D, M
+        self.T = self.G + self.Q - 1
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib().qlm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- helpers --------------------------------------------------------------
+    def _stream(self, stream):
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        return C.c_void_p(s.cuda_stream)
+
+    def _empty(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def random(self, first: int, count: int, seed: int) -> Cand:
+        return Cand(L.CAND_RANDOM, first, count, seed)
+
+    def enum(self, first: int, count: int) -> Cand:
+        return Cand(L.CAND_ENUM, first, count)
+
+    def explicit(self, rows: torch.Tensor, first: int = 0) -> Cand:
+        """rows: device uint8 (T <= 256) or int16 tensor [count, >= T], row stride a multiple of 16 B."""
+        return Cand(L.CAND_EXPLICIT, first, rows.shape[0], rows=rows)
+
+    def from_record(self, rec: torch.Tensor, kind: int = L.CAND_RANDOM, seed: int = 0) -> Cand:
+        """The single candidate named by a device record (no host sync)."""
+        return Cand(kind, 0, 1, seed, first_from=rec)
+
+    # -- hot path -------------------------------------------------------------
+    def update_groups(self, groups: np.ndarray | torch.Tensor, stream=None):
+        ptr = groups.data_ptr() if isinstance(groups, torch.Tensor) else groups.ctypes.data
+        L.check(L.lib().qlm_update_groups(self._h, C.c_void_p(ptr), self._stream(stream)),
+                "qlm_update_groups")
+
+    def score_orderings(self, cand: Cand, with_n_over: bool = True, stream=None):
+        s1 = self._empty(cand.count, torch.float32)
+        s2 = self._empty(cand.count, torch.float32)
+        no = self._empty(cand.count, torch.int32) if with_n_over else None
+        L.check(L.lib().qlm_score_orderings(self._h, C.byref(cand.c()), s1.data_ptr(), s2.data_ptr(),
+                                            None if no is None else no.data_ptr(),
+                                            self._stream(stream)), "qlm_score_orderings")
+        return s1, s2, no
+
+    def best_ordering_async(self, cand: Cand, rec: torch.Tensor | None = None, stream=None):
+        """Device record int64[2] = (key as int64 bits, global index)."""
+        rec = self._empty(2, torch.int64) if rec is None else rec
+        L.check(L.lib().qlm_best_ordering_async(self._h, C.byref(cand.c()), rec.data_ptr(),
+                                                self._stream(stream)), "qlm_best_ordering_async")
+        return rec
+
+    def reduce_records(self, recs: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        out = self._empty(2, torch.int64) if out is None else out
+        n = recs.numel() // 2
+        L.check(L.lib().qlm_reduce_records(self._h, recs.data_ptr(), n, out.data_ptr(),
+                                           self._stream(stream)), "qlm_reduce_records")
+        return out
+
+    def best_ordering(self, cand: Cand, stream=None) -> dict:
+        b = L.Best()
+        qo = np.zeros(self.G, np.int32)
+        po = np.zeros(self.G, np.int32)
+        L.check(L.lib().qlm_best_ordering(self._h, C.byref(cand.c()), C.byref(b), qo.ctypes.data,
+                                          po.ctypes.data, self._stream(stream)), "qlm_best_ordering")
+        return dict(index=b.index, s1=b.s1, s2=b.s2, n_over=b.n_over, queue_of_group=qo,
+                    pos_of_group=po)
+
+    def rwt_estimate(self, cand: Cand, want=("wt", "sd", "v"), out=None, stream=None):
+        """Per-(candidate, group) expected wait, its std and violation probability, [count, G]."""
+        if out is None:
+            out = {k: self._empty((cand.count, self.G), torch.float32) for k in want}
+        ptr = {k: (out[k].data_ptr() if k in out else None) for k in ("wt", "sd", "v")}
+        L.check(L.lib().qlm_rwt_estimate(self._h, C.byref(cand.c()), ptr["wt"], ptr["sd"], ptr["v"],
+                                         self._stream(stream)), "qlm_rwt_estimate")
+        return out
+
+    def mc_estimate(self, cand: Cand, mc_seed: int, trials: int, trial_first: int = 0,
+                    counts: torch.Tensor | None = None, stream=None):
+        """counts[k, g] = #{trials t: sampled W_g > slo_g} (uint32 stored as int32)."""
+        counts = self._empty((cand.count, self.G), torch.int32) if counts is None else counts
+        L.check(L.lib().qlm_mc_estimate(self._h, C.byref(cand.c()), mc_seed, trial_first, trials,
+                                        counts.data_ptr(), self._stream(stream)), "qlm_mc_estimate")
+        return counts
+
+    def decode(self, cand: Cand, stream=None):
+        qo = self._empty((cand.count, self.G), torch.int32)
+        po = self._empty((cand.count, self.G), torch.int32)
+        L.check(L.lib().qlm_decode(self._h, C.byref(cand.c()), qo.data_ptr(), po.data_ptr(),
+                                   self._stream(stream)), "qlm_decode")
+        return qo, po
+
+    def rows(self, cand: Cand, stream=None) -> torch.Tensor:
+        r = self._empty((cand.count, self.T), torch.int16)
+        L.check(L.lib().qlm_rows(self._h, C.byref(cand.c()), r.data_ptr(), self._stream(stream)),
+                "qlm_rows")
+        return r
+
+    def check_rows(self, cand: Cand, stream=None) -> int:
+        n = C.c_int64()
+        L.check(L.lib().qlm_check_rows(self._h, C.byref(cand.c()), C.byref(n), self._stream(stream)),
+                "qlm_check_rows")
+        return n.value
+
+
+def kernel_launches() -> int:
+    return int(L.lib().qlm_kernel_launches())
+
+
+def decode_key(key: int) -> tuple[float, float]:
+    """(fp32 S1, fp32 S2) from a record key (inverse of the kernel's packing)."""
+    key &= (1 << 64) - 1
+    b1 = np.uint32(key >> 32)
+    b2 = np.uint32(key & 0xFFFFFFFF)
+    b2 = np.uint32(b2 ^ 0x80000000) if b2 & 0x80000000 else np.uint32(~b2 & 0xFFFFFFFF)
+    return float(b1.view(np.float32)), float(b2.view(np.float32))

@@ -1,0 +1,156 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol
+include/qlm.h declares, the ctypes/numpy struct mirrors match the C layout,
+and host-side validation rejects bad inputs with a message naming the field
+(validation runs before any CUDA call, so no GPU is touched)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2407_00047_b200 import _lib as L
+from paper_2407_00047_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "qlm.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return L.lib()
+
+
+def declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"QLM_API\s+[\w\s\*]+?\b(qlm_\w+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared()
+    assert len(names) >= 15
+    out = subprocess.check_output(["nm", "-D", "--defined-only", L.LIB_PATH], text=True)
+    exported = set(re.findall(r" T (qlm_\w+)", out))
+    assert set(names) <= exported, set(names) - exported
+    assert set(names) == set(L.SIGNATURES), "ctypes signatures out of sync with qlm.h"
+    for n in names:
+        assert hasattr(lib, n)
+    # nothing but the ABI is exported
+    assert exported == set(names)
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.check_output(["cuobjdump", "--list-elf", L.LIB_PATH], text=True)
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_struct_layout_matches_c(tmp_path):
+    probe = tmp_path / "probe.c"
+    probe.write_text(r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "qlm.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(qlm_group), sizeof(qlm_queue),
+         sizeof(qlm_profile), sizeof(qlm_len_tables), sizeof(qlm_options), sizeof(qlm_record),
+         sizeof(qlm_candidates), sizeof(qlm_best));
+  printf("%zu %zu %zu %zu %zu\n", offsetof(qlm_group, slo_s), offsetof(qlm_group, dist_id),
+         offsetof(qlm_queue, backlog_mean_s), offsetof(qlm_candidates, first_from),
+         offsetof(qlm_candidates, seed));
+  return 0;
+}''')
+    exe = tmp_path / "probe"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(probe), "-o", str(exe)])
+    a, b = subprocess.check_output([str(exe)], text=True).strip().split("\n")
+    sizes = [int(x) for x in a.split()]
+    assert sizes == [L.GROUP_DTYPE.itemsize, L.QUEUE_DTYPE.itemsize, C.sizeof(L.Profile),
+                     C.sizeof(L.LenTables), C.sizeof(L.Options), C.sizeof(L.Record),
+                     C.sizeof(L.Candidates), C.sizeof(L.Best)]
+    offs = [int(x) for x in b.split()]
+    assert offs == [L.GROUP_DTYPE.fields["slo_s"][1], L.GROUP_DTYPE.fields["dist_id"][1],
+                    L.QUEUE_DTYPE.fields["backlog_mean_s"][1], L.Candidates.first_from.offset,
+                    L.Candidates.seed.offset]
+
+
+def _create(lib, groups, queues, D=1, M=1, theta=1000.0, swap_diag=0.0, K=None, opt=None):
+    arrs = [np.full((D, M), theta), np.full((D, M), 0.5), np.full((D, M), 1.2),
+            np.full((D, M), 0.025), np.full((D, M), 2048.0)]
+    sw = np.zeros((D, M, M))
+    sw[0, 0, 0] = swap_diag
+    arrs.append(sw)
+    prof = L.Profile(D, M, *[a.ctypes.data for a in arrs])
+    tabs = None
+    if K is not None:
+        t = np.ones((1, max(K, 1)), np.uint16)
+        tabs = L.LenTables(K, 1, t.ctypes.data)
+    h = C.c_void_p()
+    rc = lib.qlm_create(groups.ctypes.data if groups is not None else None,
+                        0 if groups is None else len(groups), queues.ctypes.data, len(queues),
+                        C.byref(prof), C.byref(tabs) if tabs else None,
+                        C.byref(opt) if opt else None, C.byref(h))
+    return rc, lib.qlm_last_error().decode()
+
+
+def _good():
+    g = np.zeros(3, L.GROUP_DTYPE)
+    g["n_req"], g["slo_s"], g["mu_out"], g["var_out"], g["dist_id"] = 4, 20.0, 100.0, 50.0, -1
+    q = np.zeros(2, L.QUEUE_DTYPE)
+    return g, q
+
+
+@pytest.mark.parametrize("field,value,needle", [
+    ("model", 3, "groups[1].model=3"),
+    ("n_req", 0, "groups[1].n_req=0"),
+    ("slo_s", 0.0, "groups[1].slo_s"),
+    ("slo_s", np.inf, "groups[1].slo_s"),
+    ("mu_out", -1.0, "groups[1].mu_out"),
+    ("var_out", np.nan, "groups[1].var_out"),
+    ("dist_id", 0, "groups[1].dist_id=0"),
+    ("reserved", 1, "groups[1].reserved"),
+])
+def test_group_validation_names_field(lib, field, value, needle):
+    g, q = _good()
+    g[field][1] = value
+    rc, msg = _create(lib, g, q)
+    assert rc == L.QLM_EINVAL and needle in msg
+
+
+def test_queue_and_profile_validation(lib):
+    g, q = _good()
+    q["device"][1] = 2
+    rc, msg = _create(lib, g, q)
+    assert rc == L.QLM_EINVAL and "queues[1].device=2" in msg
+    g, q = _good()
+    q["resident_model"][0] = -1
+    rc, msg = _create(lib, g, q)
+    assert rc == L.QLM_EINVAL and "queues[0].resident_model" in msg
+    g, q = _good()
+    q["backlog_mean_s"][1] = -3.0
+    rc, msg = _create(lib, g, q)
+    assert rc == L.QLM_EINVAL and "backlog_mean_s" in msg
+    g, q = _good()
+    rc, msg = _create(lib, g, q, theta=0.0)
+    assert rc == L.QLM_EINVAL and "theta[0][0]" in msg
+    rc, msg = _create(lib, g, q, swap_diag=1.5)
+    assert rc == L.QLM_EINVAL and "swap_s[0][0][0]" in msg and "diagonal" in msg
+    rc, msg = _create(lib, None, q)
+    assert rc == L.QLM_EINVAL and "G=0" in msg
+    rc, msg = _create(lib, g, q, K=3)
+    assert rc == L.QLM_EINVAL and "tabs.K=3" in msg
+    rc, msg = _create(lib, g, q, opt=L.Options(-1.0, 0.01, 0, 0))
+    assert rc == L.QLM_EINVAL and "z_clamp" in msg
+    big = np.zeros(70000, L.GROUP_DTYPE)
+    rc, msg = _create(lib, big, q)
+    assert rc == L.QLM_ERANGE and "65535" in msg
+
+
+def test_null_context_calls_fail_cleanly(lib):
+    cand = L.Candidates(L.CAND_RANDOM, 1, None, 0, 1, 0, 10, None)
+    assert lib.qlm_score_orderings(None, C.byref(cand), None, None, None, None) == L.QLM_EINVAL
+    assert lib.qlm_rwt_estimate(None, C.byref(cand), None, None, None, None) == L.QLM_EINVAL
+    assert lib.qlm_dims(None, None, None, None, None, None) == L.QLM_EINVAL
+    lib.qlm_destroy(None)
+    assert lib.qlm_abi_version() == 1

@@ -1,0 +1,304 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element
+by element on the same seeded inputs.  Tolerances: tests/parity.py."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle as O
+from tests.parity import argmin_ok, check_estimates, check_scores
+from workloads.synth import (balanced_row, make_config, make_problem, make_random_problem)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def est_of(p, **kw):
+    from paper_2407_00047_b200 import RwtEstimator
+    return RwtEstimator(p, device=0, **kw)
+
+
+def rows_tensor(rows_np, stride_bytes=None, token_bytes=1):
+    n, T = rows_np.shape
+    stride = stride_bytes or (-(-T * token_bytes // 16) * 16)
+    dt = np.uint8 if token_bytes == 1 else np.int16
+    buf = np.zeros((n, stride // token_bytes), dt)
+    buf[:, :T] = rows_np
+    return torch.tensor(buf, device="cuda")
+
+
+# ------------------------------------------------------------------ rows / generators
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C5"])
+def test_random_rows_bit_exact(cfg):
+    p = make_config(cfg)
+    e = est_of(p)
+    for first in [0, 12345, 2**33 + 5]:
+        n = 200
+        r = e.rows(e.random(first, n, seed=1)).cpu().numpy().astype(np.int64) & 0xFFFF
+        for k in range(0, n, 17):
+            np.testing.assert_array_equal(r[k], O.random_row(1, first + k, p.T))
+
+
+def test_enum_rows_bit_exact():
+    p = make_config("C1")
+    e = est_of(p)
+    r = e.rows(e.enum(0, 24)).cpu().numpy()
+    for c in range(24):
+        np.testing.assert_array_equal(r[c], O.enum_row(c, 4))
+    p6 = make_problem(6, 3, name="t8")    # T = 8: 40320 rows
+    e6 = est_of(p6)
+    r = e6.rows(e6.enum(40000, 320)).cpu().numpy()
+    for k in range(0, 320, 7):
+        np.testing.assert_array_equal(r[k], O.enum_row(40000 + k, p6.T))
+
+
+# ------------------------------------------------------------------ scores
+def test_c1_golden_exhaustive():
+    p = make_config("C1")
+    e = est_of(p)
+    s1, s2, no = e.score_orderings(e.enum(0, 24))
+    o = O.Oracle(p)
+    ref = o.score_range(O.ENUM, 0, 24)
+    check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)
+    assert np.array_equal(no.cpu().numpy(), ref["n_over"])
+    best = e.best_ordering(e.enum(0, 24))
+    assert best["index"] == 12                      # tests/golden/p7_c1.json
+    assert best["s1"] == 0.0 and best["s2"] == -42.0
+    dec = o.estimate(O.enum_row(12, 4))
+    assert np.array_equal(best["queue_of_group"], dec["queue"])
+    assert np.array_equal(best["pos_of_group"], dec["pos"])
+
+
+@pytest.mark.parametrize("cfg,n", [("C1r", 24), ("C2", 100_000), ("C3", 50_000)])
+def test_scores_random(cfg, n):
+    p = make_config(cfg)
+    e = est_of(p)
+    kind = O.ENUM if cfg == "C1r" else O.RANDOM
+    cand = e.enum(0, n) if kind == O.ENUM else e.random(0, n, seed=1)
+    s1, s2, no = e.score_orderings(cand)
+    ref = O.Oracle(p).score_range(kind, 0, n, seed=1)
+    check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)
+    no = no.cpu().numpy()
+    # n_over is an integer decided by floats: equal except where some v is within 1e-5 of alpha
+    assert np.mean(no == ref["n_over"]) > 0.999
+    assert np.all(np.abs(no - ref["n_over"]) <= 1)
+    best = e.best_ordering(cand)
+    ok, cstar = argmin_ok(best["index"], ref["s1"], ref["s2"], p)
+    assert ok, (best, cstar)
+    # reported scores of the chosen index match the oracle's re-evaluation
+    i = best["index"]
+    assert abs(best["s1"] - ref["s1"][i]) <= 1e-5
+    dec = O.Oracle(p).estimate(O.random_row(1, i, p.T) if kind == O.RANDOM else O.enum_row(i, p.T))
+    assert np.array_equal(best["queue_of_group"], dec["queue"])
+    assert np.array_equal(best["pos_of_group"], dec["pos"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_scores_random_problems(seed):
+    rng = np.random.default_rng(seed)
+    G = int(rng.integers(1, 200))
+    Q = int(rng.integers(1, 12))
+    M = int(rng.integers(1, 5))
+    D = int(rng.integers(1, 3))
+    p = make_random_problem(rng, G, Q, M, D, sigma_zero=bool(seed % 3 == 2), backlog=bool(seed % 2))
+    e = est_of(p)
+    n = 3000 + seed * 37                      # ragged vs block size
+    first = int(rng.integers(0, 2**40))
+    s1, s2, _ = e.score_orderings(e.random(first, n, seed=seed + 7))
+    ref = O.Oracle(p).score_range(O.RANDOM, first, n, seed=seed + 7)
+    check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)
+    out = e.rwt_estimate(e.random(first, 700, seed=seed + 7))
+    check_estimates(out, O.Oracle(p).estimate_range(O.RANDOM, first, 700, seed=seed + 7))
+
+
+def test_explicit_rows_u8_u16_and_padding():
+    p = make_config("C3")
+    o = O.Oracle(p)
+    n = 3001
+    rows = np.stack([O.random_row(9, c, p.T) for c in range(n)])
+    ref = o.score_range(O.EXPLICIT, 0, n, rows=rows.astype(np.uint8))
+    e = est_of(p)
+    for tb, stride in [(1, 80), (1, 112), (2, 144), (2, 256)]:
+        rt = rows_tensor(rows, stride, tb)
+        s1, s2, _ = e.score_orderings(e.explicit(rt))
+        check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)
+        assert e.check_rows(e.explicit(rt)) == 0
+    out = e.rwt_estimate(e.explicit(rows_tensor(rows[:500])))
+    check_estimates(out, o.estimate_range(O.EXPLICIT, 0, 500, rows=rows[:500].astype(np.uint8)))
+
+
+def test_check_rows_detects_bad_rows():
+    p = make_config("C2")
+    rows = np.stack([O.random_row(1, c, p.T) for c in range(64)])
+    rows[3, 0] = rows[3, 1]            # duplicate
+    rows[10, 5] = p.T                  # out of range
+    e = est_of(p)
+    assert e.check_rows(e.explicit(rows_tensor(rows))) == 2
+
+
+# ------------------------------------------------------------------ bulk estimator
+@pytest.mark.parametrize("cfg,n", [("C2", 20_000), ("C3", 20_000), ("C5", 300), ("C5h", 300)])
+def test_bulk_estimate(cfg, n):
+    p = make_config(cfg)
+    e = est_of(p)
+    first = 777
+    out = e.rwt_estimate(e.random(first, n, seed=1))
+    ref = O.Oracle(p).estimate_range(O.RANDOM, first, n, seed=1)
+    check_estimates(out, ref)
+
+
+def test_bulk_subsets_and_unaligned_outputs():
+    p = make_config("C3")
+    e = est_of(p)
+    n = 1000
+    ref = O.Oracle(p).estimate_range(O.RANDOM, 0, n, seed=1)
+    only_v = e.rwt_estimate(e.random(0, n, seed=1), want=("v",))
+    assert set(only_v) == {"v"}
+    assert np.abs(only_v["v"].cpu().numpy() - ref["v"]).max() <= 1e-5
+    # unaligned destination pointers -> non-TMA copy-out path
+    big = {k: torch.empty(n * p.G + 1, dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+    out = {k: big[k][1:].view(n, p.G) for k in big}
+    e.rwt_estimate(e.random(0, n, seed=1), out=out)
+    check_estimates(out, ref)
+
+
+def test_scores_large_G_sampled():
+    p = make_config("C5")
+    e = est_of(p)
+    first = 10**7
+    n = 1500
+    s1, s2, _ = e.score_orderings(e.random(first, n, seed=1))
+    ref = O.Oracle(p).score_range(O.RANDOM, first, n, seed=1)
+    check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)
+
+
+# ------------------------------------------------------------------ argmin / sharding
+def test_argmin_sharding_invariance_and_reduce_records():
+    p = make_config("C2")
+    e = est_of(p)
+    N = 100_000
+    full = e.best_ordering_async(e.random(0, N, seed=1)).cpu().numpy()
+    recs = []
+    for r in range(4):
+        first, cnt = r * N // 4, N // 4
+        recs.append(e.best_ordering_async(e.random(first, cnt, seed=1)))
+    merged = e.reduce_records(torch.cat(recs)).cpu().numpy()
+    assert np.array_equal(full, merged)
+    # reduce_records follows the (key, index) rule, lowest index on ties
+    rng = np.random.default_rng(0)
+    keys = rng.integers(0, 4, 300).astype(np.int64)
+    idx = rng.permutation(300).astype(np.int64)
+    t = torch.tensor(np.stack([keys, idx], 1).reshape(-1), device="cuda")
+    out = e.reduce_records(t).cpu().numpy()
+    k0 = keys.min()
+    assert out[0] == k0 and out[1] == idx[keys == k0].min()
+
+
+def test_deterministic_repeat():
+    p = make_config("C3")
+    e = est_of(p)
+    a = e.score_orderings(e.random(0, 20000, seed=3))
+    b = e.score_orderings(e.random(0, 20000, seed=3))
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
+def test_empty_and_tiny():
+    p = make_config("C2")
+    e = est_of(p)
+    s1, s2, _ = e.score_orderings(e.random(0, 0, seed=1))
+    assert s1.numel() == 0
+    assert e.best_ordering(e.random(0, 0, seed=1))["index"] == -1
+    b = e.best_ordering(e.random(5, 1, seed=1))
+    assert b["index"] == 5
+    # single group, single queue; and more queues than groups (empty queues)
+    for G, Q in [(1, 1), (3, 9)]:
+        pr = make_problem(G, Q, name="tiny")
+        er = est_of(pr)
+        n = 500
+        s1, s2, _ = er.score_orderings(er.random(0, n, seed=2))
+        ref = O.Oracle(pr).score_range(O.RANDOM, 0, n, seed=2)
+        check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, pr)
+
+
+def test_update_groups_matches_fresh_context():
+    p = make_config("C3")
+    e = est_of(p)
+    rng = np.random.default_rng(4)
+    p.slo = p.slo * rng.uniform(0.5, 2.0, p.G)
+    p.n_req = (p.n_req + rng.integers(0, 50, p.G)).astype(np.int32)
+    from paper_2407_00047_b200 import groups_array
+    g = groups_array(p.model, p.n_req, p.slo, p.mu, p.var, p.dist)
+    pinned = torch.from_numpy(g.view(np.uint8)).pin_memory()
+    e.update_groups(pinned)
+    s1, s2, _ = e.score_orderings(e.random(0, 5000, seed=1))
+    ref = O.Oracle(p).score_range(O.RANDOM, 0, 5000, seed=1)
+    check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)
+
+
+# ------------------------------------------------------------------ Monte-Carlo
+def test_mc_c4_counts_bit_exact():
+    p = make_config("C4")
+    e = est_of(p)
+    row = balanced_row(p.G, p.Q)
+    rt = rows_tensor(row[None, :], token_bytes=p.token_bytes)
+    T_mc = 1221
+    cnt = e.mc_estimate(e.explicit(rt), mc_seed=2, trials=T_mc).cpu().numpy().astype(np.uint32)
+    o = O.Oracle(p)
+    X = o.mc_sample(2, 0, T_mc)
+    ref = o.mc_count(O.EXPLICIT, 0, 1, X, rows=row[None, :])
+    np.testing.assert_array_equal(cnt, ref)
+
+
+def test_mc_random_candidates_and_trial_offsets():
+    rng = np.random.default_rng(11)
+    p = make_random_problem(rng, 40, 5, 3, 2, with_tables=True, backlog=True)
+    e = est_of(p)
+    o = O.Oracle(p)
+    t0, nt = 1000, 300
+    cnt = e.mc_estimate(e.random(50, 6, seed=4), mc_seed=9, trials=nt, trial_first=t0)
+    X = o.mc_sample(9, t0, nt)
+    ref = o.mc_count(O.RANDOM, 50, 6, X, seed=4)
+    np.testing.assert_array_equal(cnt.cpu().numpy().astype(np.uint32), ref)
+    # trial shards add up (MC sharding over ranks)
+    a = e.mc_estimate(e.random(50, 6, seed=4), mc_seed=9, trials=100, trial_first=t0)
+    b = e.mc_estimate(e.random(50, 6, seed=4), mc_seed=9, trials=200, trial_first=t0 + 100)
+    assert torch.equal(a + b, cnt)
+
+
+def test_mc_of_device_record_without_sync():
+    p = make_config("C2")
+    p.len_tables = make_config("C3").len_tables
+    e = est_of(p)
+    cand = e.random(0, 20000, seed=1)
+    rec = e.best_ordering_async(cand)
+    cnt_dev = e.mc_estimate(e.from_record(rec, seed=1), mc_seed=2, trials=500)
+    idx = int(rec[1].item())
+    cnt_host = e.mc_estimate(e.random(idx, 1, seed=1), mc_seed=2, trials=500)
+    assert torch.equal(cnt_dev, cnt_host)
+    qo, po = e.decode(e.from_record(rec, seed=1))
+    dec = O.Oracle(p).estimate(O.random_row(1, idx, p.T))
+    assert np.array_equal(qo.cpu().numpy()[0], dec["queue"])
+    assert np.array_equal(po.cpu().numpy()[0], dec["pos"])
+
+
+def test_mc_close_to_gaussian():
+    p = make_config("C4")
+    e = est_of(p)
+    row = balanced_row(p.G, p.Q)
+    rt = rows_tensor(row[None, :], token_bytes=p.token_bytes)
+    T_mc = 4000
+    cnt = e.mc_estimate(e.explicit(rt), mc_seed=2, trials=T_mc).cpu().numpy()[0]
+    out = e.rwt_estimate(e.explicit(rt))
+    v = out["v"].cpu().numpy()[0]
+    se = np.sqrt(np.maximum(v * (1 - v), 1e-4) / T_mc)
+    assert np.all(np.abs(cnt / T_mc - v) <= 0.03 + 5 * se)
