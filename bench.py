@@ -3,11 +3,11 @@
 
 One step = one pass of the whole hot path over one batch of
 C3 (64 groups, 4 models, 8 virtual queues) on every GPU:
-  a1-a5,a7  qlm_best_ordering_async: 1e6 RANDOM candidates generated on the
-            device, Eq. 10 scan, violation probabilities, S1/S2, argmin
+  a1-a7     qlm_score_estimate, ONE fused kernel: 1e6 RANDOM candidates
+            generated on the device, Eq. 10 scan, violation probabilities,
+            per-(group, candidate) wt / sd / v written to HBM (768 MB fp32),
+            S1/S2 and the argmin record
   a8        global min-loc: NCCL all-gather of 16-B records + reduce kernel
-  a6        qlm_rwt_estimate: per-(candidate, group) wt / sd / v for the same
-            1e6 candidates (768 MB of fp32 written to HBM)
   a9        decode of the global winner (queue, position per group)
   a10-a12   qlm_mc_estimate of the winner: 1221 Philox trials per GPU,
             counts summed with one NCCL all-reduce
@@ -193,7 +193,7 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     cand = est.random(first=rank * N_PER_GPU, count=N_PER_GPU, seed=CANDIDATE_SEED)
     rec = torch.empty(2, dtype=torch.int64, device=dev)
-    bulk = {k: torch.empty((N_PER_GPU, G), dtype=torch.float32, device=dev) for k in ("wt", "sd", "v")}
+    bulk = {k: torch.empty((G, N_PER_GPU), dtype=torch.float32, device=dev) for k in ("wt", "sd", "v")}
     counts = torch.empty((1, G), dtype=torch.int32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -202,15 +202,10 @@ def run_ours(args, rank, world, local_rank):
             est.update_groups(groups_host)                       # H2D of the step's inputs
         if kt:
             kt[0].record(stream)
-        r = est.best_ordering_async(cand, rec)
+        est.score_estimate(cand, out=bulk, scores=False, rec=rec)   # fused a1-a7
         if kt:
             kt[1].record(stream)
-        g = global_best(r, est.reduce_records)
-        if kt:
-            kt[2].record(stream)
-        est.rwt_estimate(cand, out=bulk)
-        if kt:
-            kt[3].record(stream)
+        g = global_best(rec, est.reduce_records)
         win = est.from_record(g, seed=CANDIDATE_SEED)
         qo, po = est.decode(win)
         est.mc_estimate(win, mc_seed=MC_SEED, trials=MC_TRIALS, trial_first=rank * MC_TRIALS,
@@ -233,7 +228,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- device-timed region
     K = args.steps
-    kts = [[ev() for _ in range(4)] for _ in range(K)]
+    kts = [[ev() for _ in range(2)] for _ in range(K)]
     e0, e1 = ev(), ev()
     barrier()
     torch.cuda.synchronize()
@@ -248,12 +243,11 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     launches = kernel_launches() - l0
     t_ms = e0.elapsed_time(e1)
-    score_ms = sum(k[0].elapsed_time(k[1]) for k in kts) / K
-    bulk_ms = sum(k[2].elapsed_time(k[3]) for k in kts) / K
-    t = torch.tensor([t_ms, score_ms, bulk_ms], dtype=torch.float64, device=dev)
+    fused_ms = sum(k[0].elapsed_time(k[1]) for k in kts) / K
+    t = torch.tensor([t_ms, fused_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_ms, score_ms, bulk_ms = t.tolist()
+    t_ms, fused_ms = t.tolist()
     ms_per_step = t_ms / K
     value = N_PER_GPU * world / (ms_per_step / 1e3)
 
@@ -302,29 +296,28 @@ def run_ours(args, rank, world, local_rank):
             "fallback 6650 GB/s (B200_PROFILING.md)"
         hbm_peak = hbm_peak or 6650.0
         bulk_bytes = N_PER_GPU * G * 3 * 4                     # algorithmic: outputs only (RANDOM)
-        bulk_gbs = bulk_bytes / (bulk_ms / 1e3) / 1e9
+        bulk_gbs = bulk_bytes / (fused_ms / 1e3) / 1e9
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get(CFG, {}).get("bulk_kernel_dram_bytes_per_launch")
+                traffic = json.load(f).get(CFG, {}).get("scan_kernel_dram_bytes_per_launch")
         except Exception:
             pass
-        roofline = {"kernel": "bulk_kernel (qlm_rwt_estimate)", "bound": "hbm",
+        roofline = {"kernel": "scan_kernel<RANDOM,u8,STAGED,SCORE> (qlm_score_estimate)", "bound": "hbm",
                     "achieved": bulk_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": bulk_gbs / hbm_peak, "traffic": traffic,
                     "algorithmic_bytes_per_launch": bulk_bytes,
                     "bytes_per_unit": G * 12, "units_per_launch": N_PER_GPU,
-                    "kernel_ms": bulk_ms, "peak_source": peak_src}
+                    "kernel_ms": fused_ms, "peak_source": peak_src}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(world),
             "roofline": roofline,
-            "kernels": {"score_argmin_ms": score_ms, "bulk_estimate_ms": bulk_ms,
-                        "score_argmin_orderings_per_s": N_PER_GPU / (score_ms / 1e3),
-                        "share_of_step": {"score_argmin": score_ms / ms_per_step,
-                                          "bulk_estimate": bulk_ms / ms_per_step}},
+            "kernels": {"fused_scan_ms": fused_ms,
+                        "fused_scan_orderings_per_s": N_PER_GPU / (fused_ms / 1e3),
+                        "share_of_step": {"fused_scan": fused_ms / ms_per_step}},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),

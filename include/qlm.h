@@ -175,12 +175,21 @@ QLM_API int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, 
 QLM_API int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
                       int32_t *queue_of_group, int32_t *pos_of_group, void *stream);
 
-/* Bulk per-group estimates for every candidate (Eq. 2/3/10): device fp32
- * [count][G] arrays, row k = candidate first + k, column = group id, each
- * nullable:  wt_mean = expected waiting time (s), wt_std = sqrt(variance),
- * viol = SLO-violation probability (R8, R9).                                */
+/* Bulk per-group estimates for every candidate (Eq. 2/3/10), group-major:
+ * device fp32 [G][count] arrays, element [g][k] = group g in candidate
+ * first + k, each nullable:  wt_mean = expected waiting time (s), wt_std =
+ * sqrt(variance), viol = SLO-violation probability (R8, R9).  Outputs that
+ * are 16-B aligned with count % 4 == 0 leave through bulk async copies.    */
 QLM_API int qlm_rwt_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean, float *wt_std,
                      float *viol, void *stream);
+
+/* The whole Gaussian hot path in ONE pass over the candidates: the bulk
+ * estimates of qlm_rwt_estimate, the per-candidate scores of
+ * qlm_score_orderings and the argmin record of qlm_best_ordering_async,
+ * every output nullable.  Asynchronous.                                    */
+QLM_API int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
+                       float *wt_std, float *viol, float *s1, float *s2, int32_t *n_over,
+                       qlm_record *rec, void *stream);
 
 /* Monte-Carlo estimate (R13): samples trials [trial_first, trial_first +
  * trial_count) of every group's total output tokens with Philox (key =

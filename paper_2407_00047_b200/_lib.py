@@ -65,6 +65,8 @@ SIGNATURES = {
     "qlm_reduce_records": (C.c_int, [_vp, _vp, _i32, _vp, _vp]),
     "qlm_best_ordering": (C.c_int, [_vp, C.POINTER(Candidates), C.POINTER(Best), _vp, _vp, _vp]),
     "qlm_rwt_estimate": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp, _vp]),
+    "qlm_score_estimate": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     _vp]),
     "qlm_mc_estimate": (C.c_int, [_vp, C.POINTER(Candidates), _u64, _i64, _i64, _vp, _vp]),
     "qlm_decode": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp]),
     "qlm_rows": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp]),

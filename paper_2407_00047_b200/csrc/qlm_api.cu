@@ -394,7 +394,7 @@ int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, flo
     if (cand->count == 0) return QLM_OK;
     ScanParams p = base_params(ctx, cand);
     p.s1 = s1; p.s2 = s2; p.n_over = n_over;
-    cudaError_t e = launch_score(p, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_scan(p, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score kernel");
 }
 
@@ -412,7 +412,7 @@ int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record
     }
     ScanParams p = base_params(ctx, cand);
     p.out_rec = rec;
-    cudaError_t e = launch_score(p, st);
+    cudaError_t e = launch_scan(p, st);
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score/argmin kernel");
 }
 
@@ -492,14 +492,30 @@ int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
 
 int qlm_rwt_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean, float *wt_std,
                      float *viol, void *stream) {
+    return qlm_score_estimate(ctx, cand, wt_mean, wt_std, viol, nullptr, nullptr, nullptr, nullptr,
+                              stream);
+}
+
+int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean, float *wt_std,
+                       float *viol, float *s1, float *s2, int32_t *n_over, qlm_record *rec,
+                       void *stream) {
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
-    if (cand->count == 0 || (!wt_mean && !wt_std && !viol)) return QLM_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cand->count == 0) {
+        if (!rec) return QLM_OK;
+        const qlm_record none = {~0ull, -1};
+        cudaError_t e = cudaMemcpyAsync(rec, &none, sizeof none, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e == cudaSuccess ? QLM_OK : cuda_fail(e, "empty record");
+    }
+    if (!wt_mean && !wt_std && !viol && !s1 && !s2 && !n_over && !rec) return QLM_OK;
     ScanParams p = base_params(ctx, cand);
     p.wt = wt_mean; p.sd = wt_std; p.vo = viol;
-    cudaError_t e = launch_bulk(p, static_cast<cudaStream_t>(stream));
-    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "bulk estimate kernel");
+    p.s1 = s1; p.s2 = s2; p.n_over = n_over; p.out_rec = rec;
+    cudaError_t e = launch_scan(p, st);
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "scan kernel");
 }
 
 int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,

@@ -154,52 +154,62 @@ __device__ __forceinline__ void tokens_enum(uint64_t c, int T, F &&f) {
 }
 
 // ---- one pass of the Eq. 2/3/10 recurrence over a row (R1-R7, R12) ---------
-// Tables are read from shared memory, replicated REP times and interleaved
-// so that lane l reads copy l % REP (REP = 8 makes 16-B reads conflict-free).
-template <int REP>
-struct Walker {
-    const GRec *sgrec;     // [G * REP]
-    const double2 *sab;    // [D * G * REP]
+// Shared-memory tables of a scan block.  Group records are replicated
+// (1 << rs) times and interleaved so that lane l reads copy l % (1 << rs):
+// with 8 copies a warp's random 16-B reads are bank-conflict free.
+struct SlotTables {
+    const GRec *sg;        // [G << rs]        {slo, n, model}
+    const double2 *sab;    // [(D*G) << rs]    {n mu / Theta, n var / Theta^2}
+    const double2 *str;    // [D*M*M]          {tail[d][prev], swap[d][prev][m]}
     const QRec *sq;        // [Q]
-    const double *stail;   // [D * M]
-    const double *sswap;   // [D * M * M]
-    int G, Q, M, lrep;
-    double A, B;           // exclusive mean / variance accumulators
-    int q, d, prev, first, backlog;
-
-    __device__ __forceinline__ void start_queue(int qq) {
-        const QRec r = sq[qq];
-        A = r.bmean; B = r.bvar; d = r.d; prev = r.r; backlog = r.backlog; first = 1; q = qq;
-    }
-    // Returns false for a queue separator.  Otherwise (wt, V) of the group.
-    __device__ __forceinline__ bool step(int tok, double &wt, double &V, GRec &g) {
-        if (tok >= G) {                                   // separator: next queue
-            start_queue(q + 1 < Q ? q + 1 : Q - 1);
-            return false;
-        }
-        g = sgrec[tok * REP + lrep];
-        const double2 ab = sab[(d * G + tok) * REP + lrep];
-        const int m = g.model;
-        if (m != prev) {                                  // t = 1 (Eq. 9)
-            const double t = (first && !backlog) ? 0.0 : stail[d * M + prev];
-            A = __dadd_rn(A, t);                          // C - W of the group ahead (R1)
-            A = __dadd_rn(A, sswap[(d * M + prev) * M + m]);   // swap S (R2)
-        }
-        wt = A; V = B;                                    // exclusive (R5)
-        A = __dadd_rn(A, ab.x);
-        B = __dadd_rn(B, ab.y);
-        prev = m; first = 0;
-        return true;
-    }
+    int G, Q, M, rs, rl;   // rl = lane & ((1 << rs) - 1)
 };
 
-// Violation probability (R8/R9): P(N(wt, V) > slo) = Phi-bar(slack / sqrt V),
-// 0/1 beyond |z| >= z_clamp (tested as slack^2 >= z_clamp^2 V, exact for V = 0).
-__device__ __forceinline__ float violation(double slack, double V, double zc2) {
-    const double c = fma(slack, slack, -zc2 * V);
-    if (c >= 0.0) return slack < 0.0 ? 1.0f : 0.0f;
-    const float z = (float)(slack * rsqrt(V));
-    return normcdff(-z);
+struct ScanState {
+    double A, B;           // exclusive mean / variance accumulators of the queue
+    int q, d, prev, tail_ok;
+};
+
+__device__ __forceinline__ void start_queue(const SlotTables &t, ScanState &s, int q) {
+    const QRec r = t.sq[q];
+    s.A = r.bmean; s.B = r.bvar; s.d = r.d; s.prev = r.r;
+    s.tail_ok = r.backlog;   // R4/R12: the first switch pays a tail only behind a backlog
+    s.q = q;
+}
+
+// One group slot: returns its (wt, V) and record.  On a model change
+// (t = 1, Eq. 9) the group ahead contributes its completion C = W + tail (R1)
+// and the swap is paid (R2); A + 0.0 == A, so the adds are unconditional and
+// the arithmetic is identical, operation by operation, to the sequential
+// definition.
+__device__ __forceinline__ void group_slot(const SlotTables &t, ScanState &s, int tok,
+                                           double &wt, double &V, GRec &g) {
+    g = t.sg[(tok << t.rs) + t.rl];
+    const double2 ab = t.sab[((s.d * t.G + tok) << t.rs) + t.rl];
+    const int m = g.model;
+    const double2 tr = t.str[(s.d * t.M + s.prev) * t.M + m];
+    const double tail = (m != s.prev && s.tail_ok) ? tr.x : 0.0;
+    s.A = __dadd_rn(__dadd_rn(s.A, tail), tr.y);     // swap[m][m] == 0
+    wt = s.A;
+    V = s.B;                                         // exclusive (R5)
+    s.A = __dadd_rn(s.A, ab.x);
+    s.B = __dadd_rn(s.B, ab.y);
+    s.prev = m;
+    s.tail_ok = 1;
+}
+
+// Phi-bar(z) = 0.5 erfc(z / sqrt 2) for |z| < z_clamp, fp32, via Abramowitz &
+// Stegun 7.1.26 (|erfc error| <= 1.5e-7, so |Phi-bar error| <= 7.5e-8 plus
+// fp32 rounding, well inside the 1e-5 parity bar; R8).
+__device__ __forceinline__ float phibar(float z) {
+    const float x = fabsf(z) * 0.70710678118654752f;
+    const float t = __fdividef(1.0f, fmaf(0.3275911f, x, 1.0f));
+    float y = fmaf(1.061405429f, t, -1.453152027f);
+    y = fmaf(y, t, 1.421413741f);
+    y = fmaf(y, t, -0.284496736f);
+    y = fmaf(y, t, 0.254829592f);
+    const float h = 0.5f * y * t * __expf(-x * x);
+    return z >= 0.0f ? h : 1.0f - h;
 }
 
 __device__ __forceinline__ uint64_t make_key(float s1, float s2) {

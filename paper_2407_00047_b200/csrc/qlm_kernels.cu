@@ -79,89 +79,175 @@ __global__ void build_tables_kernel(Dims dm, const qlm_group *__restrict__ grp,
 }
 
 // =============================================================================
-// a1-a7: the scan kernel
+// a1-a7: the fused scan kernel
 // =============================================================================
+// One thread = one candidate.  Per tile of blockDim consecutive candidates:
+// generate the row (RANDOM: Philox + forward Fisher-Yates in per-thread smem
+// scratch; EXPLICIT: 16-B row loads; ENUM: Lehmer unranking), walk it once
+// (Eq. 2/3/10), and in the same pass
+//   OUT_STAGED: stage wt / sd / v group-major in smem ([g][tid]: bank = lane,
+//               conflict-free) and write each group's row segment with one
+//               bulk async copy (TMA engine) -> out[g][c0 .. c0+n)
+//   OUT_DIRECT: store them straight to out[g][c] (large G, no room to stage)
+//   SCORE:      S1 / S2 / n_over per candidate and the running argmin.
+enum { OUT_NONE = 0, OUT_STAGED = 1, OUT_DIRECT = 2 };
+
 template <int KIND, typename TOK, typename F>
-__device__ __forceinline__ void for_tokens(const ScanParams &p, uint8_t *scratch, int64_t loc,
-                                           int64_t c, F &&f) {
+__device__ __forceinline__ void for_tokens(const Cand &cd, int T, uint8_t *scratch, int blk,
+                                           int64_t loc, int64_t c, F &&f) {
     if constexpr (KIND == QLM_CAND_RANDOM)
-        tokens_random<TOK>(scratch, p.blk, threadIdx.x, p.dm.T, p.cd.seed, (uint64_t)c, f);
+        tokens_random<TOK>(scratch, blk, threadIdx.x, T, cd.seed, (uint64_t)c, f);
     else if constexpr (KIND == QLM_CAND_EXPLICIT)
-        tokens_explicit<TOK>(p.cd.rows + loc * p.cd.stride, p.dm.T, f);
+        tokens_explicit<TOK>(cd.rows + loc * cd.stride, T, f);
     else
-        tokens_enum((uint64_t)c, p.dm.T, f);
+        tokens_enum((uint64_t)c, T, f);
 }
 
-template <int REP>
-__device__ __forceinline__ Walker<REP> stage_tables(const ScanParams &p, uint8_t *smem) {
+__device__ __forceinline__ SlotTables stage_tables(const ScanParams &p, uint8_t *smem) {
     const int tid = threadIdx.x, blk = blockDim.x;
     const Dims dm = p.dm;
-    GRec *sgrec = reinterpret_cast<GRec *>(smem + p.off_grec);
-    for (int i = tid; i < dm.G * REP; i += blk) sgrec[i] = p.tb.grec[i / REP];
+    const int rs = p.rep_shift;
+    GRec *sg = reinterpret_cast<GRec *>(smem + p.off_grec);
+    for (int i = tid; i < (dm.G << rs); i += blk) sg[i] = p.tb.grec[i >> rs];
     double2 *sab = reinterpret_cast<double2 *>(smem + p.off_ab);
-    for (int i = tid; i < dm.D * dm.G * REP; i += blk) sab[i] = p.tb.ab[i / REP];
+    for (int i = tid; i < ((dm.D * dm.G) << rs); i += blk) sab[i] = p.tb.ab[i >> rs];
     QRec *sq = reinterpret_cast<QRec *>(smem + p.off_q);
     for (int i = tid; i < dm.Q; i += blk) sq[i] = p.tb.qrec[i];
-    double *stail = reinterpret_cast<double *>(smem + p.off_tail);
-    for (int i = tid; i < dm.D * dm.M; i += blk) stail[i] = p.tb.tail[i];
-    double *sswap = reinterpret_cast<double *>(smem + p.off_swap);
-    for (int i = tid; i < dm.D * dm.M * dm.M; i += blk) sswap[i] = p.tb.swap[i];
-    Walker<REP> w;
-    w.sgrec = sgrec; w.sab = sab; w.sq = sq; w.stail = stail; w.sswap = sswap;
-    w.G = dm.G; w.Q = dm.Q; w.M = dm.M; w.lrep = tid & (REP - 1);
-    return w;
+    double2 *str = reinterpret_cast<double2 *>(smem + p.off_tr);
+    for (int i = tid; i < dm.D * dm.M * dm.M; i += blk) {
+        const int dp = i / dm.M;                        // d * M + prev
+        str[i] = make_double2(p.tb.tail[dp], p.tb.swap[i]);
+    }
+    SlotTables t;
+    t.sg = sg; t.sab = sab; t.str = str; t.sq = sq;
+    t.G = dm.G; t.Q = dm.Q; t.M = dm.M; t.rs = rs; t.rl = tid & ((1 << rs) - 1);
+    return t;
 }
 
-template <int KIND, typename TOK, int REP>
-__global__ void __launch_bounds__(256) score_kernel(const ScanParams p) {
+template <int KIND, typename TOK, int OUT, bool SCORE>
+__global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int tid = threadIdx.x, blk = p.blk;
-    Walker<REP> w = stage_tables<REP>(p, smem);
+    const int tid = threadIdx.x, blk = blockDim.x;
+    const SlotTables tab = stage_tables(p, smem);
     uint8_t *scratch = smem + p.off_scratch;
     __syncthreads();
 
-    int64_t first = p.cd.first;
-    if (p.cd.first_from) {
-        first = p.cd.first_from->index;
+    const Cand cd = p.cd;
+    int64_t first = cd.first;
+    if (cd.first_from) {
+        first = cd.first_from->index;
         if (first < 0) {
-            if (blockIdx.x == 0 && tid == 0 && p.out_rec) {
+            if (SCORE && p.out_rec && blockIdx.x == 0 && tid == 0) {
                 p.out_rec->key = ~0ull; p.out_rec->index = -1;
             }
             return;
         }
     }
-    const double den = *p.tb.den;
-    const int64_t count = p.cd.count;
+    const int G = p.dm.G, Q = p.dm.Q, T = p.dm.T;
+    const double zc2 = p.zc2;
+    const float alpha = p.alpha;
+    const int64_t count = cd.count;
+    float *const gout[3] = {p.wt, p.sd, p.vo};
+    float *st[3] = {nullptr, nullptr, nullptr};
+    if constexpr (OUT == OUT_STAGED) {
+        int k = 0;
+        for (int a = 0; a < 3; ++a)
+            if (gout[a]) st[a] = reinterpret_cast<float *>(smem + p.off_stage) + (size_t)(k++) * G * blk;
+    }
+    const double den = SCORE ? *p.tb.den : 1.0;
     uint64_t bkey = ~0ull;
     int64_t bidx = -1;
-    for (int64_t loc = (int64_t)blockIdx.x * blk + tid; loc < count;
-         loc += (int64_t)gridDim.x * blk) {
-        const int64_t c = first + loc;
-        w.start_queue(0);
-        double S2 = 0.0, frac = 0.0;
-        int cnt = 0, over = 0;
-        for_tokens<KIND, TOK>(p, scratch, loc, c, [&](int tok) {
-            double wt, V;
-            GRec g;
-            if (!w.step(tok, wt, V, g)) return;
-            const double slack = __dsub_rn(g.slo, wt);   // -p_i (Eq. 11)
-            S2 = __dsub_rn(S2, slack);                   // objective sum p
-            const float v = violation(slack, V, p.zc2);
-            if (v == 1.0f) cnt += g.n;
-            else if (v != 0.0f) frac = __dadd_rn(frac, __dmul_rn((double)g.n, (double)v));
-            over += v > p.alpha;
-        });
-        const float s1 = (float)(__dadd_rn((double)cnt, frac) / den);   // R11
-        const float s2 = (float)S2;
-        if (p.s1) p.s1[loc] = s1;
-        if (p.s2) p.s2[loc] = s2;
-        if (p.n_over) p.n_over[loc] = over;
-        const uint64_t key = make_key(s1, s2);
-        if (better(key, c, bkey, bidx)) { bkey = key; bidx = c; }
+    const int64_t ntiles = (count + blk - 1) / blk;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t c0 = tile * blk;
+        const int nvalid = (int)min((int64_t)blk, count - c0);
+        const int64_t loc = c0 + tid;
+        if constexpr (OUT == OUT_STAGED) {
+            if (tile != blockIdx.x) {                 // staging free again?
+                if (p.use_tma) bulk_wait_read0();
+                __syncthreads();
+            }
+        }
+        if (tid < nvalid) {
+            ScanState s;
+            start_queue(tab, s, 0);
+            double S2 = 0.0;
+            float frac = 0.0f;
+            int cnt = 0, over = 0;
+            for_tokens<KIND, TOK>(cd, T, scratch, blk, loc, first + loc, [&](int tok) {
+                if (tok >= G) {                          // queue separator
+                    start_queue(tab, s, s.q + 1 < Q ? s.q + 1 : Q - 1);
+                    return;
+                }
+                double wt, V;
+                GRec g;
+                group_slot(tab, s, tok, wt, V, g);
+                const double slack = __dsub_rn(g.slo, wt);        // -p_i (Eq. 11)
+                // violation probability (R8/R9): |z| >= z_clamp <=> slack^2 >= z_clamp^2 V
+                const bool clamped = fma(slack, slack, -zc2 * V) >= 0.0;
+                const bool neg = slack < 0.0;
+                float v = neg ? 1.0f : 0.0f;
+                if (!clamped) v = phibar((float)slack * rsqrtf((float)V));
+                if constexpr (SCORE) {
+                    S2 = __dsub_rn(S2, slack);                    // sum_i p_i
+                    cnt += (clamped && neg) ? g.n : 0;
+                    if (!clamped) frac = fmaf((float)g.n, v, frac);
+                    over += v > alpha;
+                }
+                if constexpr (OUT == OUT_STAGED) {
+                    const int o = tok * blk + tid;
+                    if (st[0]) st[0][o] = (float)wt;
+                    if (st[1]) st[1][o] = sqrtf((float)V);
+                    if (st[2]) st[2][o] = v;
+                } else if constexpr (OUT == OUT_DIRECT) {
+                    const int64_t o = (int64_t)tok * count + loc;
+                    if (gout[0]) gout[0][o] = (float)wt;
+                    if (gout[1]) gout[1][o] = sqrtf((float)V);
+                    if (gout[2]) gout[2][o] = v;
+                }
+            });
+            if constexpr (SCORE) {
+                const float s1 = (float)(__dadd_rn((double)cnt, (double)frac) / den);   // R11
+                const float s2 = (float)S2;
+                if (p.s1) p.s1[loc] = s1;
+                if (p.s2) p.s2[loc] = s2;
+                if (p.n_over) p.n_over[loc] = over;
+                const uint64_t key = make_key(s1, s2);
+                const int64_t c = first + loc;
+                if (better(key, c, bkey, bidx)) { bkey = key; bidx = c; }
+            }
+        }
+        if constexpr (OUT == OUT_STAGED) {
+            if (p.use_tma) {
+                fence_proxy_async_smem();
+                __syncthreads();
+                const int nrows = p.n_out * G;
+                for (int r = tid; r < nrows; r += blk) {
+                    const int k = r / G, g = r - k * G;
+                    int a = -1;
+                    for (int x = 0, seen = 0; x < 3; ++x)
+                        if (gout[x] && seen++ == k) a = x;
+                    bulk_s2g(gout[a] + (int64_t)g * count + c0, st[a] + (size_t)g * blk,
+                             (uint32_t)nvalid * 4u);
+                }
+                bulk_commit();
+            } else {
+                __syncthreads();
+                if (tid < nvalid)
+                    for (int a = 0; a < 3; ++a)
+                        if (gout[a])
+                            for (int g = 0; g < G; ++g)
+                                gout[a][(int64_t)g * count + loc] = st[a][g * blk + tid];
+            }
+        }
     }
+    if constexpr (OUT == OUT_STAGED) {
+        if (p.use_tma) bulk_wait0();
+    }
+    if constexpr (!SCORE) return;
     if (!p.out_rec) return;
 
-    // ---- argmin: warp -> block -> grid (last block reduces block records) ----
+    // ---- argmin: warp -> block -> grid (the last block reduces block records) ----
     __shared__ uint64_t rk[32];
     __shared__ int64_t ri[32];
     __shared__ int is_last;
@@ -207,75 +293,6 @@ __global__ void __launch_bounds__(256) score_kernel(const ScanParams p) {
     }
 }
 
-template <int KIND, typename TOK, int REP, bool STAGE>
-__global__ void __launch_bounds__(256) bulk_kernel(const ScanParams p) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int tid = threadIdx.x, blk = p.blk;
-    const int G = p.dm.G;
-    Walker<REP> w = stage_tables<REP>(p, smem);
-    uint8_t *scratch = smem + p.off_scratch;
-    __syncthreads();
-
-    int64_t first = p.cd.first;
-    if (p.cd.first_from) {
-        first = p.cd.first_from->index;
-        if (first < 0) return;
-    }
-    float *stw = p.off_stage_w >= 0 ? reinterpret_cast<float *>(smem + p.off_stage_w) : nullptr;
-    float *sts = p.off_stage_s >= 0 ? reinterpret_cast<float *>(smem + p.off_stage_s) : nullptr;
-    float *stv = p.off_stage_v >= 0 ? reinterpret_cast<float *>(smem + p.off_stage_v) : nullptr;
-    const int64_t count = p.cd.count;
-    const int64_t ntiles = (count + blk - 1) / blk;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t loc0 = tile * blk;
-        const int nvalid = (int)min((int64_t)blk, count - loc0);
-        const int64_t loc = loc0 + tid;
-        if (STAGE && p.use_tma && tile != blockIdx.x) {
-            if (tid == 0) bulk_wait_read0();          // staging buffer free again
-            __syncthreads();
-        }
-        if (tid < nvalid) {
-            float *pw = p.wt ? (STAGE ? stw + tid * G : p.wt + loc * G) : nullptr;
-            float *ps = p.sd ? (STAGE ? sts + tid * G : p.sd + loc * G) : nullptr;
-            float *pv = p.vo ? (STAGE ? stv + tid * G : p.vo + loc * G) : nullptr;
-            w.start_queue(0);
-            for_tokens<KIND, TOK>(p, scratch, loc, first + loc, [&](int tok) {
-                double wt, V;
-                GRec g;
-                if (!w.step(tok, wt, V, g)) return;
-                if (pw) pw[tok] = (float)wt;
-                if (ps) ps[tok] = sqrtf((float)V);
-                if (pv) pv[tok] = violation(__dsub_rn(g.slo, wt), V, p.zc2);
-            });
-        }
-        if constexpr (STAGE) {
-            const uint32_t bytes = (uint32_t)nvalid * (uint32_t)G * 4u;
-            if (p.use_tma) {
-                fence_proxy_async_smem();
-                __syncthreads();
-                if (tid == 0) {
-                    if (stw) bulk_s2g(p.wt + loc0 * G, stw, bytes);
-                    if (sts) bulk_s2g(p.sd + loc0 * G, sts, bytes);
-                    if (stv) bulk_s2g(p.vo + loc0 * G, stv, bytes);
-                    bulk_commit();
-                }
-            } else {
-                __syncthreads();
-                const int nw = nvalid * G;
-                for (int i = tid; i < nw; i += blk) {
-                    if (stw) p.wt[loc0 * G + i] = stw[i];
-                    if (sts) p.sd[loc0 * G + i] = sts[i];
-                    if (stv) p.vo[loc0 * G + i] = stv[i];
-                }
-                __syncthreads();
-            }
-        }
-    }
-    if constexpr (STAGE) {
-        if (p.use_tma && tid == 0) bulk_wait0();
-    }
-}
-
 // =============================================================================
 // a8: min-loc over records (e.g. one per rank after an all-gather)
 // =============================================================================
@@ -315,7 +332,7 @@ __global__ void __launch_bounds__(64) row_kernel(const ScanParams p, uint16_t *r
     if (loc >= p.cd.count) return;
     const int T = p.dm.T, G = p.dm.G, Q = p.dm.Q;
     int s = 0, q = 0, pos = 0;
-    for_tokens<KIND, TOK>(p, scratch, loc, first + loc, [&](int tok) {
+    for_tokens<KIND, TOK>(p.cd, T, scratch, blockDim.x, loc, first + loc, [&](int tok) {
         if (rows_out) rows_out[loc * T + s] = (uint16_t)tok;
         ++s;
         if (tok >= G) {
@@ -453,32 +470,6 @@ int sm_count() {
 
 static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Shared-memory plan of the scan kernels.
-static size_t plan_smem(ScanParams &p, int rep, int kind, int tok_bytes, int blk, int nstage,
-                        bool stage) {
-    const Dims &dm = p.dm;
-    size_t off = 0;
-    p.off_grec = (int)off; off = align16(off + (size_t)dm.G * rep * sizeof(GRec));
-    p.off_ab = (int)off;   off = align16(off + (size_t)dm.D * dm.G * rep * sizeof(double2));
-    p.off_q = (int)off;    off = align16(off + (size_t)dm.Q * sizeof(QRec));
-    p.off_tail = (int)off; off = align16(off + (size_t)dm.D * dm.M * sizeof(double));
-    p.off_swap = (int)off; off = align16(off + (size_t)dm.D * dm.M * dm.M * sizeof(double));
-    p.off_scratch = (int)off;
-    if (kind == QLM_CAND_RANDOM) {
-        const int epw = 4 / tok_bytes;
-        off = align16(off + (size_t)((dm.T + epw - 1) / epw) * 4 * blk);
-    }
-    p.off_stage_w = p.off_stage_s = p.off_stage_v = -1;
-    if (stage) {
-        const size_t arr = (size_t)blk * dm.G * 4;
-        if (p.wt) { p.off_stage_w = (int)off; off = align16(off + arr); }
-        if (p.sd) { p.off_stage_s = (int)off; off = align16(off + arr); }
-        if (p.vo) { p.off_stage_v = (int)off; off = align16(off + arr); }
-    }
-    (void)nstage;
-    return off;
-}
-
 static const size_t kMaxSmem = 227 * 1024;
 
 // Largest dynamic shared memory a launch of `kern` may use (opt-in limit
@@ -517,129 +508,93 @@ static int occupancy(K kern, int blk, size_t smem) {
     return nb;
 }
 
-static int choose_rep(const Dims &dm) {
-    const size_t rec = (size_t)dm.G * (1 + dm.D) * 16;
-    return rec * 8 <= 40 * 1024 ? 8 : 1;
+// Shared-memory plan of the scan kernel for a block of `blk` threads.
+static size_t plan_smem(ScanParams &p, int rep_shift, int kind, int tok_bytes, int blk, int out) {
+    const Dims &dm = p.dm;
+    size_t off = 0;
+    p.rep_shift = rep_shift;
+    p.off_grec = (int)off; off = align16(off + ((size_t)dm.G << rep_shift) * sizeof(GRec));
+    p.off_ab = (int)off;   off = align16(off + ((size_t)dm.D * dm.G << rep_shift) * sizeof(double2));
+    p.off_q = (int)off;    off = align16(off + (size_t)dm.Q * sizeof(QRec));
+    p.off_tr = (int)off;   off = align16(off + (size_t)dm.D * dm.M * dm.M * sizeof(double2));
+    p.off_scratch = (int)off;
+    if (kind == QLM_CAND_RANDOM) {
+        const int epw = 4 / tok_bytes;
+        off = align16(off + (size_t)((dm.T + epw - 1) / epw) * 4 * blk);
+    }
+    p.off_stage = (int)off;
+    if (out == OUT_STAGED) off = align16(off + (size_t)p.n_out * blk * dm.G * 4);
+    return off;
 }
 
-// ---- score ----
-template <int KIND, typename TOK, int REP>
-static cudaError_t launch_score_t(ScanParams p, cudaStream_t st) {
-    auto kern = score_kernel<KIND, TOK, REP>;
+static int default_rep_shift(const Dims &dm) {
+    const size_t rec = (size_t)dm.G * (1 + dm.D) * 16;
+    return rec * 8 <= 24 * 1024 ? 3 : 0;
+}
+
+template <int KIND, typename TOK, int OUT, bool SCORE>
+static cudaError_t launch_scan_t(ScanParams p, cudaStream_t st) {
+    auto kern = scan_kernel<KIND, TOK, OUT, SCORE>;
     const size_t lim = max_dyn(kern);
-    int blk = 128;
-    size_t smem = 0;
-    for (; blk >= 32; blk >>= 1) {
-        smem = plan_smem(p, REP, KIND, sizeof(TOK), blk, 0, false);
-        if (smem <= lim) break;
+    if (!lim) return cudaErrorInvalidConfiguration;
+    // choose (block size, replication) maximising resident candidates per SM
+    int best_blk = 0, best_rs = 0, best_thr = 0;
+    size_t best_smem = 0;
+    const int rs0 = default_rep_shift(p.dm);
+    const int blks[] = {128, 96, 64, 32};
+    for (int rs : {rs0, 0}) {
+        for (int blk : blks) {
+            ScanParams q = p;
+            const size_t smem = plan_smem(q, rs, KIND, sizeof(TOK), blk, OUT);
+            if (smem > lim) continue;
+            const int thr = occupancy(kern, blk, smem) * blk;
+            if (thr > best_thr) { best_thr = thr; best_blk = blk; best_rs = rs; best_smem = smem; }
+        }
+        if (best_thr >= 256 || (OUT != OUT_STAGED && best_thr)) break;
     }
-    if (blk < 32) return cudaErrorInvalidConfiguration;
-    p.blk = blk;
-    cudaError_t e = prep(kern, smem);
-    if (e != cudaSuccess) return e;
-    const int nb = occupancy(kern, blk, smem);
-    int64_t grid = (p.cd.count + blk - 1) / blk;
-    const int64_t maxg = (int64_t)sm_count() * (nb > 0 ? nb : 1);
+    if (!best_blk) return cudaErrorInvalidConfiguration;
+    p.blk = best_blk;
+    plan_smem(p, best_rs, KIND, sizeof(TOK), best_blk, OUT);
+    int64_t grid = (p.cd.count + best_blk - 1) / best_blk;
+    const int64_t maxg = (int64_t)sm_count() * (best_thr / best_blk);
     if (grid > maxg) grid = maxg;
     if (grid > p.max_blocks) grid = p.max_blocks;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, blk, smem, st>>>(p);
+    kern<<<(unsigned)grid, best_blk, best_smem, st>>>(p);
     ++g_launches;
     return cudaGetLastError();
 }
 
 template <int KIND, typename TOK>
-static cudaError_t launch_score_k(const ScanParams &p, cudaStream_t st) {
-    return choose_rep(p.dm) == 8 ? launch_score_t<KIND, TOK, 8>(p, st)
-                                 : launch_score_t<KIND, TOK, 1>(p, st);
+static cudaError_t launch_scan_k(ScanParams &p, cudaStream_t st) {
+    const bool score = p.s1 || p.s2 || p.n_over || p.out_rec;
+    p.n_out = (p.wt != nullptr) + (p.sd != nullptr) + (p.vo != nullptr);
+    if (p.n_out == 0) return launch_scan_t<KIND, TOK, OUT_NONE, true>(p, st);
+    // staged (group-major smem tile + bulk copies) when one fits, else direct stores
+    const size_t stage_bytes = (size_t)p.n_out * 32 * p.dm.G * 4;
+    const bool fits = stage_bytes + 64 * 1024 <= kMaxSmem;
+    p.use_tma = (p.cd.count % 4 == 0) && (!p.wt || ((uintptr_t)p.wt & 15) == 0) &&
+                (!p.sd || ((uintptr_t)p.sd & 15) == 0) && (!p.vo || ((uintptr_t)p.vo & 15) == 0);
+    if (fits) {
+        cudaError_t e = score ? launch_scan_t<KIND, TOK, OUT_STAGED, true>(p, st)
+                              : launch_scan_t<KIND, TOK, OUT_STAGED, false>(p, st);
+        if (e != cudaErrorInvalidConfiguration) return e;
+        cudaGetLastError();
+    }
+    return score ? launch_scan_t<KIND, TOK, OUT_DIRECT, true>(p, st)
+                 : launch_scan_t<KIND, TOK, OUT_DIRECT, false>(p, st);
 }
 
-cudaError_t launch_score(const ScanParams &p, cudaStream_t st) {
+cudaError_t launch_scan(ScanParams p, cudaStream_t st) {
     switch (p.cd.kind) {
     case QLM_CAND_RANDOM:
-        return p.dm.T <= 256 ? launch_score_k<QLM_CAND_RANDOM, uint8_t>(p, st)
-                             : launch_score_k<QLM_CAND_RANDOM, uint16_t>(p, st);
+        return p.dm.T <= 256 ? launch_scan_k<QLM_CAND_RANDOM, uint8_t>(p, st)
+                             : launch_scan_k<QLM_CAND_RANDOM, uint16_t>(p, st);
     case QLM_CAND_EXPLICIT:
-        return p.cd.tb == 1 ? launch_score_k<QLM_CAND_EXPLICIT, uint8_t>(p, st)
-                            : launch_score_k<QLM_CAND_EXPLICIT, uint16_t>(p, st);
+        return p.cd.tb == 1 ? launch_scan_k<QLM_CAND_EXPLICIT, uint8_t>(p, st)
+                            : launch_scan_k<QLM_CAND_EXPLICIT, uint16_t>(p, st);
     default:
-        return launch_score_k<QLM_CAND_ENUM, uint8_t>(p, st);
-    }
-}
-
-// ---- bulk ----
-template <int KIND, typename TOK, int REP>
-static cudaError_t launch_bulk_t(ScanParams p, cudaStream_t st) {
-    const int nout = (p.wt != nullptr) + (p.sd != nullptr) + (p.vo != nullptr);
-    // pick the block size maximising resident candidates per SM with staging
-    int best_blk = 0, best_thr = 0;
-    size_t best_smem = 0;
-    for (int blk = 128; blk >= 32; blk >>= 1) {
-        ScanParams q = p;
-        const size_t smem = plan_smem(q, REP, KIND, sizeof(TOK), blk, nout, true);
-        auto kern = bulk_kernel<KIND, TOK, REP, true>;
-        if (smem > max_dyn(kern)) continue;
-        if (prep(kern, smem) != cudaSuccess) continue;
-        const int thr = occupancy(kern, blk, smem) * blk;
-        if (thr > best_thr) { best_thr = thr; best_blk = blk; best_smem = smem; }
-    }
-    const bool aligned = (p.dm.G % 4 == 0) &&
-                         (!p.wt || ((uintptr_t)p.wt & 15) == 0) &&
-                         (!p.sd || ((uintptr_t)p.sd & 15) == 0) &&
-                         (!p.vo || ((uintptr_t)p.vo & 15) == 0);
-    if (best_blk && nout > 0) {
-        p.blk = best_blk;
-        plan_smem(p, REP, KIND, sizeof(TOK), best_blk, nout, true);
-        p.use_tma = aligned ? 1 : 0;
-        auto kern = bulk_kernel<KIND, TOK, REP, true>;
-        int64_t grid = (p.cd.count + best_blk - 1) / best_blk;
-        const int64_t maxg = (int64_t)sm_count() * (best_thr / best_blk);
-        if (grid > maxg) grid = maxg;
-        if (grid < 1) grid = 1;
-        kern<<<(unsigned)grid, best_blk, best_smem, st>>>(p);
-        ++g_launches;
-        return cudaGetLastError();
-    }
-    // no staging: direct stores
-    const size_t lim = max_dyn(bulk_kernel<KIND, TOK, REP, false>);
-    int blk = 128;
-    size_t smem = 0;
-    for (; blk >= 32; blk >>= 1) {
-        smem = plan_smem(p, REP, KIND, sizeof(TOK), blk, 0, false);
-        if (smem <= lim) break;
-    }
-    if (blk < 32) return cudaErrorInvalidConfiguration;
-    p.blk = blk;
-    p.use_tma = 0;
-    auto kern = bulk_kernel<KIND, TOK, REP, false>;
-    cudaError_t e = prep(kern, smem);
-    if (e != cudaSuccess) return e;
-    const int nb = occupancy(kern, blk, smem);
-    int64_t grid = (p.cd.count + blk - 1) / blk;
-    const int64_t maxg = (int64_t)sm_count() * (nb > 0 ? nb : 1);
-    if (grid > maxg) grid = maxg;
-    if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, blk, smem, st>>>(p);
-    ++g_launches;
-    return cudaGetLastError();
-}
-
-template <int KIND, typename TOK>
-static cudaError_t launch_bulk_k(const ScanParams &p, cudaStream_t st) {
-    return choose_rep(p.dm) == 8 ? launch_bulk_t<KIND, TOK, 8>(p, st)
-                                 : launch_bulk_t<KIND, TOK, 1>(p, st);
-}
-
-cudaError_t launch_bulk(const ScanParams &p, cudaStream_t st) {
-    switch (p.cd.kind) {
-    case QLM_CAND_RANDOM:
-        return p.dm.T <= 256 ? launch_bulk_k<QLM_CAND_RANDOM, uint8_t>(p, st)
-                             : launch_bulk_k<QLM_CAND_RANDOM, uint16_t>(p, st);
-    case QLM_CAND_EXPLICIT:
-        return p.cd.tb == 1 ? launch_bulk_k<QLM_CAND_EXPLICIT, uint8_t>(p, st)
-                            : launch_bulk_k<QLM_CAND_EXPLICIT, uint16_t>(p, st);
-    default:
-        return launch_bulk_k<QLM_CAND_ENUM, uint8_t>(p, st);
+        return launch_scan_k<QLM_CAND_ENUM, uint8_t>(p, st);
     }
 }
 

@@ -13,7 +13,7 @@ struct ScanParams {
     Cand cd;
     float *s1, *s2;            // score outputs [count] (nullable)
     int32_t *n_over;
-    float *wt, *sd, *vo;       // bulk outputs [count][G] (nullable)
+    float *wt, *sd, *vo;       // bulk outputs, group-major [G][count] (nullable)
     qlm_record *block_recs;    // [max_blocks] argmin scratch
     unsigned int *counter;     // last-block ticket
     qlm_record *out_rec;       // argmin result (nullable = no argmin)
@@ -21,9 +21,10 @@ struct ScanParams {
     double zc2;                // z_clamp^2
     float alpha;
     int blk;
-    int use_tma;
-    int off_grec, off_ab, off_q, off_tail, off_swap, off_scratch;
-    int off_stage_w, off_stage_s, off_stage_v;
+    int use_tma;               // staged outputs leave through bulk async copies
+    int n_out;                 // number of non-null bulk outputs
+    int rep_shift;             // group tables replicated 1 << rep_shift times in smem
+    int off_grec, off_ab, off_q, off_tr, off_scratch, off_stage;
 };
 
 extern std::atomic<int64_t> g_launches;
@@ -33,8 +34,7 @@ cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
                          const double *theta, const double *prefill, const double *eps,
                          const double *dec, const double *maxo, const double *swp,
                          const Tables &tb, cudaStream_t st);
-cudaError_t launch_score(const ScanParams &p, cudaStream_t st);
-cudaError_t launch_bulk(const ScanParams &p, cudaStream_t st);
+cudaError_t launch_scan(ScanParams p, cudaStream_t st);
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,
                         cudaStream_t st);
 cudaError_t launch_reduce_records(const qlm_record *recs, int n, qlm_record *out,

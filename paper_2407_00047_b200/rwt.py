@@ -164,12 +164,32 @@ class RwtEstimator:
                     pos_of_group=po)
 
     def rwt_estimate(self, cand: Cand, want=("wt", "sd", "v"), out=None, stream=None):
-        """Per-(candidate, group) expected wait, its std and violation probability, [count, G]."""
+        """Per-(group, candidate) expected wait, its std and violation probability.
+
+        Group-major: out[k] has shape [G, count]; out["v"][g, k] is group g in
+        candidate first + k.
+        """
         if out is None:
-            out = {k: self._empty((cand.count, self.G), torch.float32) for k in want}
+            out = {k: self._empty((self.G, cand.count), torch.float32) for k in want}
         ptr = {k: (out[k].data_ptr() if k in out else None) for k in ("wt", "sd", "v")}
         L.check(L.lib().qlm_rwt_estimate(self._h, C.byref(cand.c()), ptr["wt"], ptr["sd"], ptr["v"],
                                          self._stream(stream)), "qlm_rwt_estimate")
+        return out
+
+    def score_estimate(self, cand: Cand, out=None, scores=True, rec: torch.Tensor | None = None,
+                       stream=None):
+        """The fused single pass: bulk estimates + per-candidate scores + argmin record."""
+        out = {} if out is None else out
+        ptr = {k: (out[k].data_ptr() if out.get(k) is not None else None)
+               for k in ("wt", "sd", "v", "s1", "s2", "n_over")}
+        if scores and ptr["s1"] is None:
+            out["s1"] = self._empty(cand.count, torch.float32)
+            out["s2"] = self._empty(cand.count, torch.float32)
+            ptr["s1"], ptr["s2"] = out["s1"].data_ptr(), out["s2"].data_ptr()
+        L.check(L.lib().qlm_score_estimate(self._h, C.byref(cand.c()), ptr["wt"], ptr["sd"], ptr["v"],
+                                           ptr["s1"], ptr["s2"], ptr["n_over"],
+                                           None if rec is None else rec.data_ptr(),
+                                           self._stream(stream)), "qlm_score_estimate")
         return out
 
     def mc_estimate(self, cand: Cand, mc_seed: int, trials: int, trial_first: int = 0,

@@ -19,9 +19,10 @@ def check_scores(s1, s2, ref, prob, wt_sum=None):
 
 
 def check_estimates(out, ref):
-    wt = out["wt"].cpu().numpy().astype(np.float64)
-    sd = out["sd"].cpu().numpy().astype(np.float64)
-    v = out["v"].cpu().numpy().astype(np.float64)
+    """out: device tensors [G, count] (group-major); ref: oracle arrays [count, G]."""
+    wt = out["wt"].cpu().numpy().astype(np.float64).T
+    sd = out["sd"].cpu().numpy().astype(np.float64).T
+    v = out["v"].cpu().numpy().astype(np.float64).T
     zero = ref["wt"] == 0
     assert np.all(wt[zero] == 0), "wt must be exactly 0 where the oracle gives 0"
     rel = np.abs(wt - ref["wt"])[~zero] / ref["wt"][~zero]

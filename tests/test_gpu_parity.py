@@ -163,12 +163,38 @@ def test_bulk_subsets_and_unaligned_outputs():
     ref = O.Oracle(p).estimate_range(O.RANDOM, 0, n, seed=1)
     only_v = e.rwt_estimate(e.random(0, n, seed=1), want=("v",))
     assert set(only_v) == {"v"}
-    assert np.abs(only_v["v"].cpu().numpy() - ref["v"]).max() <= 1e-5
-    # unaligned destination pointers -> non-TMA copy-out path
+    assert np.abs(only_v["v"].cpu().numpy().T - ref["v"]).max() <= 1e-5
+    # unaligned destination pointers -> non-bulk-copy path
     big = {k: torch.empty(n * p.G + 1, dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
-    out = {k: big[k][1:].view(n, p.G) for k in big}
+    out = {k: big[k][1:].view(p.G, n) for k in big}
     e.rwt_estimate(e.random(0, n, seed=1), out=out)
     check_estimates(out, ref)
+    # count % 4 != 0 -> ragged tiles
+    n2 = 1001
+    check_estimates(e.rwt_estimate(e.random(3, n2, seed=1)),
+                    O.Oracle(p).estimate_range(O.RANDOM, 3, n2, seed=1))
+
+
+@pytest.mark.parametrize("cfg,n", [("C3", 40_000), ("C2", 10_001), ("C5", 256)])
+def test_fused_score_estimate_matches_separate_calls(cfg, n):
+    p = make_config(cfg)
+    e = est_of(p)
+    cand = e.random(11, n, seed=1)
+    rec = torch.empty(2, dtype=torch.int64, device="cuda")
+    no = torch.empty(n, dtype=torch.int32, device="cuda")
+    bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+    bufs["n_over"] = no
+    out = e.score_estimate(cand, out=bufs, rec=rec)
+    s1, s2, no2 = e.score_orderings(cand)
+    assert torch.equal(out["s1"], s1) and torch.equal(out["s2"], s2) and torch.equal(no, no2)
+    sep = e.rwt_estimate(cand)
+    for k in ("wt", "sd", "v"):
+        assert torch.equal(out[k], sep[k])
+    assert torch.equal(rec, e.best_ordering_async(cand))
+    o = O.Oracle(p)
+    m = min(n, 3000)
+    ref = o.score_range(O.RANDOM, 11, m, seed=1)
+    check_scores(s1[:m].cpu().numpy(), s2[:m].cpu().numpy(), ref, p)
 
 
 def test_scores_large_G_sampled():
@@ -299,6 +325,6 @@ def test_mc_close_to_gaussian():
     T_mc = 4000
     cnt = e.mc_estimate(e.explicit(rt), mc_seed=2, trials=T_mc).cpu().numpy()[0]
     out = e.rwt_estimate(e.explicit(rt))
-    v = out["v"].cpu().numpy()[0]
+    v = out["v"].cpu().numpy()[:, 0]
     se = np.sqrt(np.maximum(v * (1 - v), 1e-4) / T_mc)
     assert np.all(np.abs(cnt / T_mc - v) <= 0.03 + 5 * se)
