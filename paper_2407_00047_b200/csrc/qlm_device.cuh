@@ -77,8 +77,9 @@ constexpr uint32_t kMcTag = 0x4D430000u;
 template <typename TOK>
 __device__ __forceinline__ TOK *fy_elem(uint8_t *base, int i, int blk, int tid) {
     constexpr int EPW = 4 / (int)sizeof(TOK);
-    return reinterpret_cast<TOK *>(base + ((size_t)((i / EPW) * blk + tid) << 2) +
-                                   (i % EPW) * sizeof(TOK));
+    const unsigned u = (unsigned)i;
+    return reinterpret_cast<TOK *>(base + ((size_t)((u / EPW) * (unsigned)blk + (unsigned)tid) << 2) +
+                                   (u % EPW) * sizeof(TOK));
 }
 
 // Forward Fisher-Yates over T tokens (R10); calls f(token) for positions
@@ -113,6 +114,52 @@ __device__ __forceinline__ void tokens_random(uint8_t *scratch, int blk, int tid
                 tok = *pi;
             }
             f(tok);
+        }
+    }
+}
+
+// Forward Fisher-Yates materialised in place: after the call, element s of
+// the thread's scratch row holds token s (the same permutation tokens_random
+// streams).  Used by the two-phase scan (generate, then walk 4 tokens/load).
+template <typename TOK>
+__device__ __forceinline__ void fy_materialise(uint8_t *scratch, int blk, int tid, int T,
+                                               uint64_t seed, uint64_t c) {
+    constexpr int EPW = 4 / (int)sizeof(TOK);
+    uint32_t *w32 = reinterpret_cast<uint32_t *>(scratch);
+    const int nw = (T + EPW - 1) / EPW;
+    for (int w = 0; w < nw; ++w)
+        w32[w * blk + tid] = EPW == 4 ? 0x03020100u + 0x04040404u * (uint32_t)w
+                                      : 0x00010000u + 0x00020002u * (uint32_t)w;
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint32_t clo = (uint32_t)c, chi = (uint32_t)(c >> 32);
+    for (int i0 = 0; i0 < T - 1; i0 += 4) {
+        const uint4 wd = philox10(make_uint4((uint32_t)(i0 >> 2), clo, chi, kRowTag), key);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k;
+            if (i >= T - 1) break;
+            const int j = i + (int)__umulhi(pick4(wd, k), (uint32_t)(T - i));
+            TOK *pi = fy_elem<TOK>(scratch, i, blk, tid);
+            TOK *pj = fy_elem<TOK>(scratch, j, blk, tid);
+            const TOK ti = *pi, tj = *pj;
+            *pj = ti;
+            *pi = tj;
+        }
+    }
+}
+
+// Walk a materialised scratch row: one 32-bit load per EPW tokens.
+template <typename TOK, typename F>
+__device__ __forceinline__ void tokens_scratch(const uint8_t *scratch, int blk, int tid, int T,
+                                               F &&f) {
+    constexpr int EPW = 4 / (int)sizeof(TOK);
+    const uint32_t *w32 = reinterpret_cast<const uint32_t *>(scratch);
+    for (int s0 = 0; s0 < T; s0 += EPW) {
+        const uint32_t w = w32[(s0 / EPW) * blk + tid];
+#pragma unroll
+        for (int k = 0; k < EPW; ++k) {
+            if (s0 + k >= T) break;
+            f(EPW == 4 ? (int)((w >> (8 * k)) & 0xFFu) : (int)((w >> (16 * k)) & 0xFFFFu));
         }
     }
 }
@@ -157,45 +204,68 @@ __device__ __forceinline__ void tokens_enum(uint64_t c, int T, F &&f) {
 // Shared-memory tables of a scan block.  Group records are replicated
 // (1 << rs) times and interleaved so that lane l reads copy l % (1 << rs):
 // with 8 copies a warp's random 16-B reads are bank-conflict free.
+//
+// Transition table (Eq. 9/10, R1/R2/R4): rows p' in [0, 2M) per device:
+//   p' <  M : the previous group ran model p'   -> {m != p' ? tail[d][p'] : 0, swap[d][p'][m]}
+//   p' >= M : nothing has run yet on resident r = p' - M (no backlog)
+//                                               -> {0, swap[d][r][m]}
+// so every slot does A = (A + x) + y with no branch; x = y = 0 when the model
+// does not change, and A + 0.0 == A keeps the arithmetic operation-for-
+// operation identical to the sequential definition.
 struct SlotTables {
     const GRec *sg;        // [G << rs]        {slo, n, model}
     const double2 *sab;    // [(D*G) << rs]    {n mu / Theta, n var / Theta^2}
-    const double2 *str;    // [D*M*M]          {tail[d][prev], swap[d][prev][m]}
+    const double2 *str;    // [D * 2M * M]     {tail part, swap part}
     const QRec *sq;        // [Q]
     int G, Q, M, rs, rl;   // rl = lane & ((1 << rs) - 1)
 };
 
 struct ScanState {
     double A, B;           // exclusive mean / variance accumulators of the queue
-    int q, d, prev, tail_ok;
+    int q, d, prev;        // prev: transition-table row p'
 };
 
 __device__ __forceinline__ void start_queue(const SlotTables &t, ScanState &s, int q) {
     const QRec r = t.sq[q];
-    s.A = r.bmean; s.B = r.bvar; s.d = r.d; s.prev = r.r;
-    s.tail_ok = r.backlog;   // R4/R12: the first switch pays a tail only behind a backlog
+    s.A = r.bmean; s.B = r.bvar; s.d = r.d;
+    s.prev = r.backlog ? r.r : t.M + r.r;   // R4/R12: a tail only behind a pinned backlog
     s.q = q;
 }
 
-// One group slot: returns its (wt, V) and record.  On a model change
-// (t = 1, Eq. 9) the group ahead contributes its completion C = W + tail (R1)
-// and the swap is paid (R2); A + 0.0 == A, so the adds are unconditional and
-// the arithmetic is identical, operation by operation, to the sequential
-// definition.
+// One group slot: returns its (wt, V) and record.
 __device__ __forceinline__ void group_slot(const SlotTables &t, ScanState &s, int tok,
                                            double &wt, double &V, GRec &g) {
     g = t.sg[(tok << t.rs) + t.rl];
     const double2 ab = t.sab[((s.d * t.G + tok) << t.rs) + t.rl];
     const int m = g.model;
-    const double2 tr = t.str[(s.d * t.M + s.prev) * t.M + m];
-    const double tail = (m != s.prev && s.tail_ok) ? tr.x : 0.0;
-    s.A = __dadd_rn(__dadd_rn(s.A, tail), tr.y);     // swap[m][m] == 0
+    const double2 tr = t.str[(s.d * 2 * t.M + s.prev) * t.M + m];
+    s.A = __dadd_rn(__dadd_rn(s.A, tr.x), tr.y);     // C - W of the group ahead, swap S
     wt = s.A;
     V = s.B;                                         // exclusive (R5)
     s.A = __dadd_rn(s.A, ab.x);
     s.B = __dadd_rn(s.B, ab.y);
     s.prev = m;
-    s.tail_ok = 1;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 // Phi-bar(z) = 0.5 erfc(z / sqrt 2) for |z| < z_clamp, fp32, via Abramowitz &
@@ -203,13 +273,23 @@ __device__ __forceinline__ void group_slot(const SlotTables &t, ScanState &s, in
 // fp32 rounding, well inside the 1e-5 parity bar; R8).
 __device__ __forceinline__ float phibar(float z) {
     const float x = fabsf(z) * 0.70710678118654752f;
-    const float t = __fdividef(1.0f, fmaf(0.3275911f, x, 1.0f));
+    const float t = rcp_approx(fmaf(0.3275911f, x, 1.0f));
     float y = fmaf(1.061405429f, t, -1.453152027f);
     y = fmaf(y, t, 1.421413741f);
     y = fmaf(y, t, -0.284496736f);
     y = fmaf(y, t, 0.254829592f);
-    const float h = 0.5f * y * t * __expf(-x * x);
+    const float h = 0.5f * y * t * ex2_approx(-1.4426950408889634f * x * x);
     return z >= 0.0f ? h : 1.0f - h;
+}
+
+// Violation probability of a slot (R8/R9): v = Phi-bar(slack / sqrt V), exactly
+// 0 / 1 when |z| >= z_clamp, tested as slack^2 >= z_clamp^2 V (exact for V = 0,
+// where it reduces to the step [wt > slo]).  `clamped` reports the fast path.
+__device__ __forceinline__ float violation(double slack, double V, double zc2, bool &clamped) {
+    clamped = fma(slack, slack, -zc2 * V) >= 0.0;
+    float v = slack < 0.0 ? 1.0f : 0.0f;
+    if (!clamped) v = phibar((float)slack * rsqrt_approx((float)V));
+    return v;
 }
 
 __device__ __forceinline__ uint64_t make_key(float s1, float s2) {

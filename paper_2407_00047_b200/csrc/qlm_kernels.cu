@@ -12,6 +12,7 @@
 //   mc_count_kernel      a11: per-trial Eq. 10 walk + violation counts
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -95,9 +96,10 @@ enum { OUT_NONE = 0, OUT_STAGED = 1, OUT_DIRECT = 2 };
 template <int KIND, typename TOK, typename F>
 __device__ __forceinline__ void for_tokens(const Cand &cd, int T, uint8_t *scratch, int blk,
                                            int64_t loc, int64_t c, F &&f) {
-    if constexpr (KIND == QLM_CAND_RANDOM)
-        tokens_random<TOK>(scratch, blk, threadIdx.x, T, cd.seed, (uint64_t)c, f);
-    else if constexpr (KIND == QLM_CAND_EXPLICIT)
+    if constexpr (KIND == QLM_CAND_RANDOM) {
+        fy_materialise<TOK>(scratch, blk, threadIdx.x, T, cd.seed, (uint64_t)c);
+        tokens_scratch<TOK>(scratch, blk, threadIdx.x, T, f);
+    } else if constexpr (KIND == QLM_CAND_EXPLICIT)
         tokens_explicit<TOK>(cd.rows + loc * cd.stride, T, f);
     else
         tokens_enum((uint64_t)c, T, f);
@@ -114,9 +116,13 @@ __device__ __forceinline__ SlotTables stage_tables(const ScanParams &p, uint8_t 
     QRec *sq = reinterpret_cast<QRec *>(smem + p.off_q);
     for (int i = tid; i < dm.Q; i += blk) sq[i] = p.tb.qrec[i];
     double2 *str = reinterpret_cast<double2 *>(smem + p.off_tr);
-    for (int i = tid; i < dm.D * dm.M * dm.M; i += blk) {
-        const int dp = i / dm.M;                        // d * M + prev
-        str[i] = make_double2(p.tb.tail[dp], p.tb.swap[i]);
+    const int M = dm.M;
+    for (int i = tid; i < dm.D * 2 * M * M; i += blk) {
+        const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
+        const int from = pp < M ? pp : pp - M;
+        const double sw = p.tb.swap[(d * M + from) * M + m];
+        const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
+        str[i] = make_double2(tl, sw);
     }
     SlotTables t;
     t.sg = sg; t.sab = sab; t.str = str; t.sq = sq;
@@ -148,11 +154,11 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
     const float alpha = p.alpha;
     const int64_t count = cd.count;
     float *const gout[3] = {p.wt, p.sd, p.vo};
-    float *st[3] = {nullptr, nullptr, nullptr};
+    float *st0 = nullptr, *st1 = nullptr, *st2 = nullptr;   // staged tile [3][G][blk]
     if constexpr (OUT == OUT_STAGED) {
-        int k = 0;
-        for (int a = 0; a < 3; ++a)
-            if (gout[a]) st[a] = reinterpret_cast<float *>(smem + p.off_stage) + (size_t)(k++) * G * blk;
+        st0 = reinterpret_cast<float *>(smem + p.off_stage);
+        st1 = st0 + (size_t)G * blk;
+        st2 = st1 + (size_t)G * blk;
     }
     const double den = SCORE ? *p.tb.den : 1.0;
     uint64_t bkey = ~0ull;
@@ -183,26 +189,23 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                 GRec g;
                 group_slot(tab, s, tok, wt, V, g);
                 const double slack = __dsub_rn(g.slo, wt);        // -p_i (Eq. 11)
-                // violation probability (R8/R9): |z| >= z_clamp <=> slack^2 >= z_clamp^2 V
-                const bool clamped = fma(slack, slack, -zc2 * V) >= 0.0;
-                const bool neg = slack < 0.0;
-                float v = neg ? 1.0f : 0.0f;
-                if (!clamped) v = phibar((float)slack * rsqrtf((float)V));
+                bool clamped;
+                const float v = violation(slack, V, zc2, clamped);
                 if constexpr (SCORE) {
                     S2 = __dsub_rn(S2, slack);                    // sum_i p_i
-                    cnt += (clamped && neg) ? g.n : 0;
-                    if (!clamped) frac = fmaf((float)g.n, v, frac);
+                    if (clamped) cnt += v != 0.0f ? g.n : 0;
+                    else frac = fmaf((float)g.n, v, frac);
                     over += v > alpha;
                 }
                 if constexpr (OUT == OUT_STAGED) {
                     const int o = tok * blk + tid;
-                    if (st[0]) st[0][o] = (float)wt;
-                    if (st[1]) st[1][o] = sqrtf((float)V);
-                    if (st[2]) st[2][o] = v;
+                    st0[o] = (float)wt;
+                    st1[o] = sqrt_approx((float)V);
+                    st2[o] = v;
                 } else if constexpr (OUT == OUT_DIRECT) {
                     const int64_t o = (int64_t)tok * count + loc;
                     if (gout[0]) gout[0][o] = (float)wt;
-                    if (gout[1]) gout[1][o] = sqrtf((float)V);
+                    if (gout[1]) gout[1][o] = sqrt_approx((float)V);
                     if (gout[2]) gout[2][o] = v;
                 }
             });
@@ -218,17 +221,15 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
             }
         }
         if constexpr (OUT == OUT_STAGED) {
+            float *const sts[3] = {st0, st1, st2};
             if (p.use_tma) {
                 fence_proxy_async_smem();
                 __syncthreads();
-                const int nrows = p.n_out * G;
-                for (int r = tid; r < nrows; r += blk) {
-                    const int k = r / G, g = r - k * G;
-                    int a = -1;
-                    for (int x = 0, seen = 0; x < 3; ++x)
-                        if (gout[x] && seen++ == k) a = x;
-                    bulk_s2g(gout[a] + (int64_t)g * count + c0, st[a] + (size_t)g * blk,
-                             (uint32_t)nvalid * 4u);
+                for (int r = tid; r < 3 * G; r += blk) {
+                    const int a = r / G, g = r - a * G;
+                    if (gout[a])
+                        bulk_s2g(gout[a] + (int64_t)g * count + c0, sts[a] + (size_t)g * blk,
+                                 (uint32_t)nvalid * 4u);
                 }
                 bulk_commit();
             } else {
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                     for (int a = 0; a < 3; ++a)
                         if (gout[a])
                             for (int g = 0; g < G; ++g)
-                                gout[a][(int64_t)g * count + loc] = st[a][g * blk + tid];
+                                gout[a][(int64_t)g * count + loc] = sts[a][g * blk + tid];
             }
         }
     }
@@ -470,6 +471,11 @@ int sm_count() {
 
 static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
 static const size_t kMaxSmem = 227 * 1024;
 
 // Largest dynamic shared memory a launch of `kern` may use (opt-in limit
@@ -516,14 +522,14 @@ static size_t plan_smem(ScanParams &p, int rep_shift, int kind, int tok_bytes, i
     p.off_grec = (int)off; off = align16(off + ((size_t)dm.G << rep_shift) * sizeof(GRec));
     p.off_ab = (int)off;   off = align16(off + ((size_t)dm.D * dm.G << rep_shift) * sizeof(double2));
     p.off_q = (int)off;    off = align16(off + (size_t)dm.Q * sizeof(QRec));
-    p.off_tr = (int)off;   off = align16(off + (size_t)dm.D * dm.M * dm.M * sizeof(double2));
+    p.off_tr = (int)off;   off = align16(off + (size_t)dm.D * 2 * dm.M * dm.M * sizeof(double2));
     p.off_scratch = (int)off;
     if (kind == QLM_CAND_RANDOM) {
         const int epw = 4 / tok_bytes;
         off = align16(off + (size_t)((dm.T + epw - 1) / epw) * 4 * blk);
     }
     p.off_stage = (int)off;
-    if (out == OUT_STAGED) off = align16(off + (size_t)p.n_out * blk * dm.G * 4);
+    if (out == OUT_STAGED) off = align16(off + (size_t)3 * blk * dm.G * 4);
     return off;
 }
 
@@ -537,20 +543,24 @@ static cudaError_t launch_scan_t(ScanParams p, cudaStream_t st) {
     auto kern = scan_kernel<KIND, TOK, OUT, SCORE>;
     const size_t lim = max_dyn(kern);
     if (!lim) return cudaErrorInvalidConfiguration;
-    // choose (block size, replication) maximising resident candidates per SM
+    // choose (block size, replication) maximising resident candidates per SM;
+    // QLM_BLK / QLM_REP_SHIFT override (tuning sweeps)
     int best_blk = 0, best_rs = 0, best_thr = 0;
     size_t best_smem = 0;
     const int rs0 = default_rep_shift(p.dm);
+    const int env_blk = env_int("QLM_BLK", 0), env_rs = env_int("QLM_REP_SHIFT", -1);
     const int blks[] = {128, 96, 64, 32};
-    for (int rs : {rs0, 0}) {
+    for (int rs : {rs0, rs0 > 2 ? 2 : 0, 0}) {
+        if (env_rs >= 0 && rs != env_rs) continue;
         for (int blk : blks) {
+            if (env_blk && blk != env_blk) continue;
             ScanParams q = p;
             const size_t smem = plan_smem(q, rs, KIND, sizeof(TOK), blk, OUT);
             if (smem > lim) continue;
             const int thr = occupancy(kern, blk, smem) * blk;
             if (thr > best_thr) { best_thr = thr; best_blk = blk; best_rs = rs; best_smem = smem; }
         }
-        if (best_thr >= 256 || (OUT != OUT_STAGED && best_thr)) break;
+        if (best_thr >= 192 || (OUT != OUT_STAGED && best_thr)) break;
     }
     if (!best_blk) return cudaErrorInvalidConfiguration;
     p.blk = best_blk;
@@ -571,7 +581,7 @@ static cudaError_t launch_scan_k(ScanParams &p, cudaStream_t st) {
     p.n_out = (p.wt != nullptr) + (p.sd != nullptr) + (p.vo != nullptr);
     if (p.n_out == 0) return launch_scan_t<KIND, TOK, OUT_NONE, true>(p, st);
     // staged (group-major smem tile + bulk copies) when one fits, else direct stores
-    const size_t stage_bytes = (size_t)p.n_out * 32 * p.dm.G * 4;
+    const size_t stage_bytes = (size_t)3 * 32 * p.dm.G * 4;
     const bool fits = stage_bytes + 64 * 1024 <= kMaxSmem;
     p.use_tma = (p.cd.count % 4 == 0) && (!p.wt || ((uintptr_t)p.wt & 15) == 0) &&
                 (!p.sd || ((uintptr_t)p.sd & 15) == 0) && (!p.vo || ((uintptr_t)p.vo & 15) == 0);

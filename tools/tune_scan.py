@@ -1,0 +1,60 @@
+"""Time the fused scan kernel (qlm_score_estimate) on C3 under launch-config overrides.
+
+    python tools/tune_scan.py            # sweep QLM_BLK x QLM_REP_SHIFT
+Prints one line per config: ms per launch (CUDA events) and GB/s of outputs.
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import __graft_entry__  # noqa: E402
+from paper_2407_00047_b200 import RwtEstimator  # noqa: E402
+from workloads.synth import make_config  # noqa: E402
+
+
+def time_it(fn, reps=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    __graft_entry__.build()
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
+    N = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
+    p = make_config(cfg)
+    est = RwtEstimator(p)
+    cand = est.random(0, N, seed=1)
+    out = {k: torch.empty((p.G, N), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+    rec = torch.empty(2, dtype=torch.int64, device="cuda")
+    byts = 12 * p.G * N
+    configs = [(None, None)] + [(b, r) for b in (128, 96, 64, 32) for r in (3, 2, 0)]
+    for blk, rs in configs:
+        for k, v in (("QLM_BLK", blk), ("QLM_REP_SHIFT", rs)):
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = str(v)
+        try:
+            ms = time_it(lambda: est.score_estimate(cand, out=out, scores=False, rec=rec))
+            ms_s = time_it(lambda: est.best_ordering_async(cand, rec))
+        except Exception as e:  # config does not fit
+            print(f"blk={blk} rs={rs}: {e}")
+            continue
+        print(f"{cfg} blk={blk} rs={rs}: fused {ms:.4f} ms = {byts / ms / 1e6:.1f} GB/s "
+              f"({N / ms / 1e6:.3f} Gcand/s) | score-only {ms_s:.4f} ms ({N / ms_s / 1e6:.3f} Gcand/s)",
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
