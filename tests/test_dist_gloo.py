@@ -1,0 +1,123 @@
+"""World-size-2 gloo tests of the data-parallel plumbing (CPU, no GPU).
+
+Each rank scores its contiguous shard of candidates (here with the oracle,
+standing in for the kernel's per-rank record), the ranks exchange 16-byte
+records with paper_2407_00047_b200.dist.global_best, and the merged winner
+must equal the single-process argmin over all candidates.  MC counts of
+disjoint trial ranges summed with dist.sum_counts must equal one full run.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2407_00047_b200.dist import global_best, shard_range, sum_counts
+from workloads.synth import make_config, balanced_row
+
+
+def pack_key(s1, s2):
+    """Host mirror of the record key (fp32 S1 bits, order-preserving fp32 S2)."""
+    b1 = np.float32(s1).view(np.uint32).astype(np.uint64)
+    f2 = np.float32(s2) + np.float32(0.0)
+    b2 = int(np.float32(f2).view(np.uint32))
+    b2 = (~b2 & 0xFFFFFFFF) if b2 & 0x80000000 else (b2 | 0x80000000)
+    return int((int(b1) << 32) | b2)
+
+
+def to_i64(u):
+    return u - (1 << 64) if u >= 1 << 63 else u
+
+
+def cpu_reduce(recs):
+    """Lexicographic (unsigned key, index) min over gathered records."""
+    r = recs.view(-1, 2).tolist()
+    best = min(r, key=lambda kv: (kv[0] & ((1 << 64) - 1), kv[1] & ((1 << 64) - 1)))
+    return torch.tensor(best, dtype=torch.int64)
+
+
+def local_record(p, first, count):
+    r = O.Oracle(p).score_range(O.RANDOM, first, count, seed=1)
+    i = O.argmin_key(r["s1"], r["s2"])
+    return torch.tensor([to_i64(pack_key(r["s1"][i], r["s2"][i])), first + i], dtype=torch.int64)
+
+
+def _worker(rank, world, port, N, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = make_config("C2")
+        first, count = shard_range(N, rank, world)
+        rec = local_record(p, first, count)
+        g = global_best(rec, cpu_reduce)
+        # MC: disjoint trial ranges, counts summed across ranks
+        p4 = make_config("C4")
+        o4 = O.Oracle(p4)
+        row = balanced_row(p4.G, p4.Q)[None, :]
+        t0, nt = shard_range(60, rank, world)
+        X = o4.mc_sample(2, t0, nt)
+        cnt = torch.tensor(o4.mc_count(O.EXPLICIT, 0, 1, X, rows=row).astype(np.int64))
+        sum_counts(cnt)
+        q.put((rank, g.tolist(), cnt.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_shard_range_partitions():
+    for N in [0, 1, 7, 1000, 10**8 + 3]:
+        for W in [1, 2, 3, 4, 8]:
+            parts = [shard_range(N, r, W) for r in range(W)]
+            assert parts[0][0] == 0
+            assert sum(c for _, c in parts) == N
+            for (f0, c0), (f1, _) in zip(parts, parts[1:]):
+                assert f0 + c0 == f1
+            assert max(c for _, c in parts) - min(c for _, c in parts) <= 1
+
+
+def test_pack_key_orders_lexicographically():
+    rng = np.random.default_rng(0)
+    s1 = rng.choice([0.0, 0.25, 0.5, 1.0], 200)
+    s2 = rng.normal(0, 1e4, 200)
+    s2[:5] = [0.0, -0.0, 1e-30, -1e-30, 5.0]
+    keys = [pack_key(a, b) for a, b in zip(s1, s2)]
+    order_k = sorted(range(200), key=lambda i: (keys[i], i))
+    order_v = sorted(range(200), key=lambda i: (np.float32(s1[i]), np.float32(s2[i]) + np.float32(0), i))
+    assert order_k == order_v
+
+
+def test_two_rank_gloo_global_argmin_and_mc_sum():
+    N, world = 6000, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, N, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = make_config("C2")
+    full = O.Oracle(p).score_range(O.RANDOM, 0, N, seed=1)
+    want = O.argmin_key(full["s1"], full["s2"])
+    for _, g, _ in res:
+        assert g[1] == want
+        assert g[0] == to_i64(pack_key(full["s1"][want], full["s2"][want]))
+    p4 = make_config("C4")
+    o4 = O.Oracle(p4)
+    row = balanced_row(p4.G, p4.Q)[None, :]
+    ref = o4.mc_count(O.EXPLICIT, 0, 1, o4.mc_sample(2, 0, 60), rows=row)
+    for _, _, cnt in res:
+        np.testing.assert_array_equal(cnt, ref.astype(np.int64))
