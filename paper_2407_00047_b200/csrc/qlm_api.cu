@@ -394,7 +394,7 @@ int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, flo
     if (cand->count == 0) return QLM_OK;
     ScanParams p = base_params(ctx, cand);
     p.s1 = s1; p.s2 = s2; p.n_over = n_over;
-    cudaError_t e = launch_scan(p, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_any_scan(p, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score kernel");
 }
 
@@ -412,7 +412,7 @@ int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record
     }
     ScanParams p = base_params(ctx, cand);
     p.out_rec = rec;
-    cudaError_t e = launch_scan(p, st);
+    cudaError_t e = launch_any_scan(p, st);
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score/argmin kernel");
 }
 
@@ -514,7 +514,7 @@ int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
     ScanParams p = base_params(ctx, cand);
     p.wt = wt_mean; p.sd = wt_std; p.vo = viol;
     p.s1 = s1; p.s2 = s2; p.n_over = n_over; p.out_rec = rec;
-    cudaError_t e = launch_scan(p, st);
+    cudaError_t e = launch_any_scan(p, st);
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "scan kernel");
 }
 

@@ -595,6 +595,13 @@ static cudaError_t launch_scan_k(ScanParams &p, cudaStream_t st) {
                  : launch_scan_t<KIND, TOK, OUT_DIRECT, false>(p, st);
 }
 
+cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st) {
+    cudaError_t e = launch_ws(p, st);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+    return launch_scan(p, st);
+}
+
 cudaError_t launch_scan(ScanParams p, cudaStream_t st) {
     switch (p.cd.kind) {
     case QLM_CAND_RANDOM:

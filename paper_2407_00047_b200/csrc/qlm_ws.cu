@@ -1,0 +1,434 @@
+// qlm_ws.cu -- warp-specialised scan kernel (the bulk fast path on sm_100a).
+//
+// A block holds W producer/consumer warp pairs.  Work unit = a batch of 32
+// consecutive candidates.  Pair p of a block takes the block's batches
+// p, p+W, p+2W, ... and double-buffers them through two row slots in shared
+// memory:
+//
+//   producer warp  -- generates the batch's 32 candidate rows (Philox +
+//                     Fisher-Yates, Lehmer unranking, or a copy of EXPLICIT
+//                     rows), one row per lane, in place in the slot;
+//                     mbarrier full[slot]
+//   consumer warp  -- walks each row once (Eq. 2/3/10, R1-R7), violation
+//                     probability (R8/R9), S1/S2 (R11) and the argmin; stages
+//                     wt / sd / v group-major in its own smem tile [3][G][32]
+//                     (bank = lane) and writes each array with ONE 2-D TMA
+//                     tensor store (box {32 candidates, G groups}) into the
+//                     group-major outputs; mbarrier empty[slot]
+//
+// Row generation is a chain of dependent shared-memory swaps; the scan is a
+// chain of dependent fp64 adds.  Splitting them across warps lets each hide
+// the other's latency with only ~7 consumer tiles resident (the staging
+// tiles are what fills shared memory).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "qlm_device.cuh"
+#include "qlm_launch.h"
+
+namespace qlm {
+
+struct alignas(64) WsParams {
+    CUtensorMap tmap[3];   // wt, sd, v: fp32 [G][count], box {32, G}
+    ScanParams p;
+    int pairs;             // W
+    int tw;                // 32-bit words per row slot column
+    int off_rows, off_stage, off_bar;
+    int stage_floats;      // per consumer warp: 3 * G * 32
+    int use_tma;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, const void *src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                 ::"l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
+}
+
+// Row generation of one candidate into the lane's column of a row slot.
+template <int KIND, typename TOK>
+__device__ __forceinline__ void produce_row(const Cand &cd, int T, uint8_t *slot, int lane,
+                                            int64_t loc, int64_t c) {
+    if constexpr (KIND == QLM_CAND_RANDOM) {
+        fy_materialise<TOK>(slot, 32, lane, T, cd.seed, (uint64_t)c);
+    } else if constexpr (KIND == QLM_CAND_ENUM) {
+        int s = 0;
+        tokens_enum((uint64_t)c, T, [&](int tok) { *fy_elem<TOK>(slot, s++, 32, lane) = (TOK)tok; });
+    } else {
+        int s = 0;
+        const uint8_t *row = cd.rows + loc * cd.stride;
+        auto put = [&](int tok) { *fy_elem<TOK>(slot, s++, 32, lane) = (TOK)tok; };
+        if (cd.tb == 1) tokens_explicit<uint8_t>(row, T, put);
+        else tokens_explicit<uint16_t>(row, T, put);
+    }
+}
+
+// Warp -> block -> grid (last block) lexicographic argmin (R11/R14).
+__device__ __forceinline__ void block_grid_argmin(const ScanParams &p, uint64_t bkey, int64_t bidx) {
+    __shared__ uint64_t rk[32];
+    __shared__ int64_t ri[32];
+    __shared__ int is_last;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarp = blockDim.x >> 5;
+    warp_argmin(bkey, bidx);
+    if (lane == 0) { rk[wid] = bkey; ri[wid] = bidx; }
+    __syncthreads();
+    if (wid == 0) {
+        uint64_t k = lane < nwarp ? rk[lane] : ~0ull;
+        int64_t i = lane < nwarp ? ri[lane] : -1;
+        warp_argmin(k, i);
+        if (lane == 0) {
+            p.block_recs[blockIdx.x].key = k;
+            p.block_recs[blockIdx.x].index = i;
+            __threadfence();
+            is_last = atomicAdd(p.counter, 1u) == gridDim.x - 1;
+        }
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    uint64_t k = ~0ull;
+    int64_t i = -1;
+    for (int j = tid; j < (int)gridDim.x; j += blockDim.x) {
+        const uint64_t kk = __ldcg(reinterpret_cast<const unsigned long long *>(&p.block_recs[j].key));
+        const int64_t ii = __ldcg(reinterpret_cast<const long long *>(&p.block_recs[j].index));
+        if (better(kk, ii, k, i)) { k = kk; i = ii; }
+    }
+    warp_argmin(k, i);
+    __syncthreads();
+    if (lane == 0) { rk[wid] = k; ri[wid] = i; }
+    __syncthreads();
+    if (wid == 0) {
+        k = lane < nwarp ? rk[lane] : ~0ull;
+        i = lane < nwarp ? ri[lane] : -1;
+        warp_argmin(k, i);
+        if (lane == 0) {
+            p.out_rec->key = k;
+            p.out_rec->index = i;
+            *p.counter = 0u;
+        }
+    }
+}
+
+template <int KIND, typename TOK, bool STAGE, bool SCORE>
+__global__ void __launch_bounds__(STAGE ? 512 : 1024, 1) ws_kernel(const __grid_constant__ WsParams w) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const ScanParams &p = w.p;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = w.pairs;
+    const int G = p.dm.G, Q = p.dm.Q, T = p.dm.T;
+
+    // ---- tables -> smem (replicated group records, transition rows, queues)
+    const int rs = p.rep_shift;
+    GRec *sg = reinterpret_cast<GRec *>(smem + p.off_grec);
+    for (int i = tid; i < (G << rs); i += blockDim.x) sg[i] = p.tb.grec[i >> rs];
+    double2 *sab = reinterpret_cast<double2 *>(smem + p.off_ab);
+    for (int i = tid; i < ((p.dm.D * G) << rs); i += blockDim.x) sab[i] = p.tb.ab[i >> rs];
+    QRec *sq = reinterpret_cast<QRec *>(smem + p.off_q);
+    for (int i = tid; i < Q; i += blockDim.x) sq[i] = p.tb.qrec[i];
+    double2 *str = reinterpret_cast<double2 *>(smem + p.off_tr);
+    const int M = p.dm.M;
+    for (int i = tid; i < p.dm.D * 2 * M * M; i += blockDim.x) {
+        const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
+        const int from = pp < M ? pp : pp - M;
+        const double sw = p.tb.swap[(d * M + from) * M + m];
+        const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
+        str[i] = make_double2(tl, sw);
+    }
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + w.off_bar);
+    uint64_t *empty = full + 2 * W;
+    if (tid < 2 * W) {
+        mbar_init(&full[tid], 32);
+        mbar_init(&empty[tid], 32);
+    }
+    __syncthreads();
+
+    const Cand cd = p.cd;
+    const int64_t count = cd.count, first = cd.first;
+    const int64_t nbatch = (count + 31) >> 5;
+    const int pair = warp % W;
+    const bool producer = warp >= W;
+    const int64_t grid = gridDim.x;
+    uint64_t bkey = ~0ull;
+    int64_t bidx = -1;
+
+    if (producer) {
+        for (int j = 0;; ++j) {
+            const int64_t b = blockIdx.x + (int64_t)(pair + j * W) * grid;
+            if (b >= nbatch) break;
+            const int s = 2 * pair + (j & 1);
+            mbar_wait(&empty[s], ((j >> 1) & 1) ^ 1);
+            const int64_t loc = (b << 5) + lane;
+            uint8_t *slot = smem + w.off_rows + (size_t)s * w.tw * 128;
+            if (loc < count) produce_row<KIND, TOK>(cd, T, slot, lane, loc, first + loc);
+            mbar_arrive(&full[s]);
+        }
+    } else {
+        SlotTables tab;
+        tab.sg = sg; tab.sab = sab; tab.str = str; tab.sq = sq;
+        tab.G = G; tab.Q = Q; tab.M = M; tab.rs = rs; tab.rl = lane & ((1 << rs) - 1);
+        const double zc2 = p.zc2;
+        const float alpha = p.alpha;
+        const double den = SCORE ? *p.tb.den : 1.0;
+        float *st = reinterpret_cast<float *>(smem + w.off_stage) + (size_t)pair * w.stage_floats;
+        float *st0 = st, *st1 = st + G * 32, *st2 = st + 2 * G * 32;
+        for (int j = 0;; ++j) {
+            const int64_t b = blockIdx.x + (int64_t)(pair + j * W) * grid;
+            if (b >= nbatch) break;
+            const int s = 2 * pair + (j & 1);
+            mbar_wait(&full[s], (j >> 1) & 1);
+            if constexpr (STAGE) {
+                if (j > 0 && w.use_tma) {
+                    if (lane == 0) bulk_wait_read0();          // previous tile read out
+                    __syncwarp();
+                }
+            }
+            const int64_t c0 = b << 5, loc = c0 + lane;
+            const uint8_t *slot = smem + w.off_rows + (size_t)s * w.tw * 128;
+            if (loc < count) {
+                ScanState sst;
+                start_queue(tab, sst, 0);
+                double S2 = 0.0;
+                float frac = 0.0f;
+                int cnt = 0, over = 0;
+                tokens_scratch<TOK>(slot, 32, lane, T, [&](int tok) {
+                    if (tok >= G) {                             // queue separator
+                        start_queue(tab, sst, sst.q + 1 < Q ? sst.q + 1 : Q - 1);
+                        return;
+                    }
+                    double wt, V;
+                    GRec g;
+                    group_slot(tab, sst, tok, wt, V, g);
+                    const double slack = __dsub_rn(g.slo, wt);
+                    bool clamped;
+                    const float v = violation(slack, V, zc2, clamped);
+                    if constexpr (SCORE) {
+                        S2 = __dsub_rn(S2, slack);
+                        if (clamped) cnt += v != 0.0f ? g.n : 0;
+                        else frac = fmaf((float)g.n, v, frac);
+                        over += v > alpha;
+                    }
+                    if constexpr (STAGE) {
+                        const int o = tok * 32 + lane;
+                        st0[o] = (float)wt;
+                        st1[o] = sqrt_approx((float)V);
+                        st2[o] = v;
+                    }
+                });
+                if constexpr (SCORE) {
+                    const float s1 = (float)(__dadd_rn((double)cnt, (double)frac) / den);
+                    const float s2 = (float)S2;
+                    if (p.s1) p.s1[loc] = s1;
+                    if (p.s2) p.s2[loc] = s2;
+                    if (p.n_over) p.n_over[loc] = over;
+                    const uint64_t key = make_key(s1, s2);
+                    const int64_t c = first + loc;
+                    if (better(key, c, bkey, bidx)) { bkey = key; bidx = c; }
+                }
+            }
+            mbar_arrive(&empty[s]);                              // row slot free
+            if constexpr (STAGE) {
+                if (w.use_tma) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (p.wt) tma_store_2d(&w.tmap[0], st0, (int)c0, 0);
+                        if (p.sd) tma_store_2d(&w.tmap[1], st1, (int)c0, 0);
+                        if (p.vo) tma_store_2d(&w.tmap[2], st2, (int)c0, 0);
+                        bulk_commit();
+                    }
+                } else {
+                    __syncwarp();
+                    if (loc < count) {
+                        for (int g = 0; g < G; ++g) {
+                            const int64_t o = (int64_t)g * count + loc;
+                            if (p.wt) p.wt[o] = st0[g * 32 + lane];
+                            if (p.sd) p.sd[o] = st1[g * 32 + lane];
+                            if (p.vo) p.vo[o] = st2[g * 32 + lane];
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if constexpr (STAGE) {
+            if (w.use_tma && lane == 0) bulk_wait0();
+        }
+    }
+    if constexpr (SCORE) {
+        if (p.out_rec) block_grid_argmin(p, bkey, bidx);   // all warps take part
+    }
+}
+
+// ---- host side ----------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+static bool make_map(CUtensorMap *tm, float *ptr, int64_t count, int G) {
+    auto fn = encode_fn();
+    if (!fn || !ptr) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)count, (cuuint64_t)G};
+    const cuuint64_t strides[1] = {(cuuint64_t)count * 4};
+    const cuuint32_t box[2] = {32, (cuuint32_t)G};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+static size_t a1k(size_t x) { return (x + 1023) & ~size_t(1023); }
+
+static int env_int_ws(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+// Shared-memory plan for W pairs; returns total bytes.
+static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
+    ScanParams &p = w.p;
+    const Dims &dm = p.dm;
+    size_t off = 0;
+    p.rep_shift = rs;
+    p.off_grec = (int)off; off = a16(off + ((size_t)dm.G << rs) * sizeof(GRec));
+    p.off_ab = (int)off;   off = a16(off + ((size_t)dm.D * dm.G << rs) * sizeof(double2));
+    p.off_q = (int)off;    off = a16(off + (size_t)dm.Q * sizeof(QRec));
+    p.off_tr = (int)off;   off = a16(off + (size_t)dm.D * 2 * dm.M * dm.M * sizeof(double2));
+    const int epw = 4 / tok_bytes;
+    w.tw = (dm.T + epw - 1) / epw;
+    w.off_rows = (int)off; off = a16(off + (size_t)2 * W * w.tw * 128);
+    w.off_bar = (int)off;  off = a16(off + (size_t)4 * W * 8);
+    w.stage_floats = stage ? 3 * dm.G * 32 : 0;
+    off = a1k(off);
+    w.off_stage = (int)off;
+    off += (size_t)W * w.stage_floats * 4;
+    w.pairs = W;
+    return off;
+}
+
+template <typename K>
+static size_t ws_max_dyn(K kern) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) { cudaGetLastError(); return 0; }
+    const size_t m = optin > (int)fa.sharedSizeBytes + 1024 ? (size_t)optin - fa.sharedSizeBytes - 1024 : 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return m;
+}
+
+template <int KIND, typename TOK, bool STAGE, bool SCORE>
+static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
+    auto kern = ws_kernel<KIND, TOK, STAGE, SCORE>;
+    static size_t lim = 0;
+    if (!lim) lim = ws_max_dyn(kern);
+    if (!lim) return cudaErrorNotSupported;
+    WsParams w;
+    memset(&w, 0, sizeof w);
+    w.p = p0;
+    const int maxW = STAGE ? 8 : 16;
+    const int envW = env_int_ws("QLM_WS_PAIRS", 0), envRs = env_int_ws("QLM_REP_SHIFT", -1);
+    int bestW = 0, bestRs = 0;
+    size_t bestSmem = 0;
+    for (int rs : {3, 2, 0}) {
+        if (envRs >= 0 && rs != envRs) continue;
+        for (int W = maxW; W >= 1; --W) {
+            if (envW && W != envW) continue;
+            WsParams t = w;
+            const size_t sm = plan_ws(t, W, rs, sizeof(TOK), STAGE);
+            if (sm <= lim) {
+                if (W > bestW) { bestW = W; bestRs = rs; bestSmem = sm; }
+                break;
+            }
+        }
+        if (bestW >= (STAGE ? 6 : 16)) break;
+    }
+    if (bestW < (STAGE ? 2 : 4)) return cudaErrorNotSupported;
+    plan_ws(w, bestW, bestRs, sizeof(TOK), STAGE);
+    if (STAGE) {
+        const bool aligned = (p0.cd.count % 4 == 0) && (!p0.wt || ((uintptr_t)p0.wt & 15) == 0) &&
+                             (!p0.sd || ((uintptr_t)p0.sd & 15) == 0) &&
+                             (!p0.vo || ((uintptr_t)p0.vo & 15) == 0) && p0.dm.G <= 256;
+        bool ok = aligned;
+        if (ok && p0.wt) ok = make_map(&w.tmap[0], p0.wt, p0.cd.count, p0.dm.G);
+        if (ok && p0.sd) ok = make_map(&w.tmap[1], p0.sd, p0.cd.count, p0.dm.G);
+        if (ok && p0.vo) ok = make_map(&w.tmap[2], p0.vo, p0.cd.count, p0.dm.G);
+        w.use_tma = ok ? 1 : 0;
+    }
+    const int64_t nbatch = (p0.cd.count + 31) / 32;
+    int64_t grid = sm_count();
+    const int64_t need = (nbatch + bestW - 1) / bestW;
+    if (grid > need) grid = need;
+    if (grid > p0.max_blocks) grid = p0.max_blocks;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, 64 * bestW, bestSmem, st>>>(w);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+template <int KIND, typename TOK>
+static cudaError_t launch_ws_k(ScanParams &p, cudaStream_t st) {
+    const bool score = p.s1 || p.s2 || p.n_over || p.out_rec;
+    const bool stage = p.wt || p.sd || p.vo;
+    if (stage) {
+        if ((size_t)3 * p.dm.G * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
+        return score ? launch_ws_t<KIND, TOK, true, true>(p, st) : launch_ws_t<KIND, TOK, true, false>(p, st);
+    }
+    return launch_ws_t<KIND, TOK, false, true>(p, st);
+}
+
+// Fast path for large candidate sets; cudaErrorNotSupported -> caller falls back.
+cudaError_t launch_ws(ScanParams p, cudaStream_t st) {
+    if (p.cd.first_from || p.cd.count < 4096 || env_int_ws("QLM_NO_WS", 0)) return cudaErrorNotSupported;
+    switch (p.cd.kind) {
+    case QLM_CAND_RANDOM:
+        return p.dm.T <= 256 ? launch_ws_k<QLM_CAND_RANDOM, uint8_t>(p, st)
+                             : launch_ws_k<QLM_CAND_RANDOM, uint16_t>(p, st);
+    case QLM_CAND_EXPLICIT:
+        return p.dm.T <= 256 ? launch_ws_k<QLM_CAND_EXPLICIT, uint8_t>(p, st)
+                             : launch_ws_k<QLM_CAND_EXPLICIT, uint16_t>(p, st);
+    default:
+        return launch_ws_k<QLM_CAND_ENUM, uint8_t>(p, st);
+    }
+}
+
+}  // namespace qlm

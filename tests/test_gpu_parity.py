@@ -328,3 +328,42 @@ def test_mc_close_to_gaussian():
     v = out["v"].cpu().numpy()[:, 0]
     se = np.sqrt(np.maximum(v * (1 - v), 1e-4) / T_mc)
     assert np.all(np.abs(cnt / T_mc - v) <= 0.03 + 5 * se)
+
+
+@pytest.mark.parametrize("cfg,n,kind", [("C3", 50_000, "random"), ("C2", 40_001, "random"),
+                                         ("C4", 8192, "random"), ("C3", 9000, "explicit"),
+                                         ("C1", 24, "enum")])
+def test_warp_specialised_and_fallback_kernels_agree(cfg, n, kind, monkeypatch):
+    """The warp-specialised fast path (qlm_ws.cu) and the general scan kernel
+    compute identical bits, and both match the oracle."""
+    p = make_config(cfg)
+    e = est_of(p)
+    if kind == "random":
+        cand = e.random(5, n, seed=1)
+    elif kind == "enum":
+        cand = e.enum(0, n)
+    else:
+        rows = np.stack([O.random_row(3, c, p.T) for c in range(n)])
+        cand = e.explicit(rows_tensor(rows, token_bytes=p.token_bytes))
+    res = {}
+    for no_ws in ("1", "0"):
+        monkeypatch.setenv("QLM_NO_WS", no_ws)
+        rec = torch.empty(2, dtype=torch.int64, device="cuda")
+        bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+        bufs["n_over"] = torch.empty(n, dtype=torch.int32, device="cuda")
+        res[no_ws] = (e.score_estimate(cand, out=bufs, rec=rec), rec)
+    (a, ra), (b, rb) = res["1"], res["0"]
+    for k in ("wt", "sd", "v", "s1", "s2", "n_over"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(ra, rb)
+    m = min(n, 2000)
+    if kind == "explicit":
+        ref = O.Oracle(p).score_range(O.EXPLICIT, 0, m, rows=rows[:m].astype(np.uint8))
+        est = O.Oracle(p).estimate_range(O.EXPLICIT, 0, m, rows=rows[:m].astype(np.uint8))
+    else:
+        k_ = O.RANDOM if kind == "random" else O.ENUM
+        first = 5 if kind == "random" else 0
+        ref = O.Oracle(p).score_range(k_, first, m, seed=1)
+        est = O.Oracle(p).estimate_range(k_, first, m, seed=1)
+    check_scores(b["s1"][:m].cpu().numpy(), b["s2"][:m].cpu().numpy(), ref, p)
+    check_estimates({k: b[k][:, :m] for k in ("wt", "sd", "v")}, est)

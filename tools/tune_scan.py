@@ -38,9 +38,13 @@ def main():
     out = {k: torch.empty((p.G, N), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
     rec = torch.empty(2, dtype=torch.int64, device="cuda")
     byts = 12 * p.G * N
-    configs = [(None, None)] + [(b, r) for b in (128, 96, 64, 32) for r in (3, 2, 0)]
-    for blk, rs in configs:
-        for k, v in (("QLM_BLK", blk), ("QLM_REP_SHIFT", rs)):
+    configs = [dict()] + [dict(QLM_WS_PAIRS=w_, QLM_REP_SHIFT=r) for w_ in (8, 7, 6, 5, 4)
+                          for r in (3, 0)] + \
+        [dict(QLM_NO_WS=1, QLM_BLK=b, QLM_REP_SHIFT=r) for b in (128, 96) for r in (3, 0)]
+    keys = ("QLM_WS_PAIRS", "QLM_REP_SHIFT", "QLM_NO_WS", "QLM_BLK")
+    for cfgd in configs:
+        blk, rs = cfgd, ""
+        for k, v in ((k, cfgd.get(k)) for k in keys):
             if v is None:
                 os.environ.pop(k, None)
             else:
@@ -49,9 +53,9 @@ def main():
             ms = time_it(lambda: est.score_estimate(cand, out=out, scores=False, rec=rec))
             ms_s = time_it(lambda: est.best_ordering_async(cand, rec))
         except Exception as e:  # config does not fit
-            print(f"blk={blk} rs={rs}: {e}")
+            print(f"{blk}: {e}")
             continue
-        print(f"{cfg} blk={blk} rs={rs}: fused {ms:.4f} ms = {byts / ms / 1e6:.1f} GB/s "
+        print(f"{cfg} {blk}: fused {ms:.4f} ms = {byts / ms / 1e6:.1f} GB/s "
               f"({N / ms / 1e6:.3f} Gcand/s) | score-only {ms_s:.4f} ms ({N / ms_s / 1e6:.3f} Gcand/s)",
               flush=True)
 
