@@ -199,13 +199,15 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                 }
                 if constexpr (OUT == OUT_STAGED) {
                     const int o = tok * blk + tid;
+                    const float Vf = (float)V;
                     st0[o] = (float)wt;
-                    st1[o] = sqrt_approx((float)V);
+                    st1[o] = Vf >= 1.17549435e-38f ? Vf * rsqrt_approx(Vf) : 0.0f;
                     st2[o] = v;
                 } else if constexpr (OUT == OUT_DIRECT) {
                     const int64_t o = (int64_t)tok * count + loc;
+                    const float Vf = (float)V;
                     if (gout[0]) gout[0][o] = (float)wt;
-                    if (gout[1]) gout[1][o] = sqrt_approx((float)V);
+                    if (gout[1]) gout[1][o] = Vf >= 1.17549435e-38f ? Vf * rsqrt_approx(Vf) : 0.0f;
                     if (gout[2]) gout[2][o] = v;
                 }
             });

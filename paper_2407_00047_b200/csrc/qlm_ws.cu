@@ -88,6 +88,99 @@ __device__ __forceinline__ void produce_row(const Cand &cd, int T, uint8_t *slot
     }
 }
 
+// Branch-free consumer of one 32-bit word of a row (K = 4 / sizeof(TOK)
+// tokens).  Separators are handled with selects (a separator slot computes a
+// throw-away group slot and then resets the queue state), so the K slots of a
+// word are straight-line code: all shared-memory loads of the word are issued
+// before its fp64 chain, and its staging stores come last.  Staging offsets
+// of separator slots point at a trash row (row G of each staged array).
+struct Acc {
+    double A, B, S2;
+    float frac;
+    int d, prev, q, cnt, over;
+};
+
+template <typename TOK, bool STAGE, bool SCORE>
+__device__ __forceinline__ void consume_word(const SlotTables &t, uint32_t word, int nvalid_tok,
+                                             int G, int Q, int M, int lane, double zc2,
+                                             float alpha, float *st, int arr_stride, Acc &a) {
+    constexpr int K = 4 / (int)sizeof(TOK);
+    int tok[K], isbar[K], tg[K], qn[K];
+    GRec g[K];
+    QRec r[K];
+    // (i) tokens, separators, group and queue records (independent loads)
+    int q = a.q;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        tok[k] = K == 4 ? (int)((word >> (8 * k)) & 0xFFu) : (int)((word >> (16 * k)) & 0xFFFFu);
+        if (k >= nvalid_tok) tok[k] = G;          // padding past T: treat as a no-op separator
+        isbar[k] = tok[k] >= G;
+        tg[k] = isbar[k] ? 0 : tok[k];
+        qn[k] = q + isbar[k] < Q ? q + isbar[k] : Q - 1;
+        if (k >= nvalid_tok) qn[k] = q;
+        q = qn[k];
+        g[k] = t.sg[(tg[k] << t.rs) + t.rl];
+        r[k] = t.sq[qn[k]];
+    }
+    // (ii) per-slot device and previous-model row
+    int dk[K], pk[K];
+    int d = a.d, prev = a.prev;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        dk[k] = d;
+        pk[k] = prev;
+        const int bar_prev = r[k].backlog ? r[k].r : M + r[k].r;
+        const int pad = k >= nvalid_tok;
+        d = (isbar[k] && !pad) ? r[k].d : d;
+        prev = pad ? prev : (isbar[k] ? bar_prev : g[k].model);
+    }
+    // (iii) per-device group work and transition costs
+    double2 ab[K], tr[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        ab[k] = t.sab[((dk[k] * G + tg[k]) << t.rs) + t.rl];
+        tr[k] = t.str[(dk[k] * 2 * M + pk[k]) * M + g[k].model];
+    }
+    // (iv) the Eq. 10 chain (operation order identical to the sequential definition)
+    double wt[K], V[K];
+    double A = a.A, B = a.B;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double A1 = __dadd_rn(__dadd_rn(A, tr[k].x), tr[k].y);
+        wt[k] = A1;
+        V[k] = B;
+        const double A2 = __dadd_rn(A1, ab[k].x), B2 = __dadd_rn(B, ab[k].y);
+        const bool reset = isbar[k] && k < nvalid_tok;
+        A = reset ? r[k].bmean : (k < nvalid_tok ? A2 : A);
+        B = reset ? r[k].bvar : (k < nvalid_tok ? B2 : B);
+    }
+    a.A = A; a.B = B; a.d = d; a.prev = prev; a.q = q;
+    // (v) violation probabilities, scores, staging
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double slack = __dsub_rn(g[k].slo, wt[k]);
+        const bool clamped = fma(slack, slack, -zc2 * V[k]) >= 0.0;
+        const bool neg = slack < 0.0;
+        const float Vf = (float)V[k];
+        const float rr = rsqrt_approx(Vf);
+        const float pz = phibar((float)slack * rr);
+        const float v = clamped ? (neg ? 1.0f : 0.0f) : pz;
+        const bool grp = !isbar[k];
+        if constexpr (SCORE) {
+            a.S2 = grp ? __dsub_rn(a.S2, slack) : a.S2;
+            a.cnt += (grp && clamped && neg) ? g[k].n : 0;
+            a.frac = (grp && !clamped) ? fmaf((float)g[k].n, v, a.frac) : a.frac;
+            a.over += (grp && v > alpha) ? 1 : 0;
+        }
+        if constexpr (STAGE) {
+            const int o = (grp ? tg[k] : G) * 32 + lane;
+            st[o] = (float)wt[k];
+            st[arr_stride + o] = Vf >= 1.17549435e-38f ? Vf * rr : 0.0f;
+            st[2 * arr_stride + o] = v;
+        }
+    }
+}
+
 // Warp -> block -> grid (last block) lexicographic argmin (R11/R14).
 __device__ __forceinline__ void block_grid_argmin(const ScanParams &p, uint64_t bkey, int64_t bidx) {
     __shared__ uint64_t rk[32];
@@ -195,7 +288,7 @@ __global__ void __launch_bounds__(STAGE ? 512 : 1024, 1) ws_kernel(const __grid_
         const float alpha = p.alpha;
         const double den = SCORE ? *p.tb.den : 1.0;
         float *st = reinterpret_cast<float *>(smem + w.off_stage) + (size_t)pair * w.stage_floats;
-        float *st0 = st, *st1 = st + G * 32, *st2 = st + 2 * G * 32;
+        float *st0 = st, *st1 = st + (G + 1) * 32, *st2 = st + 2 * (G + 1) * 32;
         for (int j = 0;; ++j) {
             const int64_t b = blockIdx.x + (int64_t)(pair + j * W) * grid;
             if (b >= nbatch) break;
@@ -210,41 +303,27 @@ __global__ void __launch_bounds__(STAGE ? 512 : 1024, 1) ws_kernel(const __grid_
             const int64_t c0 = b << 5, loc = c0 + lane;
             const uint8_t *slot = smem + w.off_rows + (size_t)s * w.tw * 128;
             if (loc < count) {
-                ScanState sst;
-                start_queue(tab, sst, 0);
-                double S2 = 0.0;
-                float frac = 0.0f;
-                int cnt = 0, over = 0;
-                tokens_scratch<TOK>(slot, 32, lane, T, [&](int tok) {
-                    if (tok >= G) {                             // queue separator
-                        start_queue(tab, sst, sst.q + 1 < Q ? sst.q + 1 : Q - 1);
-                        return;
-                    }
-                    double wt, V;
-                    GRec g;
-                    group_slot(tab, sst, tok, wt, V, g);
-                    const double slack = __dsub_rn(g.slo, wt);
-                    bool clamped;
-                    const float v = violation(slack, V, zc2, clamped);
-                    if constexpr (SCORE) {
-                        S2 = __dsub_rn(S2, slack);
-                        if (clamped) cnt += v != 0.0f ? g.n : 0;
-                        else frac = fmaf((float)g.n, v, frac);
-                        over += v > alpha;
-                    }
-                    if constexpr (STAGE) {
-                        const int o = tok * 32 + lane;
-                        st0[o] = (float)wt;
-                        st1[o] = sqrt_approx((float)V);
-                        st2[o] = v;
-                    }
-                });
+                Acc a;
+                {
+                    const QRec r0 = sq[0];
+                    a.A = r0.bmean; a.B = r0.bvar; a.d = r0.d;
+                    a.prev = r0.backlog ? r0.r : M + r0.r;
+                }
+                a.q = 0; a.S2 = 0.0; a.frac = 0.0f; a.cnt = 0; a.over = 0;
+                constexpr int EPW = 4 / (int)sizeof(TOK);
+                const uint32_t *w32 = reinterpret_cast<const uint32_t *>(slot);
+                const int tw = w.tw;
+                for (int wi = 0; wi < tw; ++wi) {
+                    const uint32_t word = w32[wi * 32 + lane];
+                    consume_word<TOK, STAGE, SCORE>(tab, word, T - wi * EPW, G, Q, M, lane, zc2, alpha,
+                                                    st, (G + 1) * 32, a);
+                }
                 if constexpr (SCORE) {
-                    const float s1 = (float)(__dadd_rn((double)cnt, (double)frac) / den);
-                    const float s2 = (float)S2;
+                    const float s1 = (float)(__dadd_rn((double)a.cnt, (double)a.frac) / den);
+                    const float s2 = (float)a.S2;
                     if (p.s1) p.s1[loc] = s1;
                     if (p.s2) p.s2[loc] = s2;
-                    if (p.n_over) p.n_over[loc] = over;
+                    if (p.n_over) p.n_over[loc] = a.over;
                     const uint64_t key = make_key(s1, s2);
                     const int64_t c = first + loc;
                     if (better(key, c, bkey, bidx)) { bkey = key; bidx = c; }
@@ -333,7 +412,7 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
     w.tw = (dm.T + epw - 1) / epw;
     w.off_rows = (int)off; off = a16(off + (size_t)2 * W * w.tw * 128);
     w.off_bar = (int)off;  off = a16(off + (size_t)4 * W * 8);
-    w.stage_floats = stage ? 3 * dm.G * 32 : 0;
+    w.stage_floats = stage ? 3 * (dm.G + 1) * 32 : 0;
     off = a1k(off);
     w.off_stage = (int)off;
     off += (size_t)W * w.stage_floats * 4;
@@ -409,8 +488,9 @@ template <int KIND, typename TOK>
 static cudaError_t launch_ws_k(ScanParams &p, cudaStream_t st) {
     const bool score = p.s1 || p.s2 || p.n_over || p.out_rec;
     const bool stage = p.wt || p.sd || p.vo;
+    if (!stage) return cudaErrorNotSupported;   // score-only: the one-warp-per-32-candidates kernel is faster
     if (stage) {
-        if ((size_t)3 * p.dm.G * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
+        if ((size_t)3 * (p.dm.G + 1) * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
         return score ? launch_ws_t<KIND, TOK, true, true>(p, st) : launch_ws_t<KIND, TOK, true, false>(p, st);
     }
     return launch_ws_t<KIND, TOK, false, true>(p, st);
