@@ -283,12 +283,15 @@ __device__ __forceinline__ float phibar(float z) {
 }
 
 // Violation probability of a slot (R8/R9): v = Phi-bar(slack / sqrt V), exactly
-// 0 / 1 when |z| >= z_clamp, tested as slack^2 >= z_clamp^2 V (exact for V = 0,
-// where it reduces to the step [wt > slo]).  `clamped` reports the fast path.
+// 0 / 1 when |z| >= z_clamp, tested as slack^2 >= z_clamp^2 V in fp32 (exact
+// for V = 0, where it reduces to the step [wt > slo]; near |z| = z_clamp the
+// two forms can differ only where Phi-bar < 1e-15).  `clamped` reports the
+// fast path.
 __device__ __forceinline__ float violation(double slack, double V, double zc2, bool &clamped) {
-    clamped = fma(slack, slack, -zc2 * V) >= 0.0;
+    const float sf = (float)slack, Vf = (float)V;
+    clamped = sf * sf >= (float)zc2 * Vf;
     float v = slack < 0.0 ? 1.0f : 0.0f;
-    if (!clamped) v = phibar((float)slack * rsqrt_approx((float)V));
+    if (!clamped) v = phibar(sf * rsqrt_approx(Vf));
     return v;
 }
 

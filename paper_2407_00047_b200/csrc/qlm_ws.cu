@@ -56,12 +56,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
         "{\n"
         ".reg .pred P1;\n"
         "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@P1 bra DONE;\n"
         "bra LAB_WAIT;\n"
         "DONE:\n"
         "}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, const void *src, int x, int y) {
@@ -100,39 +100,41 @@ struct Acc {
     int d, prev, q, cnt, over;
 };
 
-template <typename TOK, bool STAGE, bool SCORE>
+// PAD: the word holds positions past T (only the last word of a row).
+template <typename TOK, bool STAGE, bool SCORE, bool PAD>
 __device__ __forceinline__ void consume_word(const SlotTables &t, uint32_t word, int nvalid_tok,
-                                             int G, int Q, int M, int lane, double zc2,
+                                             int G, int Q, int M, int lane, float zc2f,
                                              float alpha, float *st, int arr_stride, Acc &a) {
     constexpr int K = 4 / (int)sizeof(TOK);
-    int tok[K], isbar[K], tg[K], qn[K];
+    int isbar[K], tg[K], qn[K];
     GRec g[K];
     QRec r[K];
+    const GRec *sgl = t.sg + t.rl;                       // this lane's replica
     // (i) tokens, separators, group and queue records (independent loads)
     int q = a.q;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        tok[k] = K == 4 ? (int)((word >> (8 * k)) & 0xFFu) : (int)((word >> (16 * k)) & 0xFFFFu);
-        if (k >= nvalid_tok) tok[k] = G;          // padding past T: treat as a no-op separator
-        isbar[k] = tok[k] >= G;
-        tg[k] = isbar[k] ? 0 : tok[k];
+        int tok = K == 4 ? (int)((word >> (8 * k)) & 0xFFu) : (int)((word >> (16 * k)) & 0xFFFFu);
+        if (PAD && k >= nvalid_tok) tok = G;             // past T: no-op separator
+        isbar[k] = tok >= G;
+        tg[k] = isbar[k] ? 0 : tok;
         qn[k] = q + isbar[k] < Q ? q + isbar[k] : Q - 1;
-        if (k >= nvalid_tok) qn[k] = q;
+        if (PAD && k >= nvalid_tok) qn[k] = q;
         q = qn[k];
-        g[k] = t.sg[(tg[k] << t.rs) + t.rl];
+        g[k] = sgl[tg[k] << t.rs];
         r[k] = t.sq[qn[k]];
     }
-    // (ii) per-slot device and previous-model row
+    // (ii) per-slot device and previous-model row of the transition table
     int dk[K], pk[K];
     int d = a.d, prev = a.prev;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         dk[k] = d;
         pk[k] = prev;
-        const int bar_prev = r[k].backlog ? r[k].r : M + r[k].r;
-        const int pad = k >= nvalid_tok;
-        d = (isbar[k] && !pad) ? r[k].d : d;
-        prev = pad ? prev : (isbar[k] ? bar_prev : g[k].model);
+        const bool reset = PAD ? (isbar[k] && k < nvalid_tok) : isbar[k];
+        const bool keep = PAD && k >= nvalid_tok;
+        d = reset ? r[k].d : d;
+        prev = keep ? prev : (reset ? (r[k].backlog ? r[k].r : M + r[k].r) : g[k].model);
     }
     // (iii) per-device group work and transition costs
     double2 ab[K], tr[K];
@@ -142,7 +144,9 @@ __device__ __forceinline__ void consume_word(const SlotTables &t, uint32_t word,
         tr[k] = t.str[(dk[k] * 2 * M + pk[k]) * M + g[k].model];
     }
     // (iv) the Eq. 10 chain (operation order identical to the sequential definition)
-    double wt[K], V[K];
+    double wt[K];
+    float Vf[K];
+    double V[K];
     double A = a.A, B = a.B;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -150,33 +154,38 @@ __device__ __forceinline__ void consume_word(const SlotTables &t, uint32_t word,
         wt[k] = A1;
         V[k] = B;
         const double A2 = __dadd_rn(A1, ab[k].x), B2 = __dadd_rn(B, ab[k].y);
-        const bool reset = isbar[k] && k < nvalid_tok;
-        A = reset ? r[k].bmean : (k < nvalid_tok ? A2 : A);
-        B = reset ? r[k].bvar : (k < nvalid_tok ? B2 : B);
+        if (PAD && k >= nvalid_tok) continue;
+        A = isbar[k] ? r[k].bmean : A2;
+        B = isbar[k] ? r[k].bvar : B2;
     }
     a.A = A; a.B = B; a.d = d; a.prev = prev; a.q = q;
     // (v) violation probabilities, scores, staging
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const double slack = __dsub_rn(g[k].slo, wt[k]);
-        const bool clamped = fma(slack, slack, -zc2 * V[k]) >= 0.0;
+        const float sf = (float)slack;
+        Vf[k] = (float)V[k];
+        // |z| >= z_clamp  <=>  slack^2 >= z_clamp^2 V   (R9; exact for V = 0)
+        const bool clamped = sf * sf >= zc2f * Vf[k];
         const bool neg = slack < 0.0;
-        const float Vf = (float)V[k];
-        const float rr = rsqrt_approx(Vf);
-        const float pz = phibar((float)slack * rr);
-        const float v = clamped ? (neg ? 1.0f : 0.0f) : pz;
+        const float rr = rsqrt_approx(Vf[k]);
+        float v = neg ? 1.0f : 0.0f;
+        if (__any_sync(__activemask(), !clamped)) {      // warp-uniform: ~40 % of slots
+            const float pz = phibar(sf * rr);
+            v = clamped ? v : pz;
+        }
         const bool grp = !isbar[k];
         if constexpr (SCORE) {
-            a.S2 = grp ? __dsub_rn(a.S2, slack) : a.S2;
+            a.S2 = __dsub_rn(a.S2, grp ? slack : 0.0);
             a.cnt += (grp && clamped && neg) ? g[k].n : 0;
-            a.frac = (grp && !clamped) ? fmaf((float)g[k].n, v, a.frac) : a.frac;
+            if (grp && !clamped) a.frac = fmaf((float)g[k].n, v, a.frac);
             a.over += (grp && v > alpha) ? 1 : 0;
         }
         if constexpr (STAGE) {
-            const int o = (grp ? tg[k] : G) * 32 + lane;
-            st[o] = (float)wt[k];
-            st[arr_stride + o] = Vf >= 1.17549435e-38f ? Vf * rr : 0.0f;
-            st[2 * arr_stride + o] = v;
+            float *o = st + (grp ? tg[k] : G) * 32 + lane;
+            o[0] = (float)wt[k];
+            o[arr_stride] = Vf[k] >= 1.17549435e-38f ? Vf[k] * rr : 0.0f;
+            o[2 * arr_stride] = v;
         }
     }
 }
@@ -313,10 +322,17 @@ __global__ void __launch_bounds__(STAGE ? 512 : 1024, 1) ws_kernel(const __grid_
                 constexpr int EPW = 4 / (int)sizeof(TOK);
                 const uint32_t *w32 = reinterpret_cast<const uint32_t *>(slot);
                 const int tw = w.tw;
-                for (int wi = 0; wi < tw; ++wi) {
+                const float zc2f = (float)zc2;
+                const int full_words = T / EPW;
+                for (int wi = 0; wi < full_words; ++wi) {
                     const uint32_t word = w32[wi * 32 + lane];
-                    consume_word<TOK, STAGE, SCORE>(tab, word, T - wi * EPW, G, Q, M, lane, zc2, alpha,
-                                                    st, (G + 1) * 32, a);
+                    consume_word<TOK, STAGE, SCORE, false>(tab, word, EPW, G, Q, M, lane, zc2f,
+                                                           alpha, st, (G + 1) * 32, a);
+                }
+                if (full_words < tw) {
+                    const uint32_t word = w32[full_words * 32 + lane];
+                    consume_word<TOK, STAGE, SCORE, true>(tab, word, T - full_words * EPW, G, Q, M,
+                                                          lane, zc2f, alpha, st, (G + 1) * 32, a);
                 }
                 if constexpr (SCORE) {
                     const float s1 = (float)(__dadd_rn((double)a.cnt, (double)a.frac) / den);
