@@ -51,18 +51,28 @@ __device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t *b, unsigned parity) {
+    uint32_t ok;
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
-        "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n"
-        "@P1 bra DONE;\n"
-        "bra LAB_WAIT;\n"
-        "DONE:\n"
-        "}\n" ::"r"(smem_u32(b)),
-        "r"(parity), "r"(0x989680u)
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+// Wait for a phase; back off with nanosleep so waiting warps (usually the
+// producers) do not steal issue slots from the warps doing the work.
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+    if (mbar_try(b, parity)) return;
+    unsigned ns = 32;
+    while (!mbar_try(b, parity)) {
+        __nanosleep(ns);
+        ns = ns < 512 ? ns * 2 : 512;
+    }
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, const void *src, int x, int y) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
