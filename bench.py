@@ -303,7 +303,7 @@ def run_ours(args, rank, world, local_rank):
                 traffic = json.load(f).get(CFG, {}).get("scan_kernel_dram_bytes_per_launch")
         except Exception:
             pass
-        roofline = {"kernel": "scan_kernel<RANDOM,u8,STAGED,SCORE> (qlm_score_estimate)", "bound": "hbm",
+        roofline = {"kernel": "ws_kernel<RANDOM,u8,STAGE,SCORE> (qlm_score_estimate, fused a1-a7)", "bound": "hbm",
                     "achieved": bulk_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": bulk_gbs / hbm_peak, "traffic": traffic,
                     "algorithmic_bytes_per_launch": bulk_bytes,
