@@ -55,10 +55,8 @@ struct qlm_ctx {
     int32_t *d_dec_out = nullptr;          // [2][G] sync decode
     unsigned long long *d_bad = nullptr;
     int max_blocks = 0;
-    uint32_t *d_X = nullptr;
+    double *d_X = nullptr;             // MC: (X / Theta)[D][G][trials]
     size_t X_cap = 0;
-    uint16_t *d_rows = nullptr;
-    size_t rows_cap = 0;
     std::vector<qlm_group> groups;
     std::vector<qlm_queue> queues;
     std::vector<double> prof;              // theta|prefill|eps|dec|maxo [D*M] each, swap [D*M*M]
@@ -167,18 +165,6 @@ int rebuild(qlm_ctx *ctx, cudaStream_t st) {
                                  ctx->d_prefill, ctx->d_eps, ctx->d_dec, ctx->d_maxo, ctx->d_swap,
                                  ctx->tb, st);
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "build_tables");
-}
-
-int ensure_rows(qlm_ctx *ctx, int64_t count) {
-    const size_t need = (size_t)count * ctx->dm.T * sizeof(uint16_t);
-    if (need <= ctx->rows_cap) return QLM_OK;
-    if (ctx->d_rows) cudaFree(ctx->d_rows);
-    ctx->d_rows = nullptr;
-    ctx->rows_cap = 0;
-    if (cudaMalloc(&ctx->d_rows, need) != cudaSuccess)
-        return fail(QLM_ENOMEM, "rows scratch of %zu bytes", need);
-    ctx->rows_cap = need;
-    return QLM_OK;
 }
 
 }  // namespace
@@ -367,7 +353,7 @@ void qlm_destroy(qlm_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     void *ptrs[] = {ctx->d_raw, ctx->d_tab, ctx->d_block_recs, ctx->d_counter, ctx->d_rec,
-                    ctx->d_dec_out, ctx->d_bad, ctx->d_X, ctx->d_rows};
+                    ctx->d_dec_out, ctx->d_bad, ctx->d_X};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete ctx;
@@ -537,7 +523,7 @@ int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
     if ((e = cudaMemsetAsync(counts, 0, (size_t)cand->count * ctx->dm.G * 4, st)) != cudaSuccess)
         return cuda_fail(e, "counts memset");
     if (trial_count == 0) return QLM_OK;
-    const size_t needX = (size_t)trial_count * ctx->dm.G * 4;
+    const size_t needX = (size_t)trial_count * ctx->dm.G * ctx->dm.D * sizeof(double);
     if (needX > ctx->X_cap) {
         if (ctx->d_X) cudaFree(ctx->d_X);
         ctx->d_X = nullptr;
@@ -545,13 +531,10 @@ int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
         if (cudaMalloc(&ctx->d_X, needX) != cudaSuccess) return fail(QLM_ENOMEM, "MC scratch %zu B", needX);
         ctx->X_cap = needX;
     }
-    if ((rc = ensure_rows(ctx, cand->count))) return rc;
-    ScanParams p = base_params(ctx, cand);
-    if ((e = launch_rows(p, ctx->d_rows, nullptr, nullptr, st)) != cudaSuccess) return cuda_fail(e, "MC rows");
     if ((e = launch_mc_sample(ctx->dm, ctx->tb, mc_seed, trial_first, trial_count, ctx->d_X, st)) != cudaSuccess)
         return cuda_fail(e, "MC sample kernel");
-    if ((e = launch_mc_count(ctx->dm, ctx->tb, ctx->d_rows, cand->first_from, cand->count, ctx->d_X,
-                             trial_count, counts, st)) != cudaSuccess)
+    if ((e = launch_mc_count(ctx->dm, ctx->tb, to_cand(cand), ctx->d_X, trial_count, counts, st)) !=
+        cudaSuccess)
         return cuda_fail(e, "MC count kernel");
     return QLM_OK;
 }

@@ -370,91 +370,192 @@ __global__ void check_rows_kernel(const Cand cd, int T, unsigned long long *n_ba
     if (threadIdx.x == 0 && bad) atomicAdd(n_bad, 1ull);
 }
 
+// One candidate row generated by a whole warp (small counts: winner decode,
+// MC).  RANDOM: the lanes compute the row's Philox blocks in parallel, then
+// lane 0 runs the Fisher-Yates swaps from shared memory (same permutation as
+// fy_materialise).  Returns with srow[0..T) valid for all lanes.
+__device__ __forceinline__ void warp_gen_row(const Cand &cd, int T, uint64_t c, int64_t loc,
+                                             uint16_t *srow, uint4 *swords) {
+    const int lane = threadIdx.x & 31;
+    if (cd.kind == QLM_CAND_RANDOM) {
+        const int nb = (T - 1 + 3) / 4;
+        const uint2 key = make_uint2((uint32_t)cd.seed, (uint32_t)(cd.seed >> 32));
+        for (int b = lane; b < nb; b += 32)
+            swords[b] = philox10(make_uint4((uint32_t)b, (uint32_t)c, (uint32_t)(c >> 32), kRowTag), key);
+        for (int s = lane; s < T; s += 32) srow[s] = (uint16_t)s;
+        __syncwarp();
+        if (lane == 0) {
+            for (int i = 0; i + 1 < T; ++i) {
+                const uint32_t u = pick4(swords[i >> 2], i & 3);
+                const int j = i + (int)__umulhi(u, (uint32_t)(T - i));
+                const uint16_t ti = srow[i], tj = srow[j];
+                srow[j] = ti;
+                srow[i] = tj;
+            }
+        }
+    } else if (cd.kind == QLM_CAND_ENUM) {
+        if (lane == 0) {
+            int s = 0;
+            tokens_enum(c, T, [&](int tok) { srow[s++] = (uint16_t)tok; });
+        }
+    } else {
+        const uint8_t *row = cd.rows + loc * cd.stride;
+        for (int s = lane; s < T; s += 32)
+            srow[s] = cd.tb == 1 ? row[s] : reinterpret_cast<const uint16_t *>(row)[s];
+    }
+    __syncwarp();
+}
+
+// Rows / decode with one warp per candidate (small counts).
+__global__ void __launch_bounds__(32) row_warp_kernel(const ScanParams p, uint16_t *rows_out,
+                                                      int32_t *queue_of, int32_t *pos_of) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    int64_t first = p.cd.first;
+    if (p.cd.first_from) {
+        first = p.cd.first_from->index;
+        if (first < 0) return;
+    }
+    const int64_t loc = blockIdx.x;
+    const int T = p.dm.T, G = p.dm.G, Q = p.dm.Q;
+    uint4 *swords = reinterpret_cast<uint4 *>(smem);
+    uint16_t *srow = reinterpret_cast<uint16_t *>(smem + (size_t)((T + 2) / 4 + 1) * 16);
+    warp_gen_row(p.cd, T, (uint64_t)(first + loc), loc, srow, swords);
+    const int lane = threadIdx.x;
+    if (rows_out)
+        for (int s = lane; s < T; s += 32) rows_out[loc * T + s] = srow[s];
+    if ((queue_of || pos_of) && lane == 0) {
+        int q = 0, pos = 0;
+        for (int s = 0; s < T; ++s) {
+            const int tok = srow[s];
+            if (tok >= G) { q = q + 1 < Q ? q + 1 : Q - 1; pos = 0; continue; }
+            if (queue_of) queue_of[loc * G + tok] = q;
+            if (pos_of) pos_of[loc * G + tok] = pos;
+            ++pos;
+        }
+    }
+}
+
 // =============================================================================
 // a10-a11: Monte-Carlo
 // =============================================================================
-// X[k][t] = sum_{r < n_k} len[dist_k][word(t, k, r) >> shift]   (R13)
+// X[k][t] = sum_{r < n_k} len[dist_k][word(t, k, r) >> shift]   (R13).
+// One warp per (group, trial): lane l draws Philox blocks b = l, l+32, ...
+// (requests 4b..4b+3) and the warp sums them (exact integers, any order).
 __global__ void __launch_bounds__(256) mc_sample_kernel(Dims dm, Tables tb, uint64_t seed,
-                                                        int64_t t0, int64_t nt, uint32_t *X,
+                                                        int64_t t0, int64_t nt, double *Y,
                                                         int tabs_in_smem) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const uint16_t *len = tb.len;
-    if (tabs_in_smem) {
-        uint4 *s4 = reinterpret_cast<uint4 *>(smem);
-        const uint4 *g4 = reinterpret_cast<const uint4 *>(tb.len);
-        const int n4 = dm.n_tables * dm.K * 2 / 16;
-        for (int i = threadIdx.x; i < n4; i += blockDim.x) s4[i] = g4[i];
-        __syncthreads();
-        len = reinterpret_cast<const uint16_t *>(smem);
-    }
+    (void)tabs_in_smem;
+    const uint16_t *__restrict__ len = tb.len;       // read through L1 (tables <= a few 100 KB)
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     const int64_t total = (int64_t)dm.G * nt;
-    const int shift = dm.shift;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(idx / nt);
-        const int64_t tl = idx - (int64_t)k * nt;
+    const int shift = dm.shift, lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < total;
+         task += nwarps) {
+        const int k = (int)(task / nt);
+        const int64_t tl = task - (int64_t)k * nt;
         const uint32_t t = (uint32_t)(t0 + tl);
         const int n = tb.grec[k].n;
         const uint16_t *tab = len + (int64_t)tb.dist[k] * dm.K;
         uint32_t sum = 0;
-        for (int r0 = 0; r0 < n; r0 += 4) {
-            const uint4 wd = philox10(make_uint4((uint32_t)(r0 >> 2), (uint32_t)k, t, kMcTag), key);
-            sum += tab[wd.x >> shift];
-            if (r0 + 1 < n) sum += tab[wd.y >> shift];
-            if (r0 + 2 < n) sum += tab[wd.z >> shift];
-            if (r0 + 3 < n) sum += tab[wd.w >> shift];
+        for (int b = lane; 4 * b < n; b += 64) {         // two independent Philox chains
+            const int b2 = b + 32;
+            const uint4 w1 = philox10(make_uint4((uint32_t)b, (uint32_t)k, t, kMcTag), key);
+            uint4 w2 = make_uint4(0u, 0u, 0u, 0u);
+            if (4 * b2 < n) w2 = philox10(make_uint4((uint32_t)b2, (uint32_t)k, t, kMcTag), key);
+            const int r1 = 4 * b, r2 = 4 * b2;
+            sum += __ldg(&tab[w1.x >> shift]);
+            if (r1 + 1 < n) sum += __ldg(&tab[w1.y >> shift]);
+            if (r1 + 2 < n) sum += __ldg(&tab[w1.z >> shift]);
+            if (r1 + 3 < n) sum += __ldg(&tab[w1.w >> shift]);
+            if (r2 < n) sum += __ldg(&tab[w2.x >> shift]);
+            if (r2 + 1 < n) sum += __ldg(&tab[w2.y >> shift]);
+            if (r2 + 2 < n) sum += __ldg(&tab[w2.z >> shift]);
+            if (r2 + 3 < n) sum += __ldg(&tab[w2.w >> shift]);
         }
-        X[(int64_t)k * nt + tl] = sum;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+        // y[d][k][t] = X / Theta[d][m_k]: Eq. 2 with the realised token count, per device row
+        const int m = tb.grec[k].model;
+        for (int d = lane; d < dm.D; d += 32)
+            Y[((int64_t)d * dm.G + k) * nt + tl] = __ddiv_rn((double)sum, tb.theta[d * dm.M + m]);
     }
 }
 
-// One block per (candidate, chunk of trials); every thread is one trial and
-// walks the shared row; counts via warp ballots into shared counters.
-__global__ void __launch_bounds__(256) mc_count_kernel(Dims dm, Tables tb, const uint16_t *rows,
-                                                       const qlm_record *first_from,
-                                                       const uint32_t *X, int64_t nt,
-                                                       uint32_t *counts) {
+// One warp per (candidate, 32 trials); every lane is one trial.  The warp
+// materialises the candidate's row and its in-order list of group slots
+// (token, queue) in shared memory.  Phase 1 computes each group's realised
+// work X/Theta (independent across slots: loads and divisions overlap);
+// phase 2 walks the Eq. 10 chain in the oracle's operation order and counts
+// violations with warp ballots.
+__global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand cd,
+                                                      const double *Y, int64_t nt,
+                                                      uint32_t *counts) {
     extern __shared__ __align__(16) uint8_t smem[];
-    if (first_from && first_from->index < 0) return;
+    int64_t first = cd.first;
+    if (cd.first_from) {
+        first = cd.first_from->index;
+        if (first < 0) return;
+    }
     const int T = dm.T, G = dm.G, M = dm.M;
-    uint16_t *srow = reinterpret_cast<uint16_t *>(smem);
-    uint32_t *scnt = reinterpret_cast<uint32_t *>(smem + ((T * 2 + 15) & ~15));
-    const int64_t c = blockIdx.y;
-    for (int s = threadIdx.x; s < T; s += blockDim.x) srow[s] = rows[c * T + s];
-    for (int g = threadIdx.x; g < G; g += blockDim.x) scnt[g] = 0u;
-    __syncthreads();
-    const int64_t tl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double *sy = reinterpret_cast<double *>(smem);                                   // [G][32]
+    uint16_t *stok = reinterpret_cast<uint16_t *>(smem + (size_t)G * 32 * 8);         // [G]
+    uint16_t *sq = stok + G;                                                         // [G]
+    uint4 *swords = reinterpret_cast<uint4 *>(smem + (size_t)G * 32 * 8 + (((size_t)4 * G + 15) & ~15));
+    uint16_t *srow = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(swords) +
+                                                  (size_t)((T + 2) / 4 + 1) * 16);
+    const int64_t loc = blockIdx.y;
+    const int lane = threadIdx.x;
+    warp_gen_row(cd, T, (uint64_t)(first + loc), loc, srow, swords);
+    if (lane == 0) {
+        int q = 0, i = 0;
+        for (int s = 0; s < T; ++s) {
+            const int tok = srow[s];
+            if (tok >= G) { q = q + 1 < dm.Q ? q + 1 : dm.Q - 1; continue; }
+            stok[i] = (uint16_t)tok;
+            sq[i] = (uint16_t)q;
+            ++i;
+        }
+    }
+    __syncwarp();
+    const int64_t tl = (int64_t)blockIdx.x * 32 + lane;
     const bool act = tl < nt;
-    const int lane = threadIdx.x & 31;
-    int q = 0;
-    QRec qr = tb.qrec[0];
-    double A = qr.bmean;
-    int d = qr.d, prev = qr.r, first = 1, backlog = qr.backlog;
-    for (int s = 0; s < T; ++s) {
-        const int tok = srow[s];
-        if (tok >= G) {
-            q = q + 1 < dm.Q ? q + 1 : dm.Q - 1;
-            qr = tb.qrec[q];
-            A = qr.bmean; d = qr.d; prev = qr.r; first = 1; backlog = qr.backlog;
-            continue;
+    // phase 1: gather y_i = (X / Theta)[d_i][g_i][t] for the row's group slots into
+    // shared memory, 8 independent loads at a time.
+    for (int i0 = 0; i0 < G; i0 += 8) {
+        double yv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = i0 + k < G ? i0 + k : G - 1;
+            const int64_t row = (int64_t)tb.qrec[sq[i]].d * G + stok[i];
+            yv[k] = act ? __ldg(&Y[row * nt + tl]) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (i0 + k < G) sy[(i0 + k) * 32 + lane] = yv[k];
+    }
+    __syncwarp();
+    // phase 2: the sequential chain and the counts
+    int q = -1, d = 0, prev = 0, firstslot = 1, backlog = 0;
+    double A = 0.0;
+    for (int i = 0; i < G; ++i) {
+        const int tok = stok[i], qi = sq[i];
+        if (qi != q) {                                   // first group of queue qi
+            const QRec qr = tb.qrec[qi];
+            q = qi; A = qr.bmean; d = qr.d; prev = qr.r; firstslot = 1; backlog = qr.backlog;
         }
         const GRec g = tb.grec[tok];
         const int m = g.model;
         if (m != prev) {
-            const double t = (first && !backlog) ? 0.0 : tb.tail[d * M + prev];
+            const double t = (firstslot && !backlog) ? 0.0 : tb.tail[d * M + prev];
             A = __dadd_rn(A, t);
             A = __dadd_rn(A, tb.swap[(d * M + prev) * M + m]);
         }
-        const unsigned b = __ballot_sync(0xFFFFFFFFu, act && A > g.slo);
-        if (lane == 0 && b) atomicAdd(&scnt[tok], (unsigned)__popc(b));
-        const double x = act ? (double)X[(int64_t)tok * nt + tl] : 0.0;
-        A = __dadd_rn(A, __ddiv_rn(x, tb.theta[d * M + m]));   // Eq. 2 with realised O
-        prev = m; first = 0;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, act && A > g.slo);
+        if (lane == 0 && bal) atomicAdd(&counts[loc * G + tok], (unsigned)__popc(bal));
+        A = __dadd_rn(A, sy[i * 32 + lane]);
+        prev = m; firstslot = 0;
     }
-    __syncthreads();
-    for (int g = threadIdx.x; g < G; g += blockDim.x)
-        if (scnt[g]) atomicAdd(&counts[c * G + g], scnt[g]);
 }
 
 // =============================================================================
@@ -645,6 +746,14 @@ static cudaError_t launch_rows_t(ScanParams p, uint16_t *rows, int32_t *qo, int3
 
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,
                         cudaStream_t st) {
+    if (p.cd.count <= 1024) {
+        const size_t smem = (size_t)((p.dm.T + 2) / 4 + 1) * 16 + align16((size_t)p.dm.T * 2 + 4);
+        cudaError_t e = prep(row_warp_kernel, smem);
+        if (e != cudaSuccess) return e;
+        row_warp_kernel<<<(unsigned)p.cd.count, 32, smem, st>>>(p, rows, qo, po);
+        ++g_launches;
+        return cudaGetLastError();
+    }
     switch (p.cd.kind) {
     case QLM_CAND_RANDOM:
         return p.dm.T <= 256 ? launch_rows_t<QLM_CAND_RANDOM, uint8_t>(p, rows, qo, po, st)
@@ -682,15 +791,15 @@ cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
 }
 
 cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, int64_t t0,
-                             int64_t nt, uint32_t *X, cudaStream_t st) {
-    const size_t tab_bytes = (size_t)dm.n_tables * dm.K * 2;
-    const int in_smem = tab_bytes <= 160 * 1024 && (tab_bytes % 16) == 0;
-    const size_t smem = in_smem ? tab_bytes : 0;
+                             int64_t nt, double *X, cudaStream_t st) {
+    const int in_smem = 0;
+    const size_t smem = 0;
     cudaError_t e = prep(mc_sample_kernel, smem);
     if (e != cudaSuccess) return e;
     const int nb = occupancy(mc_sample_kernel, 256, smem);
-    int64_t grid = ((int64_t)dm.G * nt + 255) / 256;
-    const int64_t maxg = (int64_t)sm_count() * (nb > 0 ? nb : 1) * 4;
+    const int64_t tasks = (int64_t)dm.G * nt;                 // one warp each
+    int64_t grid = (tasks + 7) / 8;
+    const int64_t maxg = (int64_t)sm_count() * (nb > 0 ? nb : 1);
     if (grid > maxg) grid = maxg;
     if (grid < 1) grid = 1;
     mc_sample_kernel<<<(unsigned)grid, 256, smem, st>>>(dm, tb, seed, t0, nt, X, in_smem);
@@ -698,14 +807,14 @@ cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, in
     return cudaGetLastError();
 }
 
-cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const uint16_t *rows,
-                            const qlm_record *first_from, int64_t count, const uint32_t *X,
+cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const Cand &cd, const double *X,
                             int64_t nt, uint32_t *counts, cudaStream_t st) {
-    const size_t smem = align16((size_t)dm.T * 2) + (size_t)dm.G * 4;
+    const size_t smem = (size_t)dm.G * 32 * 8 + align16((size_t)4 * dm.G) +
+                        (size_t)((dm.T + 2) / 4 + 1) * 16 + align16((size_t)dm.T * 2 + 4);
     cudaError_t e = prep(mc_count_kernel, smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)((nt + 255) / 256), (unsigned)count);
-    mc_count_kernel<<<grid, 256, smem, st>>>(dm, tb, rows, first_from, X, nt, counts);
+    dim3 grid((unsigned)((nt + 31) / 32), (unsigned)cd.count);
+    mc_count_kernel<<<grid, 32, smem, st>>>(dm, tb, cd, X, nt, counts);
     ++g_launches;
     return cudaGetLastError();
 }

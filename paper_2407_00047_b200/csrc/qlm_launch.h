@@ -43,9 +43,8 @@ cudaError_t launch_reduce_records(const qlm_record *recs, int n, qlm_record *out
                                   cudaStream_t st);
 cudaError_t launch_check_rows(const Cand &cd, int T, unsigned long long *n_bad, cudaStream_t st);
 cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, int64_t t0,
-                             int64_t nt, uint32_t *X, cudaStream_t st);
-cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const uint16_t *rows,
-                            const qlm_record *first_from, int64_t count, const uint32_t *X,
+                             int64_t nt, double *Y, cudaStream_t st);
+cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const Cand &cd, const double *Y,
                             int64_t nt, uint32_t *counts, cudaStream_t st);
 
 }  // namespace qlm

@@ -8,7 +8,7 @@ st = h.index('Warp Stall Sampling (All Samples)')
 ops = collections.Counter(); stalls = collections.Counter(); tot = 0
 lines = []
 for r in rows[hi+1:]:
-    if len(r) <= ie: continue
+    if len(r) <= ie or r[0] == 'Address': continue
     try: n = int(r[ie])
     except: continue
     s = r[src].strip()
