@@ -290,8 +290,8 @@ __device__ __forceinline__ float phibar(float z) {
 __device__ __forceinline__ float violation(double slack, double V, double zc2, bool &clamped) {
     const float sf = (float)slack, Vf = (float)V;
     clamped = sf * sf >= (float)zc2 * Vf;
-    float v = slack < 0.0 ? 1.0f : 0.0f;
-    if (!clamped) v = phibar(sf * rsqrt_approx(Vf));
+    float v = sf < 0.0f ? 1.0f : 0.0f;
+    if (!clamped) v = phibar(sf * rsqrt_approx(fmaxf(Vf, 1e-30f)));
     return v;
 }
 

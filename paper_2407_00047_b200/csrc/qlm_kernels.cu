@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
             ScanState s;
             start_queue(tab, s, 0);
             double S2 = 0.0;
-            float frac = 0.0f;
-            int cnt = 0, over = 0;
+            float acc = 0.0f;                                     // sum n_i v_i (row order)
+            int over = 0;
             for_tokens<KIND, TOK>(cd, T, scratch, blk, loc, first + loc, [&](int tok) {
                 if (tok >= G) {                          // queue separator
                     start_queue(tab, s, s.q + 1 < Q ? s.q + 1 : Q - 1);
@@ -193,26 +193,25 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                 const float v = violation(slack, V, zc2, clamped);
                 if constexpr (SCORE) {
                     S2 = __dsub_rn(S2, slack);                    // sum_i p_i
-                    if (clamped) cnt += v != 0.0f ? g.n : 0;
-                    else frac = fmaf((float)g.n, v, frac);
+                    acc = fmaf((float)g.n, v, acc);
                     over += v > alpha;
                 }
                 if constexpr (OUT == OUT_STAGED) {
                     const int o = tok * blk + tid;
                     const float Vf = (float)V;
                     st0[o] = (float)wt;
-                    st1[o] = Vf >= 1.17549435e-38f ? Vf * rsqrt_approx(Vf) : 0.0f;
+                    st1[o] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
                     st2[o] = v;
                 } else if constexpr (OUT == OUT_DIRECT) {
                     const int64_t o = (int64_t)tok * count + loc;
                     const float Vf = (float)V;
                     if (gout[0]) gout[0][o] = (float)wt;
-                    if (gout[1]) gout[1][o] = Vf >= 1.17549435e-38f ? Vf * rsqrt_approx(Vf) : 0.0f;
+                    if (gout[1]) gout[1][o] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
                     if (gout[2]) gout[2][o] = v;
                 }
             });
             if constexpr (SCORE) {
-                const float s1 = (float)(__dadd_rn((double)cnt, (double)frac) / den);   // R11
+                const float s1 = (float)((double)acc / den);   // R11
                 const float s2 = (float)S2;
                 if (p.s1) p.s1[loc] = s1;
                 if (p.s2) p.s2[loc] = s2;

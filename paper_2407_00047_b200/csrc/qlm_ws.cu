@@ -104,59 +104,75 @@ __device__ __forceinline__ void produce_row(const Cand &cd, int T, uint8_t *slot
 // word are straight-line code: all shared-memory loads of the word are issued
 // before its fp64 chain, and its staging stores come last.  Staging offsets
 // of separator slots point at a trash row (row G of each staged array).
-struct Acc {
-    double A, B, S2;
-    float frac;
-    int d, prev, q, cnt, over;
+// Shared-memory tables of the warp-specialised consumer.  Index G of the
+// group tables is a zero "separator" record and row G of the staging tile a
+// trash row, so a separator slot runs the same straight-line code as a group
+// slot; the queue table is padded to T entries so the queue counter needs no
+// clamp.
+struct WsG {                 // 16 B, replicated 1 << RS times
+    double slo;
+    float nf;                // n_i as float (S1 numerator, exact below 2^24)
+    int model;
+};
+struct WsQ {                 // 32 B
+    double bmean, bvar;      // queue reset values (R12)
+    int prow0;               // transition-table row at the queue's start (R4)
+    int dG;                  // d * (G + 1): device base into the ab table
+    int dbase;               // d * 2M * M: device base into the transition table
+    int pad;
 };
 
-// PAD: the word holds positions past T (only the last word of a row).
-template <typename TOK, bool STAGE, bool SCORE, bool PAD>
-__device__ __forceinline__ void consume_word(const SlotTables &t, uint32_t word, int nvalid_tok,
-                                             int G, int Q, int M, int lane, float zc2f,
-                                             float alpha, float *st, int arr_stride, Acc &a) {
+struct Acc {
+    double A, B, S2;
+    float acc;               // sum n_i v_i (row order)
+    int prow, dG, dbase, q, over;
+};
+
+template <typename TOK, int RS, bool SCORE, bool PAD>
+__device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const double2 *__restrict__ sabl,
+                                             const double2 *__restrict__ str, const WsQ *__restrict__ sq,
+                                             uint32_t word, int nvalid_tok, int G, int M, int lane,
+                                             float zc2f, float alpha, float *st, int arr_stride,
+                                             Acc &a) {
     constexpr int K = 4 / (int)sizeof(TOK);
-    int isbar[K], tg[K], qn[K];
-    GRec g[K];
-    QRec r[K];
-    const GRec *sgl = t.sg + t.rl;                       // this lane's replica
+    int isbar[K], tg[K];
+    WsG g[K];
+    WsQ r[K];
     // (i) tokens, separators, group and queue records (independent loads)
     int q = a.q;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        int tok = K == 4 ? (int)((word >> (8 * k)) & 0xFFu) : (int)((word >> (16 * k)) & 0xFFFFu);
-        if (PAD && k >= nvalid_tok) tok = G;             // past T: no-op separator
-        isbar[k] = tok >= G;
-        tg[k] = isbar[k] ? 0 : tok;
-        qn[k] = q + isbar[k] < Q ? q + isbar[k] : Q - 1;
-        if (PAD && k >= nvalid_tok) qn[k] = q;
-        q = qn[k];
-        g[k] = sgl[tg[k] << t.rs];
-        r[k] = t.sq[qn[k]];
+        const int tok = K == 4 ? (int)((word >> (8 * k)) & 0xFFu) : (int)((word >> (16 * k)) & 0xFFFFu);
+        const bool pad = PAD && k >= nvalid_tok;
+        isbar[k] = tok >= G && !pad;
+        tg[k] = pad ? G : min(tok, G);
+        q += isbar[k];
+        g[k] = sgl[tg[k] << RS];
+        r[k] = sq[q];
     }
-    // (ii) per-slot device and previous-model row of the transition table
-    int dk[K], pk[K];
-    int d = a.d, prev = a.prev;
+    // (ii) per-slot transition row and device base
+    int pk[K], dk[K];
+    int prow = a.prow, dG = a.dG, dbase = a.dbase;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        dk[k] = d;
-        pk[k] = prev;
-        const bool reset = PAD ? (isbar[k] && k < nvalid_tok) : isbar[k];
-        const bool keep = PAD && k >= nvalid_tok;
-        d = reset ? r[k].d : d;
-        prev = keep ? prev : (reset ? (r[k].backlog ? r[k].r : M + r[k].r) : g[k].model);
+        pk[k] = prow;
+        dk[k] = dG;
+        const bool pad = PAD && k >= nvalid_tok;
+        if (!pad) {
+            prow = isbar[k] ? r[k].prow0 : dbase + g[k].model * M;
+            dG = isbar[k] ? r[k].dG : dG;
+            dbase = isbar[k] ? r[k].dbase : dbase;
+        }
     }
     // (iii) per-device group work and transition costs
     double2 ab[K], tr[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        ab[k] = t.sab[((dk[k] * G + tg[k]) << t.rs) + t.rl];
-        tr[k] = t.str[(dk[k] * 2 * M + pk[k]) * M + g[k].model];
+        ab[k] = sabl[(dk[k] + tg[k]) << RS];
+        tr[k] = str[pk[k] + g[k].model];
     }
     // (iv) the Eq. 10 chain (operation order identical to the sequential definition)
-    double wt[K];
-    float Vf[K];
-    double V[K];
+    double wt[K], V[K];
     double A = a.A, B = a.B;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -168,33 +184,31 @@ __device__ __forceinline__ void consume_word(const SlotTables &t, uint32_t word,
         A = isbar[k] ? r[k].bmean : A2;
         B = isbar[k] ? r[k].bvar : B2;
     }
-    a.A = A; a.B = B; a.d = d; a.prev = prev; a.q = q;
+    a.A = A; a.B = B; a.prow = prow; a.dG = dG; a.dbase = dbase; a.q = q;
     // (v) violation probabilities, scores, staging
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const double slack = __dsub_rn(g[k].slo, wt[k]);
         const float sf = (float)slack;
-        Vf[k] = (float)V[k];
+        const float Vf = (float)V[k];
+        const float rr = rsqrt_approx(fmaxf(Vf, 1e-30f));
         // |z| >= z_clamp  <=>  slack^2 >= z_clamp^2 V   (R9; exact for V = 0)
-        const bool clamped = sf * sf >= zc2f * Vf[k];
-        const bool neg = slack < 0.0;
-        const float rr = rsqrt_approx(Vf[k]);
-        float v = neg ? 1.0f : 0.0f;
+        const bool clamped = sf * sf >= zc2f * Vf;
+        float v = sf < 0.0f ? 1.0f : 0.0f;
         if (__any_sync(__activemask(), !clamped)) {      // warp-uniform: ~40 % of slots
             const float pz = phibar(sf * rr);
             v = clamped ? v : pz;
         }
-        const bool grp = !isbar[k];
         if constexpr (SCORE) {
+            const bool grp = !isbar[k] && tg[k] < G;
             a.S2 = __dsub_rn(a.S2, grp ? slack : 0.0);
-            a.cnt += (grp && clamped && neg) ? g[k].n : 0;
-            if (grp && !clamped) a.frac = fmaf((float)g[k].n, v, a.frac);
+            a.acc = fmaf(g[k].nf, v, a.acc);                // separator / pad records have nf = 0
             a.over += (grp && v > alpha) ? 1 : 0;
         }
-        if constexpr (STAGE) {
-            float *o = st + (grp ? tg[k] : G) * 32 + lane;
+        if (st) {
+            float *o = st + tg[k] * 32 + lane;               // separators -> trash row G
             o[0] = (float)wt[k];
-            o[arr_stride] = Vf[k] >= 1.17549435e-38f ? Vf[k] * rr : 0.0f;
+            o[arr_stride] = Vf * rr;
             o[2 * arr_stride] = v;
         }
     }
@@ -246,25 +260,47 @@ __device__ __forceinline__ void block_grid_argmin(const ScanParams &p, uint64_t 
     }
 }
 
-template <int KIND, typename TOK, bool STAGE, bool SCORE>
-__global__ void __launch_bounds__(STAGE ? 512 : 1024, 1) ws_kernel(const __grid_constant__ WsParams w) {
+template <int KIND, typename TOK, bool SCORE, int RS>
+__global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsParams w) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const ScanParams &p = w.p;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = w.pairs;
-    const int G = p.dm.G, Q = p.dm.Q, T = p.dm.T;
+    const int G = p.dm.G, Q = p.dm.Q, T = p.dm.T, M = p.dm.M, D = p.dm.D;
 
-    // ---- tables -> smem (replicated group records, transition rows, queues)
-    const int rs = p.rep_shift;
-    GRec *sg = reinterpret_cast<GRec *>(smem + p.off_grec);
-    for (int i = tid; i < (G << rs); i += blockDim.x) sg[i] = p.tb.grec[i >> rs];
+    // ---- tables -> smem: group records (+ zero separator record at index G),
+    // replicated 1 << RS times; per-device group work (+ zero record); queue
+    // records padded to T; transition rows with virtual resident rows (R4)
+    WsG *sg = reinterpret_cast<WsG *>(smem + p.off_grec);
+    for (int i = tid; i < ((G + 1) << RS); i += blockDim.x) {
+        const int gi = i >> RS;
+        WsG r;
+        if (gi < G) {
+            const GRec x = p.tb.grec[gi];
+            r.slo = x.slo; r.nf = (float)x.n; r.model = x.model;
+        } else {
+            r.slo = 0.0; r.nf = 0.0f; r.model = 0;
+        }
+        sg[i] = r;
+    }
     double2 *sab = reinterpret_cast<double2 *>(smem + p.off_ab);
-    for (int i = tid; i < ((p.dm.D * G) << rs); i += blockDim.x) sab[i] = p.tb.ab[i >> rs];
-    QRec *sq = reinterpret_cast<QRec *>(smem + p.off_q);
-    for (int i = tid; i < Q; i += blockDim.x) sq[i] = p.tb.qrec[i];
+    for (int i = tid; i < ((D * (G + 1)) << RS); i += blockDim.x) {
+        const int e = i >> RS, d = e / (G + 1), gi = e - d * (G + 1);
+        sab[i] = gi < G ? p.tb.ab[d * G + gi] : make_double2(0.0, 0.0);
+    }
+    WsQ *sq = reinterpret_cast<WsQ *>(smem + p.off_q);
+    for (int i = tid; i < T + 1; i += blockDim.x) {
+        const QRec x = p.tb.qrec[i < Q ? i : Q - 1];
+        WsQ r;
+        r.bmean = x.bmean; r.bvar = x.bvar;
+        r.prow0 = (x.d * 2 * M + (x.backlog ? x.r : M + x.r)) * M;
+        r.dG = x.d * (G + 1);
+        r.dbase = x.d * 2 * M * M;
+        r.pad = 0;
+        sq[i] = r;
+    }
     double2 *str = reinterpret_cast<double2 *>(smem + p.off_tr);
-    const int M = p.dm.M;
-    for (int i = tid; i < p.dm.D * 2 * M * M; i += blockDim.x) {
+    for (int i = tid; i < D * 2 * M * M; i += blockDim.x) {
         const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
         const int from = pp < M ? pp : pp - M;
         const double sw = p.tb.swap[(d * M + from) * M + m];
@@ -300,52 +336,41 @@ __global__ void __launch_bounds__(STAGE ? 512 : 1024, 1) ws_kernel(const __grid_
             mbar_arrive(&full[s]);
         }
     } else {
-        SlotTables tab;
-        tab.sg = sg; tab.sab = sab; tab.str = str; tab.sq = sq;
-        tab.G = G; tab.Q = Q; tab.M = M; tab.rs = rs; tab.rl = lane & ((1 << rs) - 1);
-        const double zc2 = p.zc2;
+        const WsG *sgl = sg + (lane & ((1 << RS) - 1));
+        const double2 *sabl = sab + (lane & ((1 << RS) - 1));
+        const float zc2f = (float)p.zc2;
         const float alpha = p.alpha;
-        const double den = SCORE ? *p.tb.den : 1.0;
+        const double den = *p.tb.den;
+        const int arr = (G + 1) * 32;
         float *st = reinterpret_cast<float *>(smem + w.off_stage) + (size_t)pair * w.stage_floats;
-        float *st0 = st, *st1 = st + (G + 1) * 32, *st2 = st + 2 * (G + 1) * 32;
+        float *st0 = st, *st1 = st + arr, *st2 = st + 2 * arr;
+        constexpr int EPW = 4 / (int)sizeof(TOK);
+        const int full_words = T / EPW;
         for (int j = 0;; ++j) {
             const int64_t b = blockIdx.x + (int64_t)(pair + j * W) * grid;
             if (b >= nbatch) break;
             const int s = 2 * pair + (j & 1);
             mbar_wait(&full[s], (j >> 1) & 1);
-            if constexpr (STAGE) {
-                if (j > 0 && w.use_tma) {
-                    if (lane == 0) bulk_wait_read0();          // previous tile read out
-                    __syncwarp();
-                }
+            if (j > 0 && w.use_tma) {
+                if (lane == 0) bulk_wait_read0();              // previous tile read out
+                __syncwarp();
             }
             const int64_t c0 = b << 5, loc = c0 + lane;
-            const uint8_t *slot = smem + w.off_rows + (size_t)s * w.tw * 128;
+            const uint32_t *w32 = reinterpret_cast<const uint32_t *>(smem + w.off_rows + (size_t)s * w.tw * 128);
             if (loc < count) {
                 Acc a;
-                {
-                    const QRec r0 = sq[0];
-                    a.A = r0.bmean; a.B = r0.bvar; a.d = r0.d;
-                    a.prev = r0.backlog ? r0.r : M + r0.r;
-                }
-                a.q = 0; a.S2 = 0.0; a.frac = 0.0f; a.cnt = 0; a.over = 0;
-                constexpr int EPW = 4 / (int)sizeof(TOK);
-                const uint32_t *w32 = reinterpret_cast<const uint32_t *>(slot);
-                const int tw = w.tw;
-                const float zc2f = (float)zc2;
-                const int full_words = T / EPW;
-                for (int wi = 0; wi < full_words; ++wi) {
-                    const uint32_t word = w32[wi * 32 + lane];
-                    consume_word<TOK, STAGE, SCORE, false>(tab, word, EPW, G, Q, M, lane, zc2f,
-                                                           alpha, st, (G + 1) * 32, a);
-                }
-                if (full_words < tw) {
-                    const uint32_t word = w32[full_words * 32 + lane];
-                    consume_word<TOK, STAGE, SCORE, true>(tab, word, T - full_words * EPW, G, Q, M,
-                                                          lane, zc2f, alpha, st, (G + 1) * 32, a);
-                }
+                const WsQ r0 = sq[0];
+                a.A = r0.bmean; a.B = r0.bvar; a.prow = r0.prow0; a.dG = r0.dG; a.dbase = r0.dbase;
+                a.q = 0; a.S2 = 0.0; a.acc = 0.0f; a.over = 0;
+                for (int wi = 0; wi < full_words; ++wi)
+                    consume_word<TOK, RS, SCORE, false>(sgl, sabl, str, sq, w32[wi * 32 + lane], EPW, G,
+                                                        M, lane, zc2f, alpha, st, arr, a);
+                if (full_words * EPW < T)
+                    consume_word<TOK, RS, SCORE, true>(sgl, sabl, str, sq, w32[full_words * 32 + lane],
+                                                       T - full_words * EPW, G, M, lane, zc2f, alpha,
+                                                       st, arr, a);
                 if constexpr (SCORE) {
-                    const float s1 = (float)(__dadd_rn((double)a.cnt, (double)a.frac) / den);
+                    const float s1 = (float)((double)a.acc / den);     // R11
                     const float s2 = (float)a.S2;
                     if (p.s1) p.s1[loc] = s1;
                     if (p.s2) p.s2[loc] = s2;
@@ -356,33 +381,29 @@ __global__ void __launch_bounds__(STAGE ? 512 : 1024, 1) ws_kernel(const __grid_
                 }
             }
             mbar_arrive(&empty[s]);                              // row slot free
-            if constexpr (STAGE) {
-                if (w.use_tma) {
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (p.wt) tma_store_2d(&w.tmap[0], st0, (int)c0, 0);
-                        if (p.sd) tma_store_2d(&w.tmap[1], st1, (int)c0, 0);
-                        if (p.vo) tma_store_2d(&w.tmap[2], st2, (int)c0, 0);
-                        bulk_commit();
-                    }
-                } else {
-                    __syncwarp();
-                    if (loc < count) {
-                        for (int g = 0; g < G; ++g) {
-                            const int64_t o = (int64_t)g * count + loc;
-                            if (p.wt) p.wt[o] = st0[g * 32 + lane];
-                            if (p.sd) p.sd[o] = st1[g * 32 + lane];
-                            if (p.vo) p.vo[o] = st2[g * 32 + lane];
-                        }
-                    }
-                    __syncwarp();
+            if (w.use_tma) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if (p.wt) tma_store_2d(&w.tmap[0], st0, (int)c0, 0);
+                    if (p.sd) tma_store_2d(&w.tmap[1], st1, (int)c0, 0);
+                    if (p.vo) tma_store_2d(&w.tmap[2], st2, (int)c0, 0);
+                    bulk_commit();
                 }
+            } else {
+                __syncwarp();
+                if (loc < count) {
+                    for (int g = 0; g < G; ++g) {
+                        const int64_t o = (int64_t)g * count + loc;
+                        if (p.wt) p.wt[o] = st0[g * 32 + lane];
+                        if (p.sd) p.sd[o] = st1[g * 32 + lane];
+                        if (p.vo) p.vo[o] = st2[g * 32 + lane];
+                    }
+                }
+                __syncwarp();
             }
         }
-        if constexpr (STAGE) {
-            if (w.use_tma && lane == 0) bulk_wait0();
-        }
+        if (w.use_tma && lane == 0) bulk_wait0();
     }
     if constexpr (SCORE) {
         if (p.out_rec) block_grid_argmin(p, bkey, bidx);   // all warps take part
@@ -430,9 +451,9 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
     const Dims &dm = p.dm;
     size_t off = 0;
     p.rep_shift = rs;
-    p.off_grec = (int)off; off = a16(off + ((size_t)dm.G << rs) * sizeof(GRec));
-    p.off_ab = (int)off;   off = a16(off + ((size_t)dm.D * dm.G << rs) * sizeof(double2));
-    p.off_q = (int)off;    off = a16(off + (size_t)dm.Q * sizeof(QRec));
+    p.off_grec = (int)off; off = a16(off + ((size_t)(dm.G + 1) << rs) * sizeof(WsG));
+    p.off_ab = (int)off;   off = a16(off + ((size_t)dm.D * (dm.G + 1) << rs) * sizeof(double2));
+    p.off_q = (int)off;    off = a16(off + (size_t)(dm.T + 1) * sizeof(WsQ));
     p.off_tr = (int)off;   off = a16(off + (size_t)dm.D * 2 * dm.M * dm.M * sizeof(double2));
     const int epw = 4 / tok_bytes;
     w.tw = (dm.T + epw - 1) / epw;
@@ -461,12 +482,27 @@ static size_t ws_max_dyn(K kern) {
     return m;
 }
 
-template <int KIND, typename TOK, bool STAGE, bool SCORE>
-static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
-    auto kern = ws_kernel<KIND, TOK, STAGE, SCORE>;
+template <int KIND, typename TOK, bool SCORE, int RS>
+static cudaError_t launch_ws_rs(WsParams &w, size_t smem, int W, cudaStream_t st) {
+    auto kern = ws_kernel<KIND, TOK, SCORE, RS>;
     static size_t lim = 0;
     if (!lim) lim = ws_max_dyn(kern);
-    if (!lim) return cudaErrorNotSupported;
+    if (!lim || smem > lim) return cudaErrorNotSupported;
+    const int64_t nbatch = (w.p.cd.count + 31) / 32;
+    int64_t grid = sm_count();
+    const int64_t need = (nbatch + W - 1) / W;
+    if (grid > need) grid = need;
+    if (grid > w.p.max_blocks) grid = w.p.max_blocks;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, 64 * W, smem, st>>>(w);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+template <int KIND, typename TOK, bool SCORE>
+static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
+    constexpr bool STAGE = true;
+    const size_t lim = 227 * 1024 - 2048;
     WsParams w;
     memset(&w, 0, sizeof w);
     w.p = p0;
@@ -474,7 +510,7 @@ static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
     const int envW = env_int_ws("QLM_WS_PAIRS", 0), envRs = env_int_ws("QLM_REP_SHIFT", -1);
     int bestW = 0, bestRs = 0;
     size_t bestSmem = 0;
-    for (int rs : {3, 2, 0}) {
+    for (int rs : {3, 0}) {
         if (envRs >= 0 && rs != envRs) continue;
         for (int W = maxW; W >= 1; --W) {
             if (envW && W != envW) continue;
@@ -499,15 +535,8 @@ static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
         if (ok && p0.vo) ok = make_map(&w.tmap[2], p0.vo, p0.cd.count, p0.dm.G);
         w.use_tma = ok ? 1 : 0;
     }
-    const int64_t nbatch = (p0.cd.count + 31) / 32;
-    int64_t grid = sm_count();
-    const int64_t need = (nbatch + bestW - 1) / bestW;
-    if (grid > need) grid = need;
-    if (grid > p0.max_blocks) grid = p0.max_blocks;
-    if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, 64 * bestW, bestSmem, st>>>(w);
-    ++g_launches;
-    return cudaGetLastError();
+    return bestRs == 3 ? launch_ws_rs<KIND, TOK, SCORE, 3>(w, bestSmem, bestW, st)
+                       : launch_ws_rs<KIND, TOK, SCORE, 0>(w, bestSmem, bestW, st);
 }
 
 template <int KIND, typename TOK>
@@ -515,11 +544,8 @@ static cudaError_t launch_ws_k(ScanParams &p, cudaStream_t st) {
     const bool score = p.s1 || p.s2 || p.n_over || p.out_rec;
     const bool stage = p.wt || p.sd || p.vo;
     if (!stage) return cudaErrorNotSupported;   // score-only: the one-warp-per-32-candidates kernel is faster
-    if (stage) {
-        if ((size_t)3 * (p.dm.G + 1) * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
-        return score ? launch_ws_t<KIND, TOK, true, true>(p, st) : launch_ws_t<KIND, TOK, true, false>(p, st);
-    }
-    return launch_ws_t<KIND, TOK, false, true>(p, st);
+    if ((size_t)3 * (p.dm.G + 1) * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
+    return score ? launch_ws_t<KIND, TOK, true>(p, st) : launch_ws_t<KIND, TOK, false>(p, st);
 }
 
 // Fast path for large candidate sets; cudaErrorNotSupported -> caller falls back.
