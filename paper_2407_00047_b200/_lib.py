@@ -10,7 +10,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libqlm.so")
+LIB_PATH = os.environ.get("QLM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                          "libqlm.so")
 
 QLM_OK, QLM_EINVAL, QLM_ENOMEM, QLM_ECUDA, QLM_EBADORDER, QLM_ERANGE = 0, 1, 2, 3, 5, 6
 CAND_EXPLICIT, CAND_RANDOM, CAND_ENUM = 0, 1, 2

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
             ScanState s;
             start_queue(tab, s, 0);
             double S2 = 0.0;
-            float acc = 0.0f;                                     // sum n_i v_i (row order)
+            float acc1 = 0.0f, acc2 = 0.0f;       // sum n_i v_i: clamped / unclamped slots, row order
             int over = 0;
             for_tokens<KIND, TOK>(cd, T, scratch, blk, loc, first + loc, [&](int tok) {
                 if (tok >= G) {                          // queue separator
@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                 const float v = violation(slack, V, zc2, clamped);
                 if constexpr (SCORE) {
                     S2 = __dsub_rn(S2, slack);                    // sum_i p_i
-                    acc = fmaf((float)g.n, v, acc);
+                    if (clamped) acc1 = fmaf((float)g.n, v, acc1);
+                    else acc2 = fmaf((float)g.n, v, acc2);
                     over += v > alpha;
                 }
                 if constexpr (OUT == OUT_STAGED) {
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                 }
             });
             if constexpr (SCORE) {
-                const float s1 = (float)((double)acc / den);   // R11
+                const float s1 = (float)(((double)acc1 + (double)acc2) / den);   // R11
                 const float s2 = (float)S2;
                 if (p.s1) p.s1[loc] = s1;
                 if (p.s2) p.s2[loc] = s2;

@@ -37,7 +37,7 @@ struct alignas(64) WsParams {
     ScanParams p;
     int pairs;             // W
     int tw;                // 32-bit words per row slot column
-    int off_rows, off_stage, off_bar;
+    int off_rows, off_stage, off_bar, off_pend;
     int stage_floats;      // per consumer warp: 3 * G * 32
     int use_tma;
 };
@@ -124,16 +124,46 @@ struct WsQ {                 // 32 B
 
 struct Acc {
     double A, B, S2;
-    float acc;               // sum n_i v_i (row order)
-    int prow, dG, dbase, q, over;
+    float acc1;              // sum n_i v_i over clamped slots (v in {0, 1}: exact)
+    float acc2;              // sum n_i v_i over unclamped slots, row order
+    int prow, dG, dbase, q, over, npend;
 };
+
+// Unclamped slots (|z| < z_clamp, ~1-2 % of slots) are queued per lane --
+// (z, group) in shared memory -- and their Phi-bar evaluated later in FIFO
+// (= row) order, so the warp runs the expensive path only for the lanes and
+// slots that need it instead of for the whole warp on every slot where any
+// lane needs it.
+constexpr int kPend = 8;     // queue depth per lane
+struct Pend {
+    float z;
+    int tg;
+};
+
+template <bool SCORE, int RSCALE>
+__device__ __forceinline__ void flush_pending(Pend *pq, const WsG *__restrict__ sgl, int lane,
+                                              float alpha, float *st2, Acc &a) {
+    const int maxn = (int)__reduce_max_sync(__activemask(), (unsigned)a.npend);
+    for (int i = 0; i < maxn; ++i) {
+        if (i < a.npend) {
+            const Pend e = pq[i * 32 + lane];
+            const float v = phibar(e.z);
+            st2[e.tg * 32 + lane] = v;
+            if constexpr (SCORE) {
+                a.acc2 = fmaf(sgl[e.tg * RSCALE].nf, v, a.acc2);
+                a.over += v > alpha ? 1 : 0;
+            }
+        }
+    }
+    a.npend = 0;
+}
 
 template <typename TOK, int RS, bool SCORE, bool PAD>
 __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const double2 *__restrict__ sabl,
                                              const double2 *__restrict__ str, const WsQ *__restrict__ sq,
                                              uint32_t word, int nvalid_tok, int G, int M, int lane,
                                              float zc2f, float alpha, float *st, int arr_stride,
-                                             Acc &a) {
+                                             Pend *pq, Acc &a) {
     constexpr int K = 4 / (int)sizeof(TOK);
     int isbar[K], tg[K];
     WsG g[K];
@@ -194,22 +224,28 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
         const float rr = rsqrt_approx(fmaxf(Vf, 1e-30f));
         // |z| >= z_clamp  <=>  slack^2 >= z_clamp^2 V   (R9; exact for V = 0)
         const bool clamped = sf * sf >= zc2f * Vf;
-        float v = sf < 0.0f ? 1.0f : 0.0f;
-        if (__any_sync(__activemask(), !clamped)) {      // warp-uniform: ~40 % of slots
-            const float pz = phibar(sf * rr);
-            v = clamped ? v : pz;
+        const float v = sf < 0.0f ? 1.0f : 0.0f;              // clamped value (R9)
+        const bool grp = !isbar[k] && tg[k] < G;
+        const bool defer = grp && !clamped;
+        if (defer) {                                           // exact value later, FIFO
+            Pend e;
+            e.z = sf * rr;
+            e.tg = tg[k];
+            pq[a.npend * 32 + lane] = e;
+            ++a.npend;
         }
         if constexpr (SCORE) {
-            const bool grp = !isbar[k] && tg[k] < G;
             a.S2 = __dsub_rn(a.S2, grp ? slack : 0.0);
-            a.acc = fmaf(g[k].nf, v, a.acc);                // separator / pad records have nf = 0
-            a.over += (grp && v > alpha) ? 1 : 0;
+            if (!defer) {
+                a.acc1 = fmaf(g[k].nf, v, a.acc1);             // separators have nf = 0
+                a.over += (grp && v > alpha) ? 1 : 0;
+            }
         }
         if (st) {
             float *o = st + tg[k] * 32 + lane;               // separators -> trash row G
             o[0] = (float)wt[k];
             o[arr_stride] = Vf * rr;
-            o[2 * arr_stride] = v;
+            o[2 * arr_stride] = v;                           // deferred slots overwritten at flush
         }
     }
 }
@@ -344,8 +380,11 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         const int arr = (G + 1) * 32;
         float *st = reinterpret_cast<float *>(smem + w.off_stage) + (size_t)pair * w.stage_floats;
         float *st0 = st, *st1 = st + arr, *st2 = st + 2 * arr;
+        Pend *pq = reinterpret_cast<Pend *>(smem + w.off_pend) + (size_t)pair * kPend * 32;
+        const WsG *sgl_rs = sg + ((size_t)(lane & ((1 << RS) - 1)));   // flush reads record tg << RS
         constexpr int EPW = 4 / (int)sizeof(TOK);
         const int full_words = T / EPW;
+        const int tw = w.tw;
         for (int j = 0;; ++j) {
             const int64_t b = blockIdx.x + (int64_t)(pair + j * W) * grid;
             if (b >= nbatch) break;
@@ -361,16 +400,23 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
                 Acc a;
                 const WsQ r0 = sq[0];
                 a.A = r0.bmean; a.B = r0.bvar; a.prow = r0.prow0; a.dG = r0.dG; a.dbase = r0.dbase;
-                a.q = 0; a.S2 = 0.0; a.acc = 0.0f; a.over = 0;
-                for (int wi = 0; wi < full_words; ++wi)
-                    consume_word<TOK, RS, SCORE, false>(sgl, sabl, str, sq, w32[wi * 32 + lane], EPW, G,
-                                                        M, lane, zc2f, alpha, st, arr, a);
+                a.q = 0; a.S2 = 0.0; a.acc1 = 0.0f; a.acc2 = 0.0f; a.over = 0; a.npend = 0;
+                uint32_t cur = w32[lane];
+                for (int wi = 0; wi < full_words; ++wi) {
+                    const uint32_t nxt = w32[(wi + 1 < tw ? wi + 1 : wi) * 32 + lane];   // prefetch
+                    consume_word<TOK, RS, SCORE, false>(sgl, sabl, str, sq, cur, EPW, G,
+                                                        M, lane, zc2f, alpha, st, arr, pq, a);
+                    cur = nxt;
+                    if (__any_sync(__activemask(), a.npend > kPend - EPW))
+                        flush_pending<SCORE, (1 << RS)>(pq, sgl_rs, lane, alpha, st2, a);
+                }
                 if (full_words * EPW < T)
-                    consume_word<TOK, RS, SCORE, true>(sgl, sabl, str, sq, w32[full_words * 32 + lane],
+                    consume_word<TOK, RS, SCORE, true>(sgl, sabl, str, sq, cur,
                                                        T - full_words * EPW, G, M, lane, zc2f, alpha,
-                                                       st, arr, a);
+                                                       st, arr, pq, a);
+                flush_pending<SCORE, (1 << RS)>(pq, sgl_rs, lane, alpha, st2, a);
                 if constexpr (SCORE) {
-                    const float s1 = (float)((double)a.acc / den);     // R11
+                    const float s1 = (float)(((double)a.acc1 + (double)a.acc2) / den);     // R11
                     const float s2 = (float)a.S2;
                     if (p.s1) p.s1[loc] = s1;
                     if (p.s2) p.s2[loc] = s2;
@@ -459,6 +505,7 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
     w.tw = (dm.T + epw - 1) / epw;
     w.off_rows = (int)off; off = a16(off + (size_t)2 * W * w.tw * 128);
     w.off_bar = (int)off;  off = a16(off + (size_t)4 * W * 8);
+    w.off_pend = (int)off; off = a16(off + (size_t)W * kPend * 32 * sizeof(Pend));
     w.stage_floats = stage ? 3 * (dm.G + 1) * 32 : 0;
     off = a1k(off);
     w.off_stage = (int)off;

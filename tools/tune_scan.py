@@ -38,10 +38,10 @@ def main():
     out = {k: torch.empty((p.G, N), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
     rec = torch.empty(2, dtype=torch.int64, device="cuda")
     byts = 12 * p.G * N
-    configs = [dict()] + [dict(QLM_WS_DIRECT=1, QLM_WS_PAIRS=w_) for w_ in (16, 12, 8)] + \
-        [dict(QLM_WS_PAIRS=w_, QLM_REP_SHIFT=r) for w_ in (7, 6) for r in (3,)] + \
+    quick = os.environ.get("TUNE_QUICK")
+    configs = [dict()] if quick else [dict()] + [dict(QLM_WS_PAIRS=w_, QLM_REP_SHIFT=r) for w_ in (7, 6) for r in (3, 0)] + \
         [dict(QLM_NO_WS=1, QLM_BLK=b, QLM_REP_SHIFT=r) for b in (128,) for r in (0,)]
-    keys = ("QLM_WS_PAIRS", "QLM_REP_SHIFT", "QLM_NO_WS", "QLM_BLK", "QLM_WS_DIRECT")
+    keys = ("QLM_WS_PAIRS", "QLM_REP_SHIFT", "QLM_NO_WS", "QLM_BLK")
     for cfgd in configs:
         blk, rs = cfgd, ""
         for k, v in ((k, cfgd.get(k)) for k in keys):
