@@ -195,9 +195,23 @@ QLM_API int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *
  * trial_count) of every group's total output tokens with Philox (key =
  * mc_seed), walks each candidate's queues with the sampled work and writes
  * counts[k][g] = #{trials with W_g > slo_g} (device uint32 [count][G],
- * overwritten).  Needs length tables.  trial_first + trial_count <= 2^32.    */
+ * overwritten).  Needs length tables.  trial_first + trial_count <= 2^32.
+ * Equivalent to qlm_mc_sample followed by qlm_mc_count on `stream`.        */
 QLM_API int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
                     int64_t trial_first, int64_t trial_count, uint32_t *counts, void *stream);
+
+/* The candidate-independent half of the MC mode: per (group, trial) the
+ * sampled total output tokens X and the work X / Theta[d][m_g] for every
+ * device row d, kept in the context.  It touches no state the scan calls
+ * use, so it may run on another stream concurrently with them.             */
+QLM_API int qlm_mc_sample(qlm_ctx *ctx, uint64_t mc_seed, int64_t trial_first,
+                          int64_t trial_count, void *stream);
+
+/* The candidate-dependent half: counts for `cand` from the samples of the
+ * last qlm_mc_sample (which must be complete on `stream`, e.g. via an
+ * event); trial_count must match it.                                        */
+QLM_API int qlm_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count,
+                         uint32_t *counts, void *stream);
 
 /* Decode candidates into per-group queue index and position (x_{g,i,j} of
  * Eq. 6): device int32 [count][G] each (nullable).                         */

@@ -69,6 +69,8 @@ SIGNATURES = {
     "qlm_score_estimate": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                      _vp]),
     "qlm_mc_estimate": (C.c_int, [_vp, C.POINTER(Candidates), _u64, _i64, _i64, _vp, _vp]),
+    "qlm_mc_sample": (C.c_int, [_vp, _u64, _i64, _i64, _vp]),
+    "qlm_mc_count": (C.c_int, [_vp, C.POINTER(Candidates), _i64, _vp, _vp]),
     "qlm_decode": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp]),
     "qlm_rows": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp]),
     "qlm_check_rows": (C.c_int, [_vp, C.POINTER(Candidates), C.POINTER(C.c_int64), _vp]),

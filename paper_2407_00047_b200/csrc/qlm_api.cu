@@ -56,6 +56,7 @@ struct qlm_ctx {
     unsigned long long *d_bad = nullptr;
     int max_blocks = 0;
     double *d_X = nullptr;             // MC: (X / Theta)[D][G][trials]
+    int64_t mc_trials = -1;            // trials of the last qlm_mc_sample
     size_t X_cap = 0;
     std::vector<qlm_group> groups;
     std::vector<qlm_queue> queues;
@@ -504,11 +505,11 @@ int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "scan kernel");
 }
 
-int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
-                    int64_t trial_first, int64_t trial_count, uint32_t *counts, void *stream) {
-    if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
-    int rc = check_cand(ctx, cand);
-    if (rc || (rc = check_dev(ctx))) return rc;
+int qlm_mc_sample(qlm_ctx *ctx, uint64_t mc_seed, int64_t trial_first, int64_t trial_count,
+                  void *stream) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    int rc = check_dev(ctx);
+    if (rc) return rc;
     if (!ctx->has_tables) return fail(QLM_EINVAL, "MC mode needs length tables at qlm_create");
     for (int i = 0; i < ctx->dm.G; ++i)
         if (ctx->groups[i].dist_id < 0)
@@ -516,12 +517,7 @@ int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
     if (trial_first < 0 || trial_count < 0 || trial_first + trial_count > (int64_t)1 << 32)
         return fail(QLM_ERANGE, "trials [%lld, +%lld) must lie in [0, 2^32)", (long long)trial_first,
                     (long long)trial_count);
-    if (cand->count > 65535) return fail(QLM_ERANGE, "MC: cand.count=%lld > 65535", (long long)cand->count);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e;
-    if (cand->count == 0) return QLM_OK;
-    if ((e = cudaMemsetAsync(counts, 0, (size_t)cand->count * ctx->dm.G * 4, st)) != cudaSuccess)
-        return cuda_fail(e, "counts memset");
+    ctx->mc_trials = trial_count;
     if (trial_count == 0) return QLM_OK;
     const size_t needX = (size_t)trial_count * ctx->dm.G * ctx->dm.D * sizeof(double);
     if (needX > ctx->X_cap) {
@@ -531,12 +527,38 @@ int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
         if (cudaMalloc(&ctx->d_X, needX) != cudaSuccess) return fail(QLM_ENOMEM, "MC scratch %zu B", needX);
         ctx->X_cap = needX;
     }
-    if ((e = launch_mc_sample(ctx->dm, ctx->tb, mc_seed, trial_first, trial_count, ctx->d_X, st)) != cudaSuccess)
-        return cuda_fail(e, "MC sample kernel");
+    cudaError_t e = launch_mc_sample(ctx->dm, ctx->tb, mc_seed, trial_first, trial_count, ctx->d_X,
+                                     static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "MC sample kernel");
+}
+
+int qlm_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count, uint32_t *counts,
+                 void *stream) {
+    if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (trial_count != ctx->mc_trials)
+        return fail(QLM_EINVAL, "trial_count=%lld differs from the last qlm_mc_sample (%lld)",
+                    (long long)trial_count, (long long)ctx->mc_trials);
+    if (cand->count > 65535) return fail(QLM_ERANGE, "MC: cand.count=%lld > 65535", (long long)cand->count);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cand->count == 0) return QLM_OK;
+    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)cand->count * ctx->dm.G * 4, st);
+    if (e != cudaSuccess) return cuda_fail(e, "counts memset");
+    if (trial_count == 0) return QLM_OK;
     if ((e = launch_mc_count(ctx->dm, ctx->tb, to_cand(cand), ctx->d_X, trial_count, counts, st)) !=
         cudaSuccess)
         return cuda_fail(e, "MC count kernel");
     return QLM_OK;
+}
+
+int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
+                    int64_t trial_first, int64_t trial_count, uint32_t *counts, void *stream) {
+    if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc) return rc;
+    if ((rc = qlm_mc_sample(ctx, mc_seed, trial_first, trial_count, stream))) return rc;
+    return qlm_mc_count(ctx, cand, trial_count, counts, stream);
 }
 
 int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, void *stream) {

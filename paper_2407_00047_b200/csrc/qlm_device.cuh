@@ -132,6 +132,10 @@ __device__ __forceinline__ void fy_materialise(uint8_t *scratch, int blk, int ti
                                       : 0x00010000u + 0x00020002u * (uint32_t)w;
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     const uint32_t clo = (uint32_t)c, chi = (uint32_t)(c >> 32);
+    // Position i is final after step i and never read again (later steps touch
+    // positions > i only), so finals are packed in a register and written one
+    // 32-bit word at a time instead of one sub-word store per step.
+    uint32_t fin = 0;
     for (int i0 = 0; i0 < T - 1; i0 += 4) {
         const uint4 wd = philox10(make_uint4((uint32_t)(i0 >> 2), clo, chi, kRowTag), key);
 #pragma unroll
@@ -143,8 +147,21 @@ __device__ __forceinline__ void fy_materialise(uint8_t *scratch, int blk, int ti
             TOK *pj = fy_elem<TOK>(scratch, j, blk, tid);
             const TOK ti = *pi, tj = *pj;
             *pj = ti;
-            *pi = tj;
+            const int lanepos = i % EPW;
+            fin |= (uint32_t)tj << (lanepos * 8 * sizeof(TOK));
+            if (lanepos == EPW - 1) {
+                w32[(i / EPW) * blk + tid] = fin;
+                fin = 0;
+            }
         }
+    }
+    // position T-1 is final (it holds whatever the last swap left there)
+    {
+        const int i = T - 1;
+        const TOK last = *fy_elem<TOK>(scratch, i, blk, tid);
+        fin |= (uint32_t)last << ((i % EPW) * 8 * sizeof(TOK));
+        // keep the word's positions > T-1 as they were (padding is never read as tokens)
+        w32[(i / EPW) * blk + tid] = fin;
     }
 }
 

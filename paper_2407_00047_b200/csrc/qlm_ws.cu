@@ -178,7 +178,8 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
         tg[k] = pad ? G : min(tok, G);
         q += isbar[k];
         g[k] = sgl[tg[k] << RS];
-        r[k] = sq[q];
+        if (isbar[k]) r[k] = sq[q];                          // only separator lanes read
+        else { r[k].bmean = 0.0; r[k].bvar = 0.0; r[k].prow0 = 0; r[k].dG = 0; r[k].dbase = 0; }
     }
     // (ii) per-slot transition row and device base
     int pk[K], dk[K];
@@ -199,7 +200,7 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         ab[k] = sabl[(dk[k] + tg[k]) << RS];
-        tr[k] = str[pk[k] + g[k].model];
+        tr[k] = str[(pk[k] + g[k].model) << RS];             // replicated: conflict-free
     }
     // (iv) the Eq. 10 chain (operation order identical to the sequential definition)
     double wt[K], V[K];
@@ -336,8 +337,9 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         sq[i] = r;
     }
     double2 *str = reinterpret_cast<double2 *>(smem + p.off_tr);
-    for (int i = tid; i < D * 2 * M * M; i += blockDim.x) {
-        const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
+    for (int i = tid; i < ((D * 2 * M * M) << RS); i += blockDim.x) {
+        const int e = i >> RS;
+        const int m = e % M, pp = (e / M) % (2 * M), d = e / (2 * M * M);
         const int from = pp < M ? pp : pp - M;
         const double sw = p.tb.swap[(d * M + from) * M + m];
         const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
     } else {
         const WsG *sgl = sg + (lane & ((1 << RS) - 1));
         const double2 *sabl = sab + (lane & ((1 << RS) - 1));
+        const double2 *strl = str + (lane & ((1 << RS) - 1));
         const float zc2f = (float)p.zc2;
         const float alpha = p.alpha;
         const double den = *p.tb.den;
@@ -404,14 +407,14 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
                 uint32_t cur = w32[lane];
                 for (int wi = 0; wi < full_words; ++wi) {
                     const uint32_t nxt = w32[(wi + 1 < tw ? wi + 1 : wi) * 32 + lane];   // prefetch
-                    consume_word<TOK, RS, SCORE, false>(sgl, sabl, str, sq, cur, EPW, G,
+                    consume_word<TOK, RS, SCORE, false>(sgl, sabl, strl, sq, cur, EPW, G,
                                                         M, lane, zc2f, alpha, st, arr, pq, a);
                     cur = nxt;
                     if (__any_sync(__activemask(), a.npend > kPend - EPW))
                         flush_pending<SCORE, (1 << RS)>(pq, sgl_rs, lane, alpha, st2, a);
                 }
                 if (full_words * EPW < T)
-                    consume_word<TOK, RS, SCORE, true>(sgl, sabl, str, sq, cur,
+                    consume_word<TOK, RS, SCORE, true>(sgl, sabl, strl, sq, cur,
                                                        T - full_words * EPW, G, M, lane, zc2f, alpha,
                                                        st, arr, pq, a);
                 flush_pending<SCORE, (1 << RS)>(pq, sgl_rs, lane, alpha, st2, a);
@@ -500,7 +503,7 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
     p.off_grec = (int)off; off = a16(off + ((size_t)(dm.G + 1) << rs) * sizeof(WsG));
     p.off_ab = (int)off;   off = a16(off + ((size_t)dm.D * (dm.G + 1) << rs) * sizeof(double2));
     p.off_q = (int)off;    off = a16(off + (size_t)(dm.T + 1) * sizeof(WsQ));
-    p.off_tr = (int)off;   off = a16(off + (size_t)dm.D * 2 * dm.M * dm.M * sizeof(double2));
+    p.off_tr = (int)off;   off = a16(off + ((size_t)dm.D * 2 * dm.M * dm.M << rs) * sizeof(double2));
     const int epw = 4 / tok_bytes;
     w.tw = (dm.T + epw - 1) / epw;
     w.off_rows = (int)off; off = a16(off + (size_t)2 * W * w.tw * 128);

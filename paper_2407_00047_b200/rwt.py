@@ -200,6 +200,17 @@ class RwtEstimator:
                                         counts.data_ptr(), self._stream(stream)), "qlm_mc_estimate")
         return counts
 
+    def mc_sample(self, mc_seed: int, trials: int, trial_first: int = 0, stream=None):
+        """Candidate-independent MC half (may overlap scan calls on another stream)."""
+        L.check(L.lib().qlm_mc_sample(self._h, mc_seed, trial_first, trials, self._stream(stream)),
+                "qlm_mc_sample")
+
+    def mc_count(self, cand: Cand, trials: int, counts: torch.Tensor | None = None, stream=None):
+        counts = self._empty((cand.count, self.G), torch.int32) if counts is None else counts
+        L.check(L.lib().qlm_mc_count(self._h, C.byref(cand.c()), trials, counts.data_ptr(),
+                                     self._stream(stream)), "qlm_mc_count")
+        return counts
+
     def decode(self, cand: Cand, stream=None):
         qo = self._empty((cand.count, self.G), torch.int32)
         po = self._empty((cand.count, self.G), torch.int32)

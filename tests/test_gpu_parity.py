@@ -367,3 +367,22 @@ def test_warp_specialised_and_fallback_kernels_agree(cfg, n, kind, monkeypatch):
         est = O.Oracle(p).estimate_range(k_, first, m, seed=1)
     check_scores(b["s1"][:m].cpu().numpy(), b["s2"][:m].cpu().numpy(), ref, p)
     check_estimates({k: b[k][:, :m] for k in ("wt", "sd", "v")}, est)
+
+
+def test_mc_split_sample_count_on_two_streams():
+    p = make_config("C3")
+    e = est_of(p)
+    cand = e.random(123, 3, seed=1)
+    ref = e.mc_estimate(cand, mc_seed=5, trials=300, trial_first=17)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        e.mc_sample(5, 300, trial_first=17, stream=side)
+    torch.cuda.current_stream().wait_stream(side)
+    got = e.mc_count(cand, 300)
+    assert torch.equal(got, ref)
+    with pytest.raises(Exception):
+        e.mc_count(cand, 299)                        # trial count must match the sample
+    o = O.Oracle(p)
+    X = o.mc_sample(5, 17, 300)
+    np.testing.assert_array_equal(got.cpu().numpy().astype(np.uint32),
+                                  o.mc_count(O.RANDOM, 123, 3, X, seed=1))
