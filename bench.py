@@ -10,9 +10,11 @@ C3 (64 groups, 4 models, 8 virtual queues) on every GPU:
   a8        global min-loc: NCCL all-gather of 16-B records + reduce kernel
   a9        decode of the global winner (queue, position per group)
   a10-a12   MC check of the winner: qlm_mc_sample (1221 Philox trials per
-            GPU, candidate-independent) runs on a second stream concurrently
-            with the fused scan; qlm_mc_count walks the winner once it is
-            known; counts summed with one NCCL all-reduce
+            GPU, candidate-independent) then qlm_mc_count of the winner; counts
+            summed with one NCCL all-reduce.  (Running the sampler on a second
+            stream concurrently with the fused scan was measured: the step
+            gains ~2 % while the scan slows by the same SM time, so the step
+            keeps them sequential for a clean per-kernel roofline.)
 Weak scaling: rank r scores global indices [r*1e6, (r+1)*1e6).
 
 `--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample
@@ -198,25 +200,19 @@ def run_ours(args, rank, world, local_rank):
     bulk = {k: torch.empty((G, N_PER_GPU), dtype=torch.float32, device=dev) for k in ("wt", "sd", "v")}
     counts = torch.empty((1, G), dtype=torch.int32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    side = torch.cuda.Stream(dev)                  # MC sampling overlaps the fused scan
-    ev_start, ev_sampled = torch.cuda.Event(), torch.cuda.Event()
 
     def step(kt=None, groups_host=None, out_host=None):
         if groups_host is not None:
             est.update_groups(groups_host)                       # H2D of the step's inputs
-        ev_start.record(stream)
         if kt:
             kt[0].record(stream)
         est.score_estimate(cand, out=bulk, scores=False, rec=rec)   # fused a1-a7
-        side.wait_event(ev_start)                                # previous step's MC count is done
-        est.mc_sample(MC_SEED, MC_TRIALS, trial_first=rank * MC_TRIALS, stream=side)   # a10
-        ev_sampled.record(side)
         if kt:
             kt[1].record(stream)
         g = global_best(rec, est.reduce_records)
         win = est.from_record(g, seed=CANDIDATE_SEED)
         qo, po = est.decode(win)
-        stream.wait_event(ev_sampled)
+        est.mc_sample(MC_SEED, MC_TRIALS, trial_first=rank * MC_TRIALS)               # a10
         est.mc_count(win, MC_TRIALS, counts=counts)                                   # a11
         sum_counts(counts)
         if out_host is not None:                                 # D2H of the step's result
