@@ -48,19 +48,27 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C5", "C5h"],
+                    help="workload (BASELINE.json configs); the metric is quoted on C3")
+    ap.add_argument("--candidates", type=int, default=None,
+                    help="candidates per GPU per step (default 1e6)")
     return ap.parse_args()
 
 
+SHAPES = {"C2": (16, 2, 2), "C3": (64, 8, 4), "C5": (1024, 32, 4), "C5h": (1024, 32, 4)}
+
+
 def workload_config(world):
+    G, Q, M = SHAPES[CFG]
     return {
-        "workload": f"{CFG}: 64 request groups, 4 models (7B/13B/70B-like), 8 virtual queues "
-                    f"(A100-like profile, App. B); per GPU per step {N_PER_GPU:.0e} RANDOM candidate "
+        "workload": f"{CFG}: {G} request groups, {M} models (7B/13B/70B-like), {Q} virtual queues "
+                    f"(App. B profiles); per GPU per step {N_PER_GPU:.0e} RANDOM candidate "
                     f"orderings scored + argmin, bulk per-group wt/sd/v for all of them, "
                     f"MC ({MC_TRIALS} trials) of the global winner",
-        "groups": 64, "queues": 8, "models": 4, "candidates_per_gpu": N_PER_GPU,
+        "groups": G, "queues": Q, "models": M, "candidates_per_gpu": N_PER_GPU,
         "mc_trials_per_gpu": MC_TRIALS, "parallelism": f"dp{world}",
-        "l2": "not flushed explicitly: every step writes 768 MB of bulk estimates per GPU "
-              "(>6x the 126 MB L2), evicting it between steps",
+        "l2": f"not flushed explicitly: every step writes {12 * G * N_PER_GPU / 1e6:.0f} MB of bulk "
+              "estimates per GPU (> the 126 MB L2), evicting it between steps",
     }
 
 
@@ -141,7 +149,7 @@ def cpu_baseline(budget_s: float = 15.0):
     trials = max(1, round(MC_TRIALS * n / N_PER_GPU))
     t = oracle_sample(n, trials)
     return {"value": n / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n} of the {N_PER_GPU} C3 candidates of one step (score+argmin, bulk "
+            "sample": f"{n} of the {N_PER_GPU} {CFG} candidates of one step (score+argmin, bulk "
                       f"estimates) + MC {trials} of {MC_TRIALS} trials, single-threaded plain C fp64 "
                       f"(-O2 -ffp-contract=off), {t:.2f} s; value = sampled candidates / s"}
 
@@ -167,7 +175,7 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"each step: {n} of the {N_PER_GPU} C3 candidates (score+argmin, "
+                         "sample": f"each step: {n} of the {N_PER_GPU} {CFG} candidates (score+argmin, "
                                    f"bulk estimates) + MC {trials} of {MC_TRIALS} trials; plain C "
                                    f"fp64 oracle, single thread"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -300,6 +308,7 @@ def run_ours(args, rank, world, local_rank):
             "fallback 6650 GB/s (B200_PROFILING.md)"
         hbm_peak = hbm_peak or 6650.0
         bulk_bytes = N_PER_GPU * G * 3 * 4                     # algorithmic: outputs only (RANDOM)
+        kname = ("ws_kernel<RANDOM,u8,SCORE,RS=3>" if G <= 256 else "scan_kernel<RANDOM,u16,DIRECT,SCORE>")
         bulk_gbs = bulk_bytes / (fused_ms / 1e3) / 1e9
         traffic = None
         try:
@@ -307,7 +316,7 @@ def run_ours(args, rank, world, local_rank):
                 traffic = json.load(f).get(CFG, {}).get("scan_kernel_dram_bytes_per_launch")
         except Exception:
             pass
-        roofline = {"kernel": "ws_kernel<RANDOM,u8,STAGE,SCORE> (qlm_score_estimate, fused a1-a7)", "bound": "hbm",
+        roofline = {"kernel": kname + " (qlm_score_estimate, fused a1-a7)", "bound": "hbm",
                     "achieved": bulk_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": bulk_gbs / hbm_peak, "traffic": traffic,
                     "algorithmic_bytes_per_launch": bulk_bytes,
@@ -334,7 +343,13 @@ def run_ours(args, rank, world, local_rank):
 
 
 def main():
+    global CFG, N_PER_GPU
     args = parse()
+    CFG = args.config
+    if args.candidates:
+        N_PER_GPU = args.candidates
+    elif CFG in ("C5", "C5h"):
+        N_PER_GPU = 100_000          # 1024 groups: 12 GB of bulk output would be 1e6
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

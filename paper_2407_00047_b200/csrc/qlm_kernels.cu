@@ -498,10 +498,9 @@ __global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand c
         if (first < 0) return;
     }
     const int T = dm.T, G = dm.G, M = dm.M;
-    double *sy = reinterpret_cast<double *>(smem);                                   // [G][32]
-    uint16_t *stok = reinterpret_cast<uint16_t *>(smem + (size_t)G * 32 * 8);         // [G]
+    uint16_t *stok = reinterpret_cast<uint16_t *>(smem);                             // [G]
     uint16_t *sq = stok + G;                                                         // [G]
-    uint4 *swords = reinterpret_cast<uint4 *>(smem + (size_t)G * 32 * 8 + (((size_t)4 * G + 15) & ~15));
+    uint4 *swords = reinterpret_cast<uint4 *>(smem + (((size_t)4 * G + 15) & ~15));
     uint16_t *srow = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(swords) +
                                                   (size_t)((T + 2) / 4 + 1) * 16);
     const int64_t loc = blockIdx.y;
@@ -520,41 +519,46 @@ __global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand c
     __syncwarp();
     const int64_t tl = (int64_t)blockIdx.x * 32 + lane;
     const bool act = tl < nt;
-    // phase 1: gather y_i = (X / Theta)[d_i][g_i][t] for the row's group slots into
-    // shared memory, 8 independent loads at a time.
-    for (int i0 = 0; i0 < G; i0 += 8) {
-        double yv[8];
+    // Walk the group slots in row order.  y_i = (X / Theta)[d_i][g_i][t] (Eq. 2
+    // with the realised token count) is loaded 8 slots ahead into registers, so
+    // the global loads overlap the sequential chain for any G.
+    auto load8 = [&](int i0, double *y) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int i = i0 + k < G ? i0 + k : G - 1;
             const int64_t row = (int64_t)tb.qrec[sq[i]].d * G + stok[i];
-            yv[k] = act ? __ldg(&Y[row * nt + tl]) : 0.0;
+            y[k] = act ? __ldg(&Y[row * nt + tl]) : 0.0;
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (i0 + k < G) sy[(i0 + k) * 32 + lane] = yv[k];
-    }
-    __syncwarp();
-    // phase 2: the sequential chain and the counts
+    };
+    double cur[8], nxt[8];
+    load8(0, cur);
     int q = -1, d = 0, prev = 0, firstslot = 1, backlog = 0;
     double A = 0.0;
-    for (int i = 0; i < G; ++i) {
-        const int tok = stok[i], qi = sq[i];
-        if (qi != q) {                                   // first group of queue qi
-            const QRec qr = tb.qrec[qi];
-            q = qi; A = qr.bmean; d = qr.d; prev = qr.r; firstslot = 1; backlog = qr.backlog;
+    for (int i0 = 0; i0 < G; i0 += 8) {
+        if (i0 + 8 < G) load8(i0 + 8, nxt);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = i0 + k;
+            if (i >= G) break;
+            const int tok = stok[i], qi = sq[i];
+            if (qi != q) {                               // first group of queue qi
+                const QRec qr = tb.qrec[qi];
+                q = qi; A = qr.bmean; d = qr.d; prev = qr.r; firstslot = 1; backlog = qr.backlog;
+            }
+            const GRec g = tb.grec[tok];
+            const int m = g.model;
+            if (m != prev) {
+                const double t = (firstslot && !backlog) ? 0.0 : tb.tail[d * M + prev];
+                A = __dadd_rn(A, t);
+                A = __dadd_rn(A, tb.swap[(d * M + prev) * M + m]);
+            }
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, act && A > g.slo);
+            if (lane == 0 && bal) atomicAdd(&counts[loc * G + tok], (unsigned)__popc(bal));
+            A = __dadd_rn(A, cur[k]);
+            prev = m; firstslot = 0;
         }
-        const GRec g = tb.grec[tok];
-        const int m = g.model;
-        if (m != prev) {
-            const double t = (firstslot && !backlog) ? 0.0 : tb.tail[d * M + prev];
-            A = __dadd_rn(A, t);
-            A = __dadd_rn(A, tb.swap[(d * M + prev) * M + m]);
-        }
-        const unsigned bal = __ballot_sync(0xFFFFFFFFu, act && A > g.slo);
-        if (lane == 0 && bal) atomicAdd(&counts[loc * G + tok], (unsigned)__popc(bal));
-        A = __dadd_rn(A, sy[i * 32 + lane]);
-        prev = m; firstslot = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
     }
 }
 
@@ -809,7 +813,7 @@ cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, in
 
 cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const Cand &cd, const double *X,
                             int64_t nt, uint32_t *counts, cudaStream_t st) {
-    const size_t smem = (size_t)dm.G * 32 * 8 + align16((size_t)4 * dm.G) +
+    const size_t smem = align16((size_t)4 * dm.G) +
                         (size_t)((dm.T + 2) / 4 + 1) * 16 + align16((size_t)dm.T * 2 + 4);
     cudaError_t e = prep(mc_count_kernel, smem);
     if (e != cudaSuccess) return e;

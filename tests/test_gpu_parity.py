@@ -386,3 +386,30 @@ def test_mc_split_sample_count_on_two_streams():
     X = o.mc_sample(5, 17, 300)
     np.testing.assert_array_equal(got.cpu().numpy().astype(np.uint32),
                                   o.mc_count(O.RANDOM, 123, 3, X, seed=1))
+
+
+def test_nccl_plumbing_single_rank():
+    """The multi-GPU exchange (a8, a12) through NCCL on one rank: all-gather of
+    the 16-B record + qlm_reduce_records, and the MC count all-reduce."""
+    import socket
+    import torch.distributed as dist
+    from paper_2407_00047_b200.dist import gather_records, sum_counts
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        p = make_config("C2")
+        e = est_of(p)
+        rec = e.best_ordering_async(e.random(0, 20000, seed=1))
+        g = gather_records(rec)
+        assert g.shape == (2,) and torch.equal(g, rec)
+        assert torch.equal(e.reduce_records(g), rec)
+        cnt = torch.arange(16, dtype=torch.int32, device="cuda")
+        assert torch.equal(sum_counts(cnt.clone()), cnt)
+    finally:
+        dist.destroy_process_group()
