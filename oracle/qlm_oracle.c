@@ -279,13 +279,14 @@ int64_t or_estimate_range(const or_problem *p, int kind, const void *rows, int32
 
 /* ---- Monte-Carlo mode (R13) ----------------------------------------------
  * Output lengths are sampled per request: for trial t, group k, request r,
- *   word = Philox4x32-10(key = mc_seed, ctr = (r/4, k, t, 0x4D430000))[r%4]
- *   O    = len[dist_k][word >> (32 - log2 K)]
+ *   w    = Philox4x32-10(key = mc_seed, ctr = (r/8, k, t, 0x4D430000))[(r/2) % 4]
+ *   u16  = r even ? low 16 bits of w : high 16 bits of w
+ *   O    = len[dist_k][u16 >> (16 - log2 K)]          (K divides 2^16: unbiased)
  * X[t][k] = sum_r O (exact integer), the group's total output tokens.      */
 void or_mc_sample(const or_problem *p, uint64_t mc_seed, int64_t trial_first,
                   int64_t trial_count, uint32_t *X /* [trial_count][G] */)
 {
-    int32_t shift = 32;
+    int32_t shift = 16;
     for (int32_t k = p->K; k > 1; k >>= 1) --shift;
     uint32_t key[2] = { (uint32_t)mc_seed, (uint32_t)(mc_seed >> 32) };
     uint32_t words[4];
@@ -295,11 +296,13 @@ void or_mc_sample(const or_problem *p, uint64_t mc_seed, int64_t trial_first,
             const uint16_t *tab = p->len + (int64_t)p->dist[k] * p->K;
             uint32_t sum = 0;
             for (int32_t r = 0; r < p->n_req[k]; ++r) {
-                if (r % 4 == 0) {
-                    uint32_t ctr[4] = { (uint32_t)(r / 4), (uint32_t)k, t, 0x4D430000u };
+                if (r % 8 == 0) {       /* one Philox block yields 8 16-bit draws */
+                    uint32_t ctr[4] = { (uint32_t)(r / 8), (uint32_t)k, t, 0x4D430000u };
                     or_philox4x32_10(ctr, key, words);
                 }
-                sum += tab[words[r % 4] >> shift];
+                uint32_t w = words[(r / 2) % 4];
+                uint32_t u16 = (r % 2 == 0) ? (w & 0xFFFFu) : (w >> 16);
+                sum += tab[u16 >> shift];
             }
             X[tt * p->G + k] = sum;
         }

@@ -517,6 +517,8 @@ int qlm_mc_sample(qlm_ctx *ctx, uint64_t mc_seed, int64_t trial_first, int64_t t
     if (trial_first < 0 || trial_count < 0 || trial_first + trial_count > (int64_t)1 << 32)
         return fail(QLM_ERANGE, "trials [%lld, +%lld) must lie in [0, 2^32)", (long long)trial_first,
                     (long long)trial_count);
+    if ((uint64_t)trial_count * (uint64_t)ctx->dm.G >= ((uint64_t)1 << 32))
+        return fail(QLM_ERANGE, "trial_count * G = %lld must be < 2^32", (long long)(trial_count * ctx->dm.G));
     ctx->mc_trials = trial_count;
     if (trial_count == 0) return QLM_OK;
     const size_t needX = (size_t)trial_count * ctx->dm.G * ctx->dm.D * sizeof(double);

@@ -444,41 +444,49 @@ __global__ void __launch_bounds__(32) row_warp_kernel(const ScanParams p, uint16
 __global__ void __launch_bounds__(256) mc_sample_kernel(Dims dm, Tables tb, uint64_t seed,
                                                         int64_t t0, int64_t nt, double *Y,
                                                         int tabs_in_smem) {
-    (void)tabs_in_smem;
-    const uint16_t *__restrict__ len = tb.len;       // read through L1 (tables <= a few 100 KB)
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint16_t *len = tb.len;
+    if (tabs_in_smem) {
+        uint4 *s4 = reinterpret_cast<uint4 *>(smem);
+        const uint4 *g4 = reinterpret_cast<const uint4 *>(tb.len);
+        const int n4 = dm.n_tables * dm.K * 2 / 16;
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) s4[i] = g4[i];
+        __syncthreads();
+        len = reinterpret_cast<const uint16_t *>(smem);
+    }
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    const int64_t total = (int64_t)dm.G * nt;
-    const int shift = dm.shift, lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t task = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < total;
-         task += nwarps) {
-        const int k = (int)(task / nt);
-        const int64_t tl = task - (int64_t)k * nt;
-        const uint32_t t = (uint32_t)(t0 + tl);
+    const uint32_t ntu = (uint32_t)nt;                   // trials < 2^32 (validated)
+    const uint32_t total = (uint32_t)dm.G * ntu;         // G * trials < 2^32 (validated)
+    const int shift = dm.shift - 16;                     // 16-bit draws: u16 >> (16 - log2 K)
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < total; task += nwarps) {
+        const uint32_t k = task / ntu;
+        const uint32_t tl = task - k * ntu;
+        const uint32_t t = (uint32_t)t0 + tl;
         const int n = tb.grec[k].n;
-        const uint16_t *tab = len + (int64_t)tb.dist[k] * dm.K;
+        const uint16_t *tab = len + (uint32_t)tb.dist[k] * (uint32_t)dm.K;
         uint32_t sum = 0;
-        for (int b = lane; 4 * b < n; b += 64) {         // two independent Philox chains
-            const int b2 = b + 32;
-            const uint4 w1 = philox10(make_uint4((uint32_t)b, (uint32_t)k, t, kMcTag), key);
-            uint4 w2 = make_uint4(0u, 0u, 0u, 0u);
-            if (4 * b2 < n) w2 = philox10(make_uint4((uint32_t)b2, (uint32_t)k, t, kMcTag), key);
-            const int r1 = 4 * b, r2 = 4 * b2;
-            sum += __ldg(&tab[w1.x >> shift]);
-            if (r1 + 1 < n) sum += __ldg(&tab[w1.y >> shift]);
-            if (r1 + 2 < n) sum += __ldg(&tab[w1.z >> shift]);
-            if (r1 + 3 < n) sum += __ldg(&tab[w1.w >> shift]);
-            if (r2 < n) sum += __ldg(&tab[w2.x >> shift]);
-            if (r2 + 1 < n) sum += __ldg(&tab[w2.y >> shift]);
-            if (r2 + 2 < n) sum += __ldg(&tab[w2.z >> shift]);
-            if (r2 + 3 < n) sum += __ldg(&tab[w2.w >> shift]);
-        }
+        // lane l draws Philox blocks b = l, l + 32, ...: requests 8b .. 8b+7
+        for (int b = lane; 8 * b < n; b += 32) {
+            const uint4 wd = philox10(make_uint4((uint32_t)b, k, t, kMcTag), key);
+            const int r0 = 8 * b;
+            const uint32_t w[4] = {wd.x, wd.y, wd.z, wd.w};
+            if (r0 + 8 <= n) {
 #pragma unroll
-        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+                for (int h = 0; h < 4; ++h)
+                    sum += (uint32_t)tab[(w[h] & 0xFFFFu) >> shift] + (uint32_t)tab[(w[h] >> 16) >> shift];
+            } else {
+#pragma unroll
+                for (int h = 0; h < 8; ++h)
+                    if (r0 + h < n) sum += tab[((h & 1) ? (w[h >> 1] >> 16) : (w[h >> 1] & 0xFFFFu)) >> shift];
+            }
+        }
+        sum = __reduce_add_sync(0xFFFFFFFFu, sum);
         // y[d][k][t] = X / Theta[d][m_k]: Eq. 2 with the realised token count, per device row
         const int m = tb.grec[k].model;
         for (int d = lane; d < dm.D; d += 32)
-            Y[((int64_t)d * dm.G + k) * nt + tl] = __ddiv_rn((double)sum, tb.theta[d * dm.M + m]);
+            Y[((size_t)d * dm.G + k) * ntu + tl] = __ddiv_rn((double)sum, tb.theta[d * dm.M + m]);
     }
 }
 
@@ -796,8 +804,9 @@ cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
 
 cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, int64_t t0,
                              int64_t nt, double *X, cudaStream_t st) {
-    const int in_smem = 0;
-    const size_t smem = 0;
+    const size_t tab_bytes = (size_t)dm.n_tables * dm.K * 2;
+    const int in_smem = tab_bytes <= 100 * 1024 && (tab_bytes % 16) == 0;
+    const size_t smem = in_smem ? tab_bytes : 0;
     cudaError_t e = prep(mc_sample_kernel, smem);
     if (e != cudaSuccess) return e;
     const int nb = occupancy(mc_sample_kernel, 256, smem);
