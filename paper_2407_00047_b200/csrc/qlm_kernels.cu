@@ -374,23 +374,39 @@ __global__ void check_rows_kernel(const Cand cd, int T, unsigned long long *n_ba
 // MC).  RANDOM: the lanes compute the row's Philox blocks in parallel, then
 // lane 0 runs the Fisher-Yates swaps from shared memory (same permutation as
 // fy_materialise).  Returns with srow[0..T) valid for all lanes.
+// Materialise one candidate row into srow[0..T) with a warp (R9/R10).  For
+// RANDOM, the lanes first compute every swap target j_i = i + mulhi(u_i, T-i)
+// in parallel (they depend only on the Philox words, not on the row), then
+// lane 0 runs the forward Fisher-Yates swaps with one shared-memory round trip
+// per step: the value at position i+1 is loaded together with row[j_i] (the
+// only store of step i that can touch position i+1 is row[j_i] = row[i]).
 __device__ __forceinline__ void warp_gen_row(const Cand &cd, int T, uint64_t c, int64_t loc,
-                                             uint16_t *srow, uint4 *swords) {
+                                             uint16_t *srow, uint16_t *sJ) {
     const int lane = threadIdx.x & 31;
     if (cd.kind == QLM_CAND_RANDOM) {
         const int nb = (T - 1 + 3) / 4;
         const uint2 key = make_uint2((uint32_t)cd.seed, (uint32_t)(cd.seed >> 32));
-        for (int b = lane; b < nb; b += 32)
-            swords[b] = philox10(make_uint4((uint32_t)b, (uint32_t)c, (uint32_t)(c >> 32), kRowTag), key);
+        for (int b = lane; b < nb; b += 32) {
+            const uint4 wd = philox10(make_uint4((uint32_t)b, (uint32_t)c, (uint32_t)(c >> 32), kRowTag), key);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int i = 4 * b + h;
+                if (i + 1 < T) sJ[i] = (uint16_t)(i + (int)__umulhi(pick4(wd, h), (uint32_t)(T - i)));
+            }
+        }
         for (int s = lane; s < T; s += 32) srow[s] = (uint16_t)s;
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && T > 1) {
+            uint32_t ti = srow[0];
+            int j = sJ[0];
             for (int i = 0; i + 1 < T; ++i) {
-                const uint32_t u = pick4(swords[i >> 2], i & 3);
-                const int j = i + (int)__umulhi(u, (uint32_t)(T - i));
-                const uint16_t ti = srow[i], tj = srow[j];
-                srow[j] = ti;
-                srow[i] = tj;
+                const int jn = i + 2 < T ? sJ[i + 1] : 0;
+                const uint32_t tj = srow[j];
+                const uint32_t nx = srow[i + 1];
+                srow[j] = (uint16_t)ti;
+                srow[i] = (uint16_t)tj;
+                ti = (j == i + 1) ? ti : nx;
+                j = jn;
             }
         }
     } else if (cd.kind == QLM_CAND_ENUM) {
@@ -406,6 +422,31 @@ __device__ __forceinline__ void warp_gen_row(const Cand &cd, int T, uint64_t c, 
     __syncwarp();
 }
 
+// Walk a materialised row in 32-token chunks with warp ballots: for each
+// group token, its queue q (separators before it, capped at Q-1, R9), its
+// position within the queue and its slot index (groups before it).
+template <typename F>
+__device__ __forceinline__ void warp_slots(const uint16_t *srow, int T, int G, int Q, F &&f) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    int nsep = 0, lastsep = -1;
+    for (int s0 = 0; s0 < T; s0 += 32) {
+        const int s = s0 + lane;
+        const int tok = s < T ? srow[s] : 0;
+        const bool sep = s < T && tok >= G;
+        const uint32_t bs = __ballot_sync(0xFFFFFFFFu, sep);
+        const uint32_t below = bs & lt;
+        const int before = nsep + __popc(below);
+        const int ls = below ? s0 + 31 - __clz(below) : lastsep;
+        if (s < T && !sep) {
+            const int q = before < Q - 1 ? before : Q - 1;
+            f(tok, q, s - ls - 1, s - before);
+        }
+        nsep += __popc(bs);
+        if (bs) lastsep = s0 + 31 - __clz(bs);
+    }
+}
+
 // Rows / decode with one warp per candidate (small counts).
 __global__ void __launch_bounds__(32) row_warp_kernel(const ScanParams p, uint16_t *rows_out,
                                                       int32_t *queue_of, int32_t *pos_of) {
@@ -417,85 +458,124 @@ __global__ void __launch_bounds__(32) row_warp_kernel(const ScanParams p, uint16
     }
     const int64_t loc = blockIdx.x;
     const int T = p.dm.T, G = p.dm.G, Q = p.dm.Q;
-    uint4 *swords = reinterpret_cast<uint4 *>(smem);
-    uint16_t *srow = reinterpret_cast<uint16_t *>(smem + (size_t)((T + 2) / 4 + 1) * 16);
-    warp_gen_row(p.cd, T, (uint64_t)(first + loc), loc, srow, swords);
+    uint16_t *srow = reinterpret_cast<uint16_t *>(smem);
+    uint16_t *sJ = srow + ((T + 7) & ~7);
+    warp_gen_row(p.cd, T, (uint64_t)(first + loc), loc, srow, sJ);
     const int lane = threadIdx.x;
     if (rows_out)
         for (int s = lane; s < T; s += 32) rows_out[loc * T + s] = srow[s];
-    if ((queue_of || pos_of) && lane == 0) {
-        int q = 0, pos = 0;
-        for (int s = 0; s < T; ++s) {
-            const int tok = srow[s];
-            if (tok >= G) { q = q + 1 < Q ? q + 1 : Q - 1; pos = 0; continue; }
+    if (queue_of || pos_of)
+        warp_slots(srow, T, G, Q, [&](int tok, int q, int pos, int) {
             if (queue_of) queue_of[loc * G + tok] = q;
             if (pos_of) pos_of[loc * G + tok] = pos;
-            ++pos;
-        }
-    }
+        });
 }
 
 // =============================================================================
 // a10-a11: Monte-Carlo
 // =============================================================================
-// X[k][t] = sum_{r < n_k} len[dist_k][word(t, k, r) >> shift]   (R13).
-// One warp per (group, trial): lane l draws Philox blocks b = l, l+32, ...
-// (requests 4b..4b+3) and the warp sums them (exact integers, any order).
+// X[k][t] = sum_{r < n_k} len[dist_k][u16(t, k, r) >> (16 - log2 K)]   (R13).
+// One block per item (group k, 32 consecutive trials), persistent over items:
+// lane = trial, so every lane walks the same n_k requests; the 8 warps split
+// the request blocks (warp w takes Philox blocks b = w, w+8, ...; block b holds
+// requests 8b..8b+7, two 16-bit halves per word) and reduce through shared
+// memory, so a 1000-request group costs the block ~16 blocks per warp instead
+// of one warp 127. Tables are staged in shared memory once per block when they
+// fit; a lookup is SHF/LOP3 + LEA + LDS. Sums are exact integers, order-free.
+template <bool SMEM>
+__device__ __forceinline__ uint32_t mc_lookup(const uint16_t *tab, uint32_t tab_s, uint32_t idx) {
+    if constexpr (SMEM) {
+        uint16_t v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(tab_s + (idx << 1)));
+        return v;
+    } else {
+        return __ldg(tab + idx);
+    }
+}
+
+template <bool SMEM>
+__device__ __forceinline__ uint32_t mc_block8(const uint16_t *tab, uint32_t tab_s, uint4 wd,
+                                              int s, uint32_t km) {
+    const uint32_t w[4] = {wd.x, wd.y, wd.z, wd.w};
+    uint32_t a = 0;
+#pragma unroll
+    for (int h = 0; h < 4; ++h)       // (w >> s) & (K-1) == (w & 0xFFFF) >> s since s + log2 K = 16
+        a += mc_lookup<SMEM>(tab, tab_s, (w[h] >> s) & km) + mc_lookup<SMEM>(tab, tab_s, w[h] >> (16 + s));
+    return a;
+}
+
+template <bool SMEM>
 __global__ void __launch_bounds__(256) mc_sample_kernel(Dims dm, Tables tb, uint64_t seed,
-                                                        int64_t t0, int64_t nt, double *Y,
-                                                        int tabs_in_smem) {
+                                                        int64_t t0, int64_t nt, double *Y) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const uint16_t *len = tb.len;
-    if (tabs_in_smem) {
+    if constexpr (SMEM) {
         uint4 *s4 = reinterpret_cast<uint4 *>(smem);
         const uint4 *g4 = reinterpret_cast<const uint4 *>(tb.len);
         const int n4 = dm.n_tables * dm.K * 2 / 16;
         for (int i = threadIdx.x; i < n4; i += blockDim.x) s4[i] = g4[i];
         __syncthreads();
-        len = reinterpret_cast<const uint16_t *>(smem);
     }
+    __shared__ uint32_t red[8][32];
+    const uint32_t smem_s = (uint32_t)__cvta_generic_to_shared(smem);
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     const uint32_t ntu = (uint32_t)nt;                   // trials < 2^32 (validated)
-    const uint32_t total = (uint32_t)dm.G * ntu;         // G * trials < 2^32 (validated)
-    const int shift = dm.shift - 16;                     // 16-bit draws: u16 >> (16 - log2 K)
-    const int lane = threadIdx.x & 31;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; task < total; task += nwarps) {
-        const uint32_t k = task / ntu;
-        const uint32_t tl = task - k * ntu;
+    const uint32_t ntw = (ntu + 31) >> 5;                // items per group
+    const uint32_t total = (uint32_t)dm.G * ntw;
+    const int s = dm.shift - 16;                         // 16 - log2 K
+    const uint32_t km = (uint32_t)dm.K - 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
+        const uint32_t k = item / ntw;
+        const uint32_t tl = (item - k * ntw) * 32 + lane;
         const uint32_t t = (uint32_t)t0 + tl;
         const int n = tb.grec[k].n;
-        const uint16_t *tab = len + (uint32_t)tb.dist[k] * (uint32_t)dm.K;
-        uint32_t sum = 0;
-        // lane l draws Philox blocks b = l, l + 32, ...: requests 8b .. 8b+7
-        for (int b = lane; 8 * b < n; b += 32) {
-            const uint4 wd = philox10(make_uint4((uint32_t)b, k, t, kMcTag), key);
-            const int r0 = 8 * b;
-            const uint32_t w[4] = {wd.x, wd.y, wd.z, wd.w};
-            if (r0 + 8 <= n) {
-#pragma unroll
-                for (int h = 0; h < 4; ++h)
-                    sum += (uint32_t)tab[(w[h] & 0xFFFFu) >> shift] + (uint32_t)tab[(w[h] >> 16) >> shift];
-            } else {
-#pragma unroll
-                for (int h = 0; h < 8; ++h)
-                    if (r0 + h < n) sum += tab[((h & 1) ? (w[h >> 1] >> 16) : (w[h >> 1] & 0xFFFFu)) >> shift];
-            }
+        const uint32_t toff = (uint32_t)tb.dist[k] * (uint32_t)dm.K;
+        const uint16_t *tab = tb.len + toff;
+        const uint32_t tab_s = smem_s + 2 * toff;
+        const uint32_t nfull = (uint32_t)n >> 3;
+        uint32_t sum = 0, sum2 = 0;
+        uint32_t b = warp;
+        for (; b + 8 < nfull; b += 16) {                 // two independent Philox chains
+            const uint4 w0 = philox10(make_uint4(b, k, t, kMcTag), key);
+            const uint4 w1 = philox10(make_uint4(b + 8, k, t, kMcTag), key);
+            sum += mc_block8<SMEM>(tab, tab_s, w0, s, km);
+            sum2 += mc_block8<SMEM>(tab, tab_s, w1, s, km);
         }
-        sum = __reduce_add_sync(0xFFFFFFFFu, sum);
+        if (b < nfull) {
+            sum += mc_block8<SMEM>(tab, tab_s, philox10(make_uint4(b, k, t, kMcTag), key), s, km);
+            b += 8;
+        }
+        const int rem = n & 7;                            // the partial last block (uniform)
+        if (rem && b == nfull) {
+            const uint4 wd = philox10(make_uint4(b, k, t, kMcTag), key);
+            const uint32_t w[4] = {wd.x, wd.y, wd.z, wd.w};
+#pragma unroll
+            for (int h = 0; h < 7; ++h)
+                if (h < rem) sum2 += mc_lookup<SMEM>(tab, tab_s, (h & 1) ? (w[h >> 1] >> (16 + s)) : ((w[h >> 1] >> s) & km));
+        }
+        red[warp][lane] = sum + sum2;
+        __syncthreads();
         // y[d][k][t] = X / Theta[d][m_k]: Eq. 2 with the realised token count, per device row
-        const int m = tb.grec[k].model;
-        for (int d = lane; d < dm.D; d += 32)
-            Y[((size_t)d * dm.G + k) * ntu + tl] = __ddiv_rn((double)sum, tb.theta[d * dm.M + m]);
+        if (warp == 0 && tl < ntu) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) x += red[w][lane];
+            const int m = tb.grec[k].model;
+            for (int d = 0; d < dm.D; ++d)
+                Y[((size_t)d * dm.G + k) * ntu + tl] = __ddiv_rn((double)x, tb.theta[d * dm.M + m]);
+        }
+        __syncthreads();
     }
 }
 
 // One warp per (candidate, 32 trials); every lane is one trial.  The warp
-// materialises the candidate's row and its in-order list of group slots
-// (token, queue) in shared memory.  Phase 1 computes each group's realised
-// work X/Theta (independent across slots: loads and divisions overlap);
-// phase 2 walks the Eq. 10 chain in the oracle's operation order and counts
-// violations with warp ballots.
+// materialises the candidate's row, then precomputes per group slot (in row
+// order, all trial-independent): the deterministic addends of the Eq. 10 walk
+// at a model change (tail, R3/R4/R12; swap, R2), the SLO, the start value of
+// the queue (backlog mean) and the row of Y to read.  The walk itself is then
+// A = start?; A += tail; A += swap; count A > slo; A += y  -- branch-free, in
+// the oracle's operation order (+0.0 where no model change: A >= 0, so
+// A + 0.0 == A bit for bit).  y is prefetched 16 slots ahead.
 __global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand cd,
                                                       const double *Y, int64_t nt,
                                                       uint32_t *counts) {
@@ -506,67 +586,72 @@ __global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand c
         if (first < 0) return;
     }
     const int T = dm.T, G = dm.G, M = dm.M;
-    uint16_t *stok = reinterpret_cast<uint16_t *>(smem);                             // [G]
-    uint16_t *sq = stok + G;                                                         // [G]
-    uint4 *swords = reinterpret_cast<uint4 *>(smem + (((size_t)4 * G + 15) & ~15));
-    uint16_t *srow = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(swords) +
-                                                  (size_t)((T + 2) / 4 + 1) * 16);
+    double *st = reinterpret_cast<double *>(smem);     // [G] tail addend
+    double *ss = st + G;                                // [G] swap addend
+    double *sslo = ss + G;                              // [G] SLO
+    double *sa0 = sslo + G;                             // [G] queue start (backlog mean) or -1
+    int32_t *yrow = reinterpret_cast<int32_t *>(sa0 + G);   // [G] d * G + token
+    uint16_t *stok = reinterpret_cast<uint16_t *>(yrow + G);  // [G]
+    uint16_t *sq = stok + G;                            // [G]
+    uint16_t *srow = sq + G;                            // [T]
+    uint16_t *sJ = srow + ((T + 7) & ~7);               // [T]
     const int64_t loc = blockIdx.y;
     const int lane = threadIdx.x;
-    warp_gen_row(cd, T, (uint64_t)(first + loc), loc, srow, swords);
-    if (lane == 0) {
-        int q = 0, i = 0;
-        for (int s = 0; s < T; ++s) {
-            const int tok = srow[s];
-            if (tok >= G) { q = q + 1 < dm.Q ? q + 1 : dm.Q - 1; continue; }
-            stok[i] = (uint16_t)tok;
-            sq[i] = (uint16_t)q;
-            ++i;
+    warp_gen_row(cd, T, (uint64_t)(first + loc), loc, srow, sJ);
+    warp_slots(srow, T, G, dm.Q, [&](int tok, int q, int, int i) {
+        stok[i] = (uint16_t)tok;
+        sq[i] = (uint16_t)q;
+    });
+    __syncwarp();
+    for (int i = lane; i < G; i += 32) {
+        const int tok = stok[i], q = sq[i];
+        const QRec qr = tb.qrec[q];
+        const GRec g = tb.grec[tok];
+        const bool firsts = i == 0 || sq[i - 1] != q;
+        const int prev = firsts ? qr.r : tb.grec[stok[i - 1]].model;
+        const int d = qr.d, m = g.model;
+        double t = 0.0, w = 0.0;
+        if (m != prev) {
+            t = (firsts && !qr.backlog) ? 0.0 : tb.tail[d * M + prev];
+            w = tb.swap[(d * M + prev) * M + m];
         }
+        st[i] = t;
+        ss[i] = w;
+        sslo[i] = g.slo;
+        sa0[i] = firsts ? qr.bmean : -1.0;
+        yrow[i] = d * G + tok;
     }
     __syncwarp();
     const int64_t tl = (int64_t)blockIdx.x * 32 + lane;
     const bool act = tl < nt;
-    // Walk the group slots in row order.  y_i = (X / Theta)[d_i][g_i][t] (Eq. 2
-    // with the realised token count) is loaded 8 slots ahead into registers, so
-    // the global loads overlap the sequential chain for any G.
-    auto load8 = [&](int i0, double *y) {
+    constexpr int PF = 16;
+    auto load = [&](int i0, double *y) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < PF; ++k) {
             const int i = i0 + k < G ? i0 + k : G - 1;
-            const int64_t row = (int64_t)tb.qrec[sq[i]].d * G + stok[i];
-            y[k] = act ? __ldg(&Y[row * nt + tl]) : 0.0;
+            y[k] = act ? __ldg(&Y[(int64_t)yrow[i] * nt + tl]) : 0.0;
         }
     };
-    double cur[8], nxt[8];
-    load8(0, cur);
-    int q = -1, d = 0, prev = 0, firstslot = 1, backlog = 0;
+    double cur[PF], nxt[PF];
+    load(0, cur);
     double A = 0.0;
-    for (int i0 = 0; i0 < G; i0 += 8) {
-        if (i0 + 8 < G) load8(i0 + 8, nxt);
+    uint32_t *cnt = counts + loc * G;
+    for (int i0 = 0; i0 < G; i0 += PF) {
+        if (i0 + PF < G) load(i0 + PF, nxt);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < PF; ++k) {
             const int i = i0 + k;
             if (i >= G) break;
-            const int tok = stok[i], qi = sq[i];
-            if (qi != q) {                               // first group of queue qi
-                const QRec qr = tb.qrec[qi];
-                q = qi; A = qr.bmean; d = qr.d; prev = qr.r; firstslot = 1; backlog = qr.backlog;
-            }
-            const GRec g = tb.grec[tok];
-            const int m = g.model;
-            if (m != prev) {
-                const double t = (firstslot && !backlog) ? 0.0 : tb.tail[d * M + prev];
-                A = __dadd_rn(A, t);
-                A = __dadd_rn(A, tb.swap[(d * M + prev) * M + m]);
-            }
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, act && A > g.slo);
-            if (lane == 0 && bal) atomicAdd(&counts[loc * G + tok], (unsigned)__popc(bal));
+            const double a0 = sa0[i];
+            A = a0 >= 0.0 ? a0 : A;
+            A = __dadd_rn(A, st[i]);
+            A = __dadd_rn(A, ss[i]);
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, act && A > sslo[i]);
+            if (lane == 0 && bal) atomicAdd(&cnt[stok[i]], (unsigned)__popc(bal));
             A = __dadd_rn(A, cur[k]);
-            prev = m; firstslot = 0;
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) cur[k] = nxt[k];
+        for (int k = 0; k < PF; ++k) cur[k] = nxt[k];
     }
 }
 
@@ -759,7 +844,7 @@ static cudaError_t launch_rows_t(ScanParams p, uint16_t *rows, int32_t *qo, int3
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,
                         cudaStream_t st) {
     if (p.cd.count <= 1024) {
-        const size_t smem = (size_t)((p.dm.T + 2) / 4 + 1) * 16 + align16((size_t)p.dm.T * 2 + 4);
+        const size_t smem = (size_t)4 * ((p.dm.T + 7) & ~7);
         cudaError_t e = prep(row_warp_kernel, smem);
         if (e != cudaSuccess) return e;
         row_warp_kernel<<<(unsigned)p.cd.count, 32, smem, st>>>(p, rows, qo, po);
@@ -805,25 +890,25 @@ cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
 cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, int64_t t0,
                              int64_t nt, double *X, cudaStream_t st) {
     const size_t tab_bytes = (size_t)dm.n_tables * dm.K * 2;
-    const int in_smem = tab_bytes <= 100 * 1024 && (tab_bytes % 16) == 0;
+    const bool in_smem = tab_bytes <= 100 * 1024 && (tab_bytes % 16) == 0;
     const size_t smem = in_smem ? tab_bytes : 0;
-    cudaError_t e = prep(mc_sample_kernel, smem);
+    auto kern = in_smem ? mc_sample_kernel<true> : mc_sample_kernel<false>;
+    cudaError_t e = prep(kern, smem);
     if (e != cudaSuccess) return e;
-    const int nb = occupancy(mc_sample_kernel, 256, smem);
-    const int64_t tasks = (int64_t)dm.G * nt;                 // one warp each
-    int64_t grid = (tasks + 7) / 8;
+    const int nb = occupancy(kern, 256, smem);
+    const int64_t items = (int64_t)dm.G * ((nt + 31) / 32);   // one block each
+    int64_t grid = items;
     const int64_t maxg = (int64_t)sm_count() * (nb > 0 ? nb : 1);
     if (grid > maxg) grid = maxg;
     if (grid < 1) grid = 1;
-    mc_sample_kernel<<<(unsigned)grid, 256, smem, st>>>(dm, tb, seed, t0, nt, X, in_smem);
+    kern<<<(unsigned)grid, 256, smem, st>>>(dm, tb, seed, t0, nt, X);
     ++g_launches;
     return cudaGetLastError();
 }
 
 cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const Cand &cd, const double *X,
                             int64_t nt, uint32_t *counts, cudaStream_t st) {
-    const size_t smem = align16((size_t)4 * dm.G) +
-                        (size_t)((dm.T + 2) / 4 + 1) * 16 + align16((size_t)dm.T * 2 + 4);
+    const size_t smem = (size_t)40 * dm.G + (size_t)4 * ((dm.T + 7) & ~7);
     cudaError_t e = prep(mc_count_kernel, smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((nt + 31) / 32), (unsigned)cd.count);

@@ -64,14 +64,11 @@ __device__ __forceinline__ bool mbar_try(uint64_t *b, unsigned parity) {
         : "memory");
     return ok != 0;
 }
-// Wait for a phase; back off with nanosleep so waiting warps (usually the
-// producers) do not steal issue slots from the warps doing the work.
+// Wait for a phase.
 __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
-    if (mbar_try(b, parity)) return;
-    unsigned ns = 32;
+    // try_wait suspends the warp in hardware until the phase completes (or a
+    // time limit passes), so the loop issues a handful of instructions per wait
     while (!mbar_try(b, parity)) {
-        __nanosleep(ns);
-        ns = ns < 512 ? ns * 2 : 512;
     }
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, const void *src, int x, int y) {
@@ -242,7 +239,7 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
                 a.over += (grp && v > alpha) ? 1 : 0;
             }
         }
-        if (st) {
+        {
             float *o = st + tg[k] * 32 + lane;               // separators -> trash row G
             o[0] = (float)wt[k];
             o[arr_stride] = Vf * rr;
