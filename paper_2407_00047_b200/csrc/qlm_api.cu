@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -55,6 +56,9 @@ struct qlm_ctx {
     int32_t *d_dec_out = nullptr;          // [2][G] sync decode
     unsigned long long *d_bad = nullptr;
     int max_blocks = 0;
+    uint32_t *d_ilv = nullptr;         // large-T RANDOM: interleaved row chunk
+    int64_t ilv_cap = 0;               // candidates per chunk
+    qlm_record *d_chunk_recs = nullptr;
     double *d_X = nullptr;             // MC: (X / Theta)[D][G][trials]
     int64_t mc_trials = -1;            // trials of the last qlm_mc_sample
     size_t X_cap = 0;
@@ -159,6 +163,40 @@ ScanParams base_params(const qlm_ctx *ctx, const qlm_candidates *c) {
     p.zc2 = ctx->zc2;
     p.alpha = ctx->alpha;
     return p;
+}
+
+// Large-T RANDOM scoring runs in chunks through an interleaved row scratch
+// (launch_two_phase); allocated on first use, at most 1 GB (enough candidates
+// per chunk to fill every SM with scan warps).
+void attach_ilv(qlm_ctx *ctx, ScanParams &p) {
+    if (p.cd.kind != QLM_CAND_RANDOM || ctx->dm.T <= 256 || p.cd.first_from || p.cd.count < 4096)
+        return;
+    const char *off = getenv("QLM_NO_TWO_PHASE");       // tests: force the fused fallback
+    if (off && *off && *off != '0') return;
+    if (!ctx->d_ilv) {
+        const size_t row_bytes = (size_t)((ctx->dm.T + 1) / 2) * 4;
+        int64_t cap = (int64_t)(((size_t)1 << 30) / row_bytes);
+        cap = cap > 262144 ? 262144 : cap;
+        const char *ec = getenv("QLM_ILV_CAP");           // tests: small chunks
+        if (ec && *ec && atoll(ec) > 0 && atoll(ec) < cap) cap = atoll(ec);
+        cap &= ~int64_t(31);
+        if (cap < 32) return;
+        if (cudaMalloc(&ctx->d_ilv, (size_t)cap * row_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            ctx->d_ilv = nullptr;
+            return;
+        }
+        if (cudaMalloc(&ctx->d_chunk_recs, 2 * sizeof(qlm_record)) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(ctx->d_ilv);
+            ctx->d_ilv = nullptr;
+            return;
+        }
+        ctx->ilv_cap = cap;
+    }
+    p.ilv = ctx->d_ilv;
+    p.ilv_cap = ctx->ilv_cap;
+    p.chunk_recs = ctx->d_chunk_recs;
 }
 
 int rebuild(qlm_ctx *ctx, cudaStream_t st) {
@@ -354,7 +392,7 @@ void qlm_destroy(qlm_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     void *ptrs[] = {ctx->d_raw, ctx->d_tab, ctx->d_block_recs, ctx->d_counter, ctx->d_rec,
-                    ctx->d_dec_out, ctx->d_bad, ctx->d_X};
+                    ctx->d_dec_out, ctx->d_bad, ctx->d_X, ctx->d_ilv, ctx->d_chunk_recs};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete ctx;
@@ -381,6 +419,7 @@ int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, flo
     if (cand->count == 0) return QLM_OK;
     ScanParams p = base_params(ctx, cand);
     p.s1 = s1; p.s2 = s2; p.n_over = n_over;
+    attach_ilv(ctx, p);
     cudaError_t e = launch_any_scan(p, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score kernel");
 }
@@ -399,6 +438,7 @@ int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record
     }
     ScanParams p = base_params(ctx, cand);
     p.out_rec = rec;
+    attach_ilv(ctx, p);
     cudaError_t e = launch_any_scan(p, st);
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score/argmin kernel");
 }
@@ -501,6 +541,7 @@ int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
     ScanParams p = base_params(ctx, cand);
     p.wt = wt_mean; p.sd = wt_std; p.vo = viol;
     p.s1 = s1; p.s2 = s2; p.n_over = n_over; p.out_rec = rec;
+    attach_ilv(ctx, p);
     cudaError_t e = launch_any_scan(p, st);
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "scan kernel");
 }

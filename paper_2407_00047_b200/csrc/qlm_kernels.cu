@@ -99,10 +99,27 @@ __device__ __forceinline__ void for_tokens(const Cand &cd, int T, uint8_t *scrat
     if constexpr (KIND == QLM_CAND_RANDOM) {
         fy_materialise<TOK>(scratch, blk, threadIdx.x, T, cd.seed, (uint64_t)c);
         tokens_scratch<TOK>(scratch, blk, threadIdx.x, T, f);
-    } else if constexpr (KIND == QLM_CAND_EXPLICIT)
+    } else if constexpr (KIND == QLM_CAND_EXPLICIT) {
         tokens_explicit<TOK>(cd.rows + loc * cd.stride, T, f);
-    else
+    } else if constexpr (KIND == KIND_ILV) {
+        // word-interleaved rows: consecutive candidates read consecutive words
+        constexpr int EPW = 4 / (int)sizeof(TOK);
+        const uint32_t *w32 = reinterpret_cast<const uint32_t *>(cd.rows) + loc;
+        const int nw = (T + EPW - 1) / EPW;
+        uint32_t nxt = __ldcs(w32);
+        for (int w = 0; w < nw; ++w) {
+            const uint32_t cur = nxt;
+            if (w + 1 < nw) nxt = __ldcs(w32 + (size_t)(w + 1) * cd.stride);   // prefetch
+#pragma unroll
+            for (int k = 0; k < EPW; ++k) {
+                const int s = w * EPW + k;
+                if (s >= T) break;
+                f(EPW == 2 ? (int)((cur >> (16 * k)) & 0xFFFFu) : (int)((cur >> (8 * k)) & 0xFFu));
+            }
+        }
+    } else {
         tokens_enum((uint64_t)c, T, f);
+    }
 }
 
 __device__ __forceinline__ SlotTables stage_tables(const ScanParams &p, uint8_t *smem) {
@@ -153,6 +170,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
     const double zc2 = p.zc2;
     const float alpha = p.alpha;
     const int64_t count = cd.count;
+    const int64_t ldo = p.ld_out ? p.ld_out : count;     // bulk leading dimension
     float *const gout[3] = {p.wt, p.sd, p.vo};
     float *st0 = nullptr, *st1 = nullptr, *st2 = nullptr;   // staged tile [3][G][blk]
     if constexpr (OUT == OUT_STAGED) {
@@ -204,7 +222,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                     st1[o] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
                     st2[o] = v;
                 } else if constexpr (OUT == OUT_DIRECT) {
-                    const int64_t o = (int64_t)tok * count + loc;
+                    const int64_t o = (int64_t)tok * ldo + loc;
                     const float Vf = (float)V;
                     if (gout[0]) gout[0][o] = (float)wt;
                     if (gout[1]) gout[1][o] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                 for (int r = tid; r < 3 * G; r += blk) {
                     const int a = r / G, g = r - a * G;
                     if (gout[a])
-                        bulk_s2g(gout[a] + (int64_t)g * count + c0, sts[a] + (size_t)g * blk,
+                        bulk_s2g(gout[a] + (int64_t)g * ldo + c0, sts[a] + (size_t)g * blk,
                                  (uint32_t)nvalid * 4u);
                 }
                 bulk_commit();
@@ -240,7 +258,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
                     for (int a = 0; a < 3; ++a)
                         if (gout[a])
                             for (int g = 0; g < G; ++g)
-                                gout[a][(int64_t)g * count + loc] = sts[a][g * blk + tid];
+                                gout[a][(int64_t)g * ldo + loc] = sts[a][g * blk + tid];
             }
         }
     }
@@ -316,6 +334,85 @@ __global__ void reduce_records_kernel(const qlm_record *recs, int n, qlm_record 
         warp_argmin(k, i);
         if (lane == 0) { out->key = k; out->index = i; }
     }
+}
+
+// =============================================================================
+// a1 for large T: RANDOM rows materialised word-interleaved (two-phase path)
+// =============================================================================
+// One lane per candidate; the lane's row lives in its column of a [T][32] u16
+// shared-memory tile (address = base + 64 j).  Forward Fisher-Yates (R10),
+// software-pipelined two steps deep: step i issues the loads of position i+2
+// and of row[j_{i+1}] before its own store, and the consumers forward the
+// values of the (at most two) stores issued after a load that may alias it.
+// So the store chain waits on a load issued two steps earlier.  Finals are
+// packed two per word and leave as coalesced 128-B warp stores.
+__global__ void __launch_bounds__(32) fy_rows_kernel(Cand cd, int T, uint32_t *out, int64_t ld) {
+    extern __shared__ __align__(16) uint16_t srow16[];
+    const int lane = threadIdx.x;
+    const int64_t loc = (int64_t)blockIdx.x * 32 + lane;
+    const bool act = loc < cd.count;
+    const uint64_t c = (uint64_t)(cd.first + loc);
+    for (int i = 0; i < T; ++i) srow16[i * 32 + lane] = (uint16_t)i;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(srow16) + 2u * lane;
+    auto ld16 = [&](int i) {
+        uint16_t v;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(base + ((uint32_t)i << 6)) : "memory");
+        return (uint32_t)v;
+    };
+    auto st16 = [&](int i, uint32_t v) {
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(base + ((uint32_t)i << 6)), "h"((uint16_t)v) : "memory");
+    };
+    const uint2 key = make_uint2((uint32_t)cd.seed, (uint32_t)(cd.seed >> 32));
+    const uint32_t clo = (uint32_t)c, chi = (uint32_t)(c >> 32);
+    uint32_t *o = out + loc;
+    auto jof = [&](uint4 wd, int k, int i) { return i + (int)__umulhi(pick4(wd, k), (uint32_t)(T - i)); };
+    if (T == 1) {
+        if (act) __stcs(o, 0u);
+        return;
+    }
+    // pipeline state: t0 = value at position i, t1m = value step i-1 stored,
+    // jm = j_{i-1}; raw1 = mem[i+1] loaded before store i-1 (pending forwards
+    // from steps i-1 and i); rj = mem[j_i] loaded before store i-1 (forward
+    // from step i-1)
+    uint4 wd = philox10(make_uint4(0u, clo, chi, kRowTag), key);
+    int j = jof(wd, 0, 0);
+    uint32_t t0 = 0, t1m = 0xFFFFFFFFu;
+    int jm = -1;
+    uint32_t raw1 = ld16(1), rj = ld16(j);
+    uint32_t fin = 0;
+    uint32_t *op = o;                                  // word (i >> 1) of this lane's row
+    for (int i0 = 0; i0 < T - 1; i0 += 4) {
+        // the next Philox block is independent of this one's steps: issue it first
+        const uint4 wn = i0 + 4 < T - 1 ? philox10(make_uint4((uint32_t)((i0 >> 2) + 1), clo, chi, kRowTag), key)
+                                        : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k;
+            if (i >= T - 1) break;
+            const int jn = i + 1 < T - 1 ? (k < 3 ? jof(wd, k + 1, i + 1) : jof(wn, 0, i + 1)) : 0;
+            // loads for the next steps, issued before this step's store
+            const uint32_t raw2 = i + 2 < T ? ld16(i + 2) : 0u;   // mem[i+2]: misses stores i, i+1
+            const uint32_t rjn = ld16(jn);                         // mem[j_{i+1}]: misses store i
+            const uint32_t tj = (jm == j) ? t1m : rj;              // value at j_i before step i
+            st16(j, t0);                                           // row[j_i] = row[i]
+            if (k & 1) {
+                fin |= tj << 16;
+                if (act) __stcs(op, fin);
+                op += ld;
+            } else {
+                fin = tj;
+            }
+            // value at position i+1 before step i+1 (raw1 misses stores i-1 and i)
+            const uint32_t t1 = (j == i + 1) ? t0 : ((jm == i + 1) ? t1m : raw1);
+            t1m = t0; jm = j;
+            t0 = t1; j = jn;
+            raw1 = raw2; rj = rjn;
+        }
+        wd = wn;
+    }
+    if ((T - 1) & 1) fin |= t0 << 16;             // position T-1 holds the carried value
+    else fin = t0;
+    if (act) __stcs(op, fin);
 }
 
 // =============================================================================
@@ -783,7 +880,7 @@ static cudaError_t launch_scan_k(ScanParams &p, cudaStream_t st) {
     // staged (group-major smem tile + bulk copies) when one fits, else direct stores
     const size_t stage_bytes = (size_t)3 * 32 * p.dm.G * 4;
     const bool fits = stage_bytes + 64 * 1024 <= kMaxSmem;
-    p.use_tma = (p.cd.count % 4 == 0) && (!p.wt || ((uintptr_t)p.wt & 15) == 0) &&
+    p.use_tma = ((p.ld_out ? p.ld_out : p.cd.count) % 4 == 0) && (!p.wt || ((uintptr_t)p.wt & 15) == 0) &&
                 (!p.sd || ((uintptr_t)p.sd & 15) == 0) && (!p.vo || ((uintptr_t)p.vo & 15) == 0);
     if (fits) {
         cudaError_t e = score ? launch_scan_t<KIND, TOK, OUT_STAGED, true>(p, st)
@@ -795,10 +892,60 @@ static cudaError_t launch_scan_k(ScanParams &p, cudaStream_t st) {
                  : launch_scan_t<KIND, TOK, OUT_DIRECT, false>(p, st);
 }
 
+// Large-T RANDOM (T > 256, outside the warp-specialised kernel's range): the
+// per-thread Fisher-Yates scratch (2T bytes) would cap the fused scan at a few
+// warps per SM, so rows are generated per chunk into an interleaved scratch by
+// fy_rows_kernel (cheap, latency-bound) and scored by the scan kernel reading
+// them with coalesced loads at full occupancy.  Argmin is carried across
+// chunks in chunk_recs[0].
+static cudaError_t launch_two_phase(const ScanParams &p0, cudaStream_t st) {
+    const int64_t count = p0.cd.count, cap = p0.ilv_cap;
+    const size_t fy_smem = (size_t)p0.dm.T * 32 * 2;
+    cudaError_t e = prep(fy_rows_kernel, fy_smem);
+    if (e != cudaSuccess) return e;
+    for (int64_t c0 = 0; c0 < count; c0 += cap) {
+        const int64_t n = count - c0 < cap ? count - c0 : cap;
+        Cand g = p0.cd;
+        g.first = p0.cd.first + c0;
+        g.count = n;
+        fy_rows_kernel<<<(unsigned)((n + 31) / 32), 32, fy_smem, st>>>(g, p0.dm.T, p0.ilv, n);
+        ++g_launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ScanParams p = p0;
+        p.cd.kind = KIND_ILV;
+        p.cd.tb = 2;
+        p.cd.rows = reinterpret_cast<const uint8_t *>(p0.ilv);
+        p.cd.stride = n;
+        p.cd.first = g.first;
+        p.cd.count = n;
+        p.ld_out = count;
+        if (p.s1) p.s1 += c0;
+        if (p.s2) p.s2 += c0;
+        if (p.n_over) p.n_over += c0;
+        if (p.wt) p.wt += c0;
+        if (p.sd) p.sd += c0;
+        if (p.vo) p.vo += c0;
+        if (p0.out_rec) p.out_rec = p0.chunk_recs + (c0 ? 1 : 0);
+        if ((e = launch_scan_k<KIND_ILV, uint16_t>(p, st)) != cudaSuccess) return e;
+        if (p0.out_rec && c0) {
+            reduce_records_kernel<<<1, 64, 0, st>>>(p0.chunk_recs, 2, p0.chunk_recs);
+            ++g_launches;
+        }
+    }
+    if (p0.out_rec) {
+        reduce_records_kernel<<<1, 32, 0, st>>>(p0.chunk_recs, 1, p0.out_rec);
+        ++g_launches;
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st) {
     cudaError_t e = launch_ws(p, st);
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();
+    if (p.cd.kind == QLM_CAND_RANDOM && p.dm.T > 256 && p.ilv && p.ilv_cap >= 32 &&
+        p.chunk_recs && !p.cd.first_from && p.cd.count >= 4096)
+        return launch_two_phase(p, st);
     return launch_scan(p, st);
 }
 

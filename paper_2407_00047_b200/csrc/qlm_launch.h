@@ -25,7 +25,15 @@ struct ScanParams {
     int n_out;                 // number of non-null bulk outputs
     int rep_shift;             // group tables replicated 1 << rep_shift times in smem
     int off_grec, off_ab, off_q, off_tr, off_scratch, off_stage;
+    int64_t ld_out;            // leading dimension of the bulk outputs (0 = count)
+    uint32_t *ilv;             // large-T RANDOM: word-interleaved row scratch [words][ilv_cap]
+    int64_t ilv_cap;           // candidates per chunk that fit the scratch
+    qlm_record *chunk_recs;    // [2] running argmin across chunks
 };
+
+// Internal candidate kind: rows materialised word-interleaved by fy_rows_kernel
+// (word w of chunk-local candidate l at rows[(w * stride + l) * 4]).
+constexpr int KIND_ILV = 3;
 
 extern std::atomic<int64_t> g_launches;
 int sm_count();

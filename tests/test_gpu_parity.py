@@ -413,3 +413,34 @@ def test_nccl_plumbing_single_rank():
         assert torch.equal(sum_counts(cnt.clone()), cnt)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,n,out", [("C5", 10_000, False), ("C5h", 4_160, True), ("C4", 9_000, False)])
+def test_two_phase_large_T_matches_fused(cfg, n, out, monkeypatch):
+    """Large-T RANDOM scoring through interleaved row chunks (fy_rows_kernel +
+    the scan kernel) equals the fused per-thread Fisher-Yates scan bit for bit,
+    across several chunks with a ragged tail, and matches the oracle."""
+    p = make_config(cfg)
+    res = {}
+    for mode in ("fused", "two_phase"):
+        monkeypatch.setenv("QLM_NO_TWO_PHASE", "1" if mode == "fused" else "0")
+        monkeypatch.setenv("QLM_ILV_CAP", "4096")
+        e = est_of(p)
+        cand = e.random(7, n, seed=1)
+        rec = torch.empty(2, dtype=torch.int64, device="cuda")
+        bufs = {"n_over": torch.empty(n, dtype=torch.int32, device="cuda")}
+        if out:
+            bufs.update({k: torch.empty((p.G, n), dtype=torch.float32, device="cuda")
+                         for k in ("wt", "sd", "v")})
+        r = e.score_estimate(cand, out=bufs, rec=rec)
+        res[mode] = (r, rec.clone(), e.best_ordering_async(cand).clone())
+    (a, ra, ba), (b, rb, bb) = res["fused"], res["two_phase"]
+    for k in ("s1", "s2", "n_over") + (("wt", "sd", "v") if out else ()):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(ra, rb) and torch.equal(ba, bb) and torch.equal(ra, ba)
+    idx = np.r_[0:200, 4090:4100, n - 200:n]
+    o = O.Oracle(p)
+    ref = {k: np.concatenate([o.score_range(O.RANDOM, 7 + s, t - s, seed=1)[k]
+                              for s, t in ((0, 200), (4090, 4100), (n - 200, n))])
+           for k in ("s1", "s2", "n_over")}
+    check_scores(b["s1"].cpu().numpy()[idx], b["s2"].cpu().numpy()[idx], ref, p)
