@@ -132,10 +132,11 @@ static double tail_of(const or_problem *p, int32_t d, int32_t m)
  * prose of P:L705): walking a queue in order, an exclusive accumulator A
  * holds the expected time until the slot can start, B its variance.
  *   - on a model change into the slot (Eq. 9, m_{-1} = resident model, R4):
- *       A += tail(previous model)   [the group before the boundary contributes
- *                                    its completion C = W + P + D, R1]
- *            (skipped at the queue's first slot unless a backlog is pinned, R4/R12)
- *       A += swap[prev][m]          [Eq. 10 2nd term, incl. slot's own switch, R2]
+ *       A += tail(previous model) + swap[prev][m]    (one transition term)
+ *            tail: the group before the boundary contributes its completion
+ *                  C = W + P + D (R1); skipped at the queue's first slot
+ *                  unless a backlog is pinned (R4/R12)
+ *            swap: Eq. 10 2nd term, incl. the slot's own switch (R2)
  *   - wt = A, V = B                 [exclusive: groups ahead only, R5]
  *   - A += n*mu/Theta, B += n*var/Theta^2   [Eq. 2/3, each group its own stats, R6/R7]
  * Returns 0, or -1 if the row is not a permutation of 0..T-1 (Eq. 6).     */
@@ -164,8 +165,9 @@ int or_estimate_row(const or_problem *p, const int32_t *row,
         int32_t i = tok, m = p->model[i];
         if (m != prev) {                                     /* t = 1, Eq. 9 */
             int backlog = p->q_bmean[q] > 0.0;
-            if (!first || backlog) A = A + tail_of(p, d, prev);
-            A = A + p->swap[(d * p->M + prev) * p->M + m];
+            double trans = p->swap[(d * p->M + prev) * p->M + m];
+            if (!first || backlog) trans = tail_of(p, d, prev) + trans;
+            A = A + trans;
         }
         wt[i] = A;
         V[i] = B;
@@ -349,8 +351,9 @@ int64_t or_mc_count(const or_problem *p, int kind, const void *rows, int32_t tok
                 int32_t i = tok, m = p->model[i];
                 if (m != prev) {
                     int backlog = p->q_bmean[q] > 0.0;
-                    if (!first_slot || backlog) A = A + tail_of(p, d, prev);
-                    A = A + p->swap[(d * p->M + prev) * p->M + m];
+                    double trans = p->swap[(d * p->M + prev) * p->M + m];
+                    if (!first_slot || backlog) trans = tail_of(p, d, prev) + trans;
+                    A = A + trans;
                 }
                 if (A > p->slo[i]) cnt[i] += 1;
                 A = A + (double)x[i] / p->theta[d * p->M + m];

@@ -223,16 +223,16 @@ __device__ __forceinline__ void tokens_enum(uint64_t c, int T, F &&f) {
 // with 8 copies a warp's random 16-B reads are bank-conflict free.
 //
 // Transition table (Eq. 9/10, R1/R2/R4): rows p' in [0, 2M) per device:
-//   p' <  M : the previous group ran model p'   -> {m != p' ? tail[d][p'] : 0, swap[d][p'][m]}
+//   p' <  M : the previous group ran model p'   -> (m != p' ? tail[d][p'] : 0) + swap[d][p'][m]
 //   p' >= M : nothing has run yet on resident r = p' - M (no backlog)
-//                                               -> {0, swap[d][r][m]}
-// so every slot does A = (A + x) + y with no branch; x = y = 0 when the model
-// does not change, and A + 0.0 == A keeps the arithmetic operation-for-
-// operation identical to the sequential definition.
+//                                               -> 0 + swap[d][r][m]
+// (one fp64 transition term, R2/R3), so every slot does A = A + c with no
+// branch; c = 0 when the model does not change, and A + 0.0 == A keeps the
+// arithmetic operation-for-operation identical to the sequential definition.
 struct SlotTables {
     const GRec *sg;        // [G << rs]        {slo, n, model}
     const double2 *sab;    // [(D*G) << rs]    {n mu / Theta, n var / Theta^2}
-    const double2 *str;    // [D * 2M * M]     {tail part, swap part}
+    const double *str;     // [D * 2M * M]     tail part + swap part (one transition term)
     const QRec *sq;        // [Q]
     int G, Q, M, rs, rl;   // rl = lane & ((1 << rs) - 1)
 };
@@ -255,8 +255,7 @@ __device__ __forceinline__ void group_slot(const SlotTables &t, ScanState &s, in
     g = t.sg[(tok << t.rs) + t.rl];
     const double2 ab = t.sab[((s.d * t.G + tok) << t.rs) + t.rl];
     const int m = g.model;
-    const double2 tr = t.str[(s.d * 2 * t.M + s.prev) * t.M + m];
-    s.A = __dadd_rn(__dadd_rn(s.A, tr.x), tr.y);     // C - W of the group ahead, swap S
+    s.A = __dadd_rn(s.A, t.str[(s.d * 2 * t.M + s.prev) * t.M + m]);   // C - W ahead + swap S
     wt = s.A;
     V = s.B;                                         // exclusive (R5)
     s.A = __dadd_rn(s.A, ab.x);

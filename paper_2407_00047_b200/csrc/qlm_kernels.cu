@@ -132,14 +132,14 @@ __device__ __forceinline__ SlotTables stage_tables(const ScanParams &p, uint8_t 
     for (int i = tid; i < ((dm.D * dm.G) << rs); i += blk) sab[i] = p.tb.ab[i >> rs];
     QRec *sq = reinterpret_cast<QRec *>(smem + p.off_q);
     for (int i = tid; i < dm.Q; i += blk) sq[i] = p.tb.qrec[i];
-    double2 *str = reinterpret_cast<double2 *>(smem + p.off_tr);
+    double *str = reinterpret_cast<double *>(smem + p.off_tr);
     const int M = dm.M;
     for (int i = tid; i < dm.D * 2 * M * M; i += blk) {
         const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
         const int from = pp < M ? pp : pp - M;
         const double sw = p.tb.swap[(d * M + from) * M + m];
         const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
-        str[i] = make_double2(tl, sw);
+        str[i] = __dadd_rn(tl, sw);                       // one transition term (R2/R3)
     }
     SlotTables t;
     t.sg = sg; t.sab = sab; t.str = str; t.sq = sq;
@@ -667,10 +667,10 @@ __global__ void __launch_bounds__(256) mc_sample_kernel(Dims dm, Tables tb, uint
 
 // One warp per (candidate, 32 trials); every lane is one trial.  The warp
 // materialises the candidate's row, then precomputes per group slot (in row
-// order, all trial-independent): the deterministic addends of the Eq. 10 walk
-// at a model change (tail, R3/R4/R12; swap, R2), the SLO, the start value of
+// order, all trial-independent): the deterministic addend of the Eq. 10 walk
+// at a model change (tail + swap, R2/R3/R4/R12), the SLO, the start value of
 // the queue (backlog mean) and the row of Y to read.  The walk itself is then
-// A = start?; A += tail; A += swap; count A > slo; A += y  -- branch-free, in
+// A = start?; A += tail + swap; count A > slo; A += y  -- branch-free, in
 // the oracle's operation order (+0.0 where no model change: A >= 0, so
 // A + 0.0 == A bit for bit).  y is prefetched 16 slots ahead.
 __global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand cd,
@@ -683,9 +683,8 @@ __global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand c
         if (first < 0) return;
     }
     const int T = dm.T, G = dm.G, M = dm.M;
-    double *st = reinterpret_cast<double *>(smem);     // [G] tail addend
-    double *ss = st + G;                                // [G] swap addend
-    double *sslo = ss + G;                              // [G] SLO
+    double *st = reinterpret_cast<double *>(smem);     // [G] transition addend
+    double *sslo = st + G;                              // [G] SLO
     double *sa0 = sslo + G;                             // [G] queue start (backlog mean) or -1
     int32_t *yrow = reinterpret_cast<int32_t *>(sa0 + G);   // [G] d * G + token
     uint16_t *stok = reinterpret_cast<uint16_t *>(yrow + G);  // [G]
@@ -707,13 +706,12 @@ __global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand c
         const bool firsts = i == 0 || sq[i - 1] != q;
         const int prev = firsts ? qr.r : tb.grec[stok[i - 1]].model;
         const int d = qr.d, m = g.model;
-        double t = 0.0, w = 0.0;
+        double c = 0.0;                                  // transition term (R2/R3)
         if (m != prev) {
-            t = (firsts && !qr.backlog) ? 0.0 : tb.tail[d * M + prev];
-            w = tb.swap[(d * M + prev) * M + m];
+            const double t = (firsts && !qr.backlog) ? 0.0 : tb.tail[d * M + prev];
+            c = __dadd_rn(t, tb.swap[(d * M + prev) * M + m]);
         }
-        st[i] = t;
-        ss[i] = w;
+        st[i] = c;
         sslo[i] = g.slo;
         sa0[i] = firsts ? qr.bmean : -1.0;
         yrow[i] = d * G + tok;
@@ -742,7 +740,6 @@ __global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand c
             const double a0 = sa0[i];
             A = a0 >= 0.0 ? a0 : A;
             A = __dadd_rn(A, st[i]);
-            A = __dadd_rn(A, ss[i]);
             const unsigned bal = __ballot_sync(0xFFFFFFFFu, act && A > sslo[i]);
             if (lane == 0 && bal) atomicAdd(&cnt[stok[i]], (unsigned)__popc(bal));
             A = __dadd_rn(A, cur[k]);
@@ -819,7 +816,7 @@ static size_t plan_smem(ScanParams &p, int rep_shift, int kind, int tok_bytes, i
     p.off_grec = (int)off; off = align16(off + ((size_t)dm.G << rep_shift) * sizeof(GRec));
     p.off_ab = (int)off;   off = align16(off + ((size_t)dm.D * dm.G << rep_shift) * sizeof(double2));
     p.off_q = (int)off;    off = align16(off + (size_t)dm.Q * sizeof(QRec));
-    p.off_tr = (int)off;   off = align16(off + (size_t)dm.D * 2 * dm.M * dm.M * sizeof(double2));
+    p.off_tr = (int)off;   off = align16(off + (size_t)dm.D * 2 * dm.M * dm.M * sizeof(double));
     p.off_scratch = (int)off;
     if (kind == QLM_CAND_RANDOM) {
         const int epw = 4 / tok_bytes;
@@ -1055,7 +1052,7 @@ cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, in
 
 cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const Cand &cd, const double *X,
                             int64_t nt, uint32_t *counts, cudaStream_t st) {
-    const size_t smem = (size_t)40 * dm.G + (size_t)4 * ((dm.T + 7) & ~7);
+    const size_t smem = (size_t)32 * dm.G + (size_t)4 * ((dm.T + 7) & ~7);
     cudaError_t e = prep(mc_count_kernel, smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((nt + 31) / 32), (unsigned)cd.count);

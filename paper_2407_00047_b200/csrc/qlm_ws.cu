@@ -106,12 +106,12 @@ __device__ __forceinline__ void produce_row(const Cand &cd, int T, uint8_t *slot
 // trash row, so a separator slot runs the same straight-line code as a group
 // slot; the queue table is padded to T entries so the queue counter needs no
 // clamp.
-struct WsG {                 // 16 B, replicated 1 << RS times
+struct alignas(16) WsG {      // 16 B (one LDS.128), replicated 1 << RS times
     double slo;
     float nf;                // n_i as float (S1 numerator, exact below 2^24)
     int model;
 };
-struct WsQ {                 // 32 B
+struct alignas(16) WsQ {      // 32 B (two LDS.128)
     double bmean, bvar;      // queue reset values (R12)
     int prow0;               // transition-table row at the queue's start (R4)
     int dG;                  // d * (G + 1): device base into the ab table
@@ -157,7 +157,7 @@ __device__ __forceinline__ void flush_pending(Pend *pq, const WsG *__restrict__ 
 
 template <typename TOK, int RS, bool SCORE, bool PAD>
 __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const double2 *__restrict__ sabl,
-                                             const double2 *__restrict__ str, const WsQ *__restrict__ sq,
+                                             const double *__restrict__ str, const WsQ *__restrict__ sq,
                                              uint32_t word, int nvalid_tok, int G, int M, int lane,
                                              float zc2f, float alpha, float *st, int arr_stride,
                                              Pend *pq, Acc &a) {
@@ -193,7 +193,8 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
         }
     }
     // (iii) per-device group work and transition costs
-    double2 ab[K], tr[K];
+    double2 ab[K];
+    double tr[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         ab[k] = sabl[(dk[k] + tg[k]) << RS];
@@ -204,7 +205,7 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
     double A = a.A, B = a.B;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const double A1 = __dadd_rn(__dadd_rn(A, tr[k].x), tr[k].y);
+        const double A1 = __dadd_rn(A, tr[k]);
         wt[k] = A1;
         V[k] = B;
         const double A2 = __dadd_rn(A1, ab[k].x), B2 = __dadd_rn(B, ab[k].y);
@@ -333,14 +334,14 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         r.pad = 0;
         sq[i] = r;
     }
-    double2 *str = reinterpret_cast<double2 *>(smem + p.off_tr);
+    double *str = reinterpret_cast<double *>(smem + p.off_tr);
     for (int i = tid; i < ((D * 2 * M * M) << RS); i += blockDim.x) {
         const int e = i >> RS;
         const int m = e % M, pp = (e / M) % (2 * M), d = e / (2 * M * M);
         const int from = pp < M ? pp : pp - M;
         const double sw = p.tb.swap[(d * M + from) * M + m];
         const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
-        str[i] = make_double2(tl, sw);
+        str[i] = __dadd_rn(tl, sw);                      // one transition term (R2/R3)
     }
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + w.off_bar);
     uint64_t *empty = full + 2 * W;
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
     } else {
         const WsG *sgl = sg + (lane & ((1 << RS) - 1));
         const double2 *sabl = sab + (lane & ((1 << RS) - 1));
-        const double2 *strl = str + (lane & ((1 << RS) - 1));
+        const double *strl = str + (lane & ((1 << RS) - 1));
         const float zc2f = (float)p.zc2;
         const float alpha = p.alpha;
         const double den = *p.tb.den;
@@ -500,7 +501,7 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
     p.off_grec = (int)off; off = a16(off + ((size_t)(dm.G + 1) << rs) * sizeof(WsG));
     p.off_ab = (int)off;   off = a16(off + ((size_t)dm.D * (dm.G + 1) << rs) * sizeof(double2));
     p.off_q = (int)off;    off = a16(off + (size_t)(dm.T + 1) * sizeof(WsQ));
-    p.off_tr = (int)off;   off = a16(off + ((size_t)dm.D * 2 * dm.M * dm.M << rs) * sizeof(double2));
+    p.off_tr = (int)off;   off = a16(off + ((size_t)dm.D * 2 * dm.M * dm.M << rs) * sizeof(double));
     const int epw = 4 / tok_bytes;
     w.tw = (dm.T + epw - 1) / epw;
     w.off_rows = (int)off; off = a16(off + (size_t)2 * W * w.tw * 128);
