@@ -889,6 +889,16 @@ static cudaError_t launch_scan_k(ScanParams &p, cudaStream_t st) {
                  : launch_scan_t<KIND, TOK, OUT_DIRECT, false>(p, st);
 }
 
+// The warp-per-candidate kernel (qlm_wide.cu) takes bulk outputs whose
+// [G][32] staging tile does not fit (G > ~420): thread-per-candidate direct
+// stores would scatter 4-B writes across partial sectors.
+static bool wide_first(const ScanParams &p) {
+    const bool bulk = p.wt || p.sd || p.vo;
+    if (env_int("QLM_WIDE_SCORE", 0)) return true;         // experiments: score-only too
+    const size_t stage_bytes = (size_t)3 * 32 * p.dm.G * 4;
+    return bulk && stage_bytes + 64 * 1024 > kMaxSmem;
+}
+
 // Large-T RANDOM (T > 256, outside the warp-specialised kernel's range): the
 // per-thread Fisher-Yates scratch (2T bytes) would cap the fused scan at a few
 // warps per SM, so rows are generated per chunk into an interleaved scratch by
@@ -923,7 +933,12 @@ static cudaError_t launch_two_phase(const ScanParams &p0, cudaStream_t st) {
         if (p.sd) p.sd += c0;
         if (p.vo) p.vo += c0;
         if (p0.out_rec) p.out_rec = p0.chunk_recs + (c0 ? 1 : 0);
-        if ((e = launch_scan_k<KIND_ILV, uint16_t>(p, st)) != cudaSuccess) return e;
+        e = wide_first(p) ? launch_wide(p, st) : cudaErrorNotSupported;
+        if (e == cudaErrorNotSupported) {
+            cudaGetLastError();
+            e = launch_scan_k<KIND_ILV, uint16_t>(p, st);
+        }
+        if (e != cudaSuccess) return e;
         if (p0.out_rec && c0) {
             reduce_records_kernel<<<1, 64, 0, st>>>(p0.chunk_recs, 2, p0.chunk_recs);
             ++g_launches;
@@ -940,6 +955,11 @@ cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st) {
     cudaError_t e = launch_ws(p, st);
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();
+    if (p.cd.kind == QLM_CAND_EXPLICIT && p.cd.tb == 2 && wide_first(p)) {
+        e = launch_wide(p, st);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
     if (p.cd.kind == QLM_CAND_RANDOM && p.dm.T > 256 && p.ilv && p.ilv_cap >= 32 &&
         p.chunk_recs && !p.cd.first_from && p.cd.count >= 4096)
         return launch_two_phase(p, st);

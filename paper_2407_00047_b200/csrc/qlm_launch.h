@@ -45,6 +45,7 @@ cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
 cudaError_t launch_scan(ScanParams p, cudaStream_t st);
 cudaError_t launch_ws(ScanParams p, cudaStream_t st);      // warp-specialised fast path
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st);   // ws, else scan
+cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per candidate (large G)
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,
                         cudaStream_t st);
 cudaError_t launch_reduce_records(const qlm_record *recs, int n, qlm_record *out,

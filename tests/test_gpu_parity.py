@@ -435,12 +435,53 @@ def test_two_phase_large_T_matches_fused(cfg, n, out, monkeypatch):
         r = e.score_estimate(cand, out=bufs, rec=rec)
         res[mode] = (r, rec.clone(), e.best_ordering_async(cand).clone())
     (a, ra, ba), (b, rb, bb) = res["fused"], res["two_phase"]
-    for k in ("s1", "s2", "n_over") + (("wt", "sd", "v") if out else ()):
-        assert torch.equal(a[k], b[k]), k
-    assert torch.equal(ra, rb) and torch.equal(ba, bb) and torch.equal(ra, ba)
+    if not out:          # same thread-per-candidate scan on both sides: identical bits
+        for k in ("s1", "s2", "n_over"):
+            assert torch.equal(a[k], b[k]), k
+        assert torch.equal(ra, rb) and torch.equal(ba, bb) and torch.equal(ra, ba)
+    else:                # bulk at G = 1024 runs the warp-per-candidate kernel (DESIGN R15)
+        o = O.Oracle(p)
+        est = o.estimate_range(O.RANDOM, 7, 64, seed=1)
+        check_estimates({k: b[k][:, :64] for k in ("wt", "sd", "v")}, est)
+        tail = o.estimate_range(O.RANDOM, 7 + n - 40, 40, seed=1)
+        check_estimates({k: b[k][:, n - 40:] for k in ("wt", "sd", "v")}, tail)
     idx = np.r_[0:200, 4090:4100, n - 200:n]
     o = O.Oracle(p)
     ref = {k: np.concatenate([o.score_range(O.RANDOM, 7 + s, t - s, seed=1)[k]
                               for s, t in ((0, 200), (4090, 4100), (n - 200, n))])
            for k in ("s1", "s2", "n_over")}
     check_scores(b["s1"].cpu().numpy()[idx], b["s2"].cpu().numpy()[idx], ref, p)
+
+
+@pytest.mark.parametrize("G,Q,D,backlog,n", [(1024, 32, 1, False, 4104), (430, 3, 2, True, 4099),
+                                               (700, 60, 2, False, 4096)])
+def test_wide_kernel_bulk_large_G(G, Q, D, backlog, n):
+    """Bulk outputs with no [G][32] staging tile (warp-per-candidate kernel,
+    segmented scan over 32 row chunks; DESIGN R15): oracle parity on the
+    first and last candidates (ragged batch of 8), EXPLICIT u16 rows and the
+    RANDOM two-phase chunks agree, and the argmin follows the oracle rule."""
+    rng = np.random.default_rng(G + Q)
+    p = make_random_problem(rng, G, Q, 4, D, backlog=backlog)
+    e = est_of(p)
+    o = O.Oracle(p)
+    cand = e.random(11, n, seed=5)
+    bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+    rec = torch.empty(2, dtype=torch.int64, device="cuda")
+    r = e.score_estimate(cand, out=bufs, rec=rec)
+    for lo, cnt in ((0, 48), (n - 37, 37)):
+        est = o.estimate_range(O.RANDOM, 11 + lo, cnt, seed=5)
+        check_estimates({k: r[k][:, lo:lo + cnt] for k in ("wt", "sd", "v")}, est)
+        ref = o.score_range(O.RANDOM, 11 + lo, cnt, seed=5)
+        check_scores(r["s1"][lo:lo + cnt].cpu().numpy(), r["s2"][lo:lo + cnt].cpu().numpy(), ref, p)
+    # EXPLICIT u16 rows of the same candidates take the same kernel
+    m = 600
+    rows = np.stack([O.random_row(5, 11 + c, p.T) for c in range(m)])
+    ex = e.explicit(rows_tensor(rows, token_bytes=2))
+    b2 = {k: torch.empty((p.G, m), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+    r2 = e.score_estimate(ex, out=b2)
+    for k in ("wt", "sd", "v"):
+        assert torch.allclose(r2[k], r[k][:, :m], rtol=1e-6, atol=1e-6), k
+    ref = o.score_range(O.RANDOM, 11, min(n, 4096), seed=5)
+    s1 = r["s1"].cpu().numpy()[:4096]
+    s2 = r["s2"].cpu().numpy()[:4096]
+    check_scores(s1, s2, ref, p)
