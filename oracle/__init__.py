@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "qlm_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-EXPLICIT, RANDOM, ENUM = 0, 1, 2
+EXPLICIT, RANDOM, ENUM, NEIGHBOR = 0, 1, 2, 3
 Z_CLAMP = 8.0
 ALPHA = 0.01
 
@@ -54,6 +54,7 @@ def lib():
         _lib.or_philox4x32_10.argtypes = [vp, vp, vp]
         _lib.or_random_row.argtypes = [u64, u64, i32, vp]
         _lib.or_enum_row.argtypes = [u64, i32, vp]
+        _lib.or_neighbor_row.argtypes = [vp, i32, u64, u64, i32, vp]
         _lib.or_estimate_row.argtypes = [P, vp, dp, dp, vp, vp]
         _lib.or_estimate_row.restype = C.c_int
         _lib.or_violation.argtypes = [C.c_double] * 4
@@ -131,21 +132,27 @@ class Oracle:
         return s1.value, s2.value, no.value
 
     # -- ranges --------------------------------------------------------------
-    def _rows_args(self, kind, rows):
+    def _rows_args(self, kind, rows, moves=0):
         if kind == EXPLICIT:
             rows = np.ascontiguousarray(rows)
             return rows, rows.dtype.itemsize, rows.strides[0]
+        if kind == NEIGHBOR:         # rows = base row (uint8 / uint16), stride slot = moves
+            rows = np.ascontiguousarray(rows, np.uint16)
+            return rows, 2, int(moves)
         return None, 1, 0
 
-    def score_range(self, kind, first, count, seed=0, rows=None):
-        rows, tb, stride = self._rows_args(kind, rows)
+    def neighbor_row(self, base, seed: int, c: int, moves: int) -> np.ndarray:
+        return neighbor_row(base, seed, c, moves)
+
+    def score_range(self, kind, first, count, seed=0, rows=None, moves=0):
+        rows, tb, stride = self._rows_args(kind, rows, moves)
         s1, s2, no = np.zeros(count), np.zeros(count), np.zeros(count, np.int32)
         bad = lib().or_score_range(C.byref(self.p), kind, _ptr(rows), tb, stride, seed, first,
                                    count, _ptr(s1), _ptr(s2), _ptr(no))
         return dict(s1=s1, s2=s2, n_over=no, bad=bad)
 
-    def estimate_range(self, kind, first, count, seed=0, rows=None):
-        rows, tb, stride = self._rows_args(kind, rows)
+    def estimate_range(self, kind, first, count, seed=0, rows=None, moves=0):
+        rows, tb, stride = self._rows_args(kind, rows, moves)
         G = self.G
         wt, sd, v = np.zeros((count, G)), np.zeros((count, G)), np.zeros((count, G))
         bad = lib().or_estimate_range(C.byref(self.p), kind, _ptr(rows), tb, stride, seed, first,
@@ -157,8 +164,8 @@ class Oracle:
         lib().or_mc_sample(C.byref(self.p), mc_seed, trial_first, trial_count, _ptr(X))
         return X
 
-    def mc_count(self, kind, first, count, X, seed=0, rows=None):
-        rows, tb, stride = self._rows_args(kind, rows)
+    def mc_count(self, kind, first, count, X, seed=0, rows=None, moves=0):
+        rows, tb, stride = self._rows_args(kind, rows, moves)
         X = np.ascontiguousarray(X, np.uint32)
         counts = np.zeros((count, self.G), np.uint32)
         bad = lib().or_mc_count(C.byref(self.p), kind, _ptr(rows), tb, stride, seed, first, count,
@@ -180,6 +187,39 @@ def random_row(seed: int, c: int, T: int) -> np.ndarray:
     row = np.zeros(T, np.int32)
     lib().or_random_row(seed, c, T, _ptr(row))
     return row
+
+
+def neighbor_row(base, seed: int, c: int, moves: int) -> np.ndarray:
+    """R18: the base row with `moves` Philox-drawn transpositions."""
+    b = np.ascontiguousarray(base, np.int32)
+    row = np.zeros(len(b), np.int32)
+    lib().or_neighbor_row(_ptr(b), len(b), seed, c, moves, _ptr(row))
+    return row
+
+
+def key32(s1: float, s2: float):
+    """The objective key of R11 as a comparable tuple (fp32 S1, fp32 S2)."""
+    return (float(np.float32(s1)), float(np.float32(s2)))
+
+
+def local_search(o: "Oracle", start_row, seed: int, moves: int, per_iter: int, iters: int):
+    """SURVEY 8(f) N1 as plain iterated best-of-N: each iteration scores the
+    per_iter NEIGHBOR candidates [it*per_iter, (it+1)*per_iter) of the
+    incumbent (R18) and adopts the lexicographic argmin (R11/R14) if its key
+    beats the incumbent's.  Returns (row, key, number of adoptions)."""
+    inc = np.ascontiguousarray(start_row, np.int32)
+    s1, s2, _ = o.score(inc)
+    inc_key = key32(s1, s2)
+    adopted = 0
+    for it in range(iters):
+        r = o.score_range(NEIGHBOR, it * per_iter, per_iter, seed=seed, rows=inc, moves=moves)
+        i = argmin_key(r["s1"], r["s2"])
+        k = key32(r["s1"][i], r["s2"][i])
+        if k < inc_key:
+            inc = neighbor_row(inc, seed, it * per_iter + i, moves)
+            inc_key = k
+            adopted += 1
+    return inc, inc_key, adopted
 
 
 def enum_row(c: int, T: int) -> np.ndarray:

@@ -19,6 +19,10 @@
  *   or_philox4x32_10   Random123 known-answer vectors.
  *   or_enum_row        itertools.permutations lexicographic order (T <= 7).
  *   or_random_row      permutation invariant + chi-square uniformity (T = 4).
+ *   or_neighbor_row    permutation invariant, <= 2k displaced positions,
+ *                      k = 0 identity, chi-square uniformity of (i, j);
+ *                      local search built on it reaches the brute-force
+ *                      optimum on small instances (tests/test_oracle_pins.py).
  *   or_estimate_row    SPEC worked examples S:L279/287/296/306/315, closed
  *                      form for identical groups (Eq. 2/3), Insight-3
  *                      transition arithmetic, textbook Phi-bar values.
@@ -94,6 +98,29 @@ void or_random_row(uint64_t seed, uint64_t c, int32_t T, int32_t *row)
         }
         uint32_t u = words[i % 4];
         int32_t j = i + (int32_t)(((uint64_t)u * (uint64_t)(T - i)) >> 32);
+        int32_t t = row[i]; row[i] = row[j]; row[j] = t;
+    }
+}
+
+/* NEIGHBOR(base, seed, c, k) (R18, neighbourhood search of
+ * the incumbent ordering): the base row with k random transpositions.  Move
+ * m swaps positions i = (u0 * T) >> 32 and j = (u1 * T) >> 32 (i == j leaves
+ * the row as it is), with (u0, u1) = words 2(m mod 2), 2(m mod 2)+1 of
+ * Philox4x32-10(key = seed, ctr = (m / 2, lo32 c, hi32 c, 0x4E424852)).     */
+void or_neighbor_row(const int32_t *base, int32_t T, uint64_t seed, uint64_t c, int32_t k,
+                     int32_t *row)
+{
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint32_t words[4];
+    for (int32_t s = 0; s < T; ++s) row[s] = base[s];
+    for (int32_t m = 0; m < k; ++m) {
+        if (m % 2 == 0) {
+            uint32_t ctr[4] = { (uint32_t)(m / 2), (uint32_t)c, (uint32_t)(c >> 32), 0x4E424852u };
+            or_philox4x32_10(ctr, key, words);
+        }
+        uint32_t u0 = words[2 * (m % 2)], u1 = words[2 * (m % 2) + 1];
+        int32_t i = (int32_t)(((uint64_t)u0 * (uint64_t)T) >> 32);
+        int32_t j = (int32_t)(((uint64_t)u1 * (uint64_t)T) >> 32);
         int32_t t = row[i]; row[i] = row[j]; row[j] = t;
     }
 }
@@ -226,13 +253,21 @@ int or_score_row(const or_problem *p, const int32_t *row, double *s1, double *s2
 }
 
 /* ---- candidate ranges ---------------------------------------------------- */
-enum { OR_EXPLICIT = 0, OR_RANDOM = 1, OR_ENUM = 2 };
+enum { OR_EXPLICIT = 0, OR_RANDOM = 1, OR_ENUM = 2, OR_NEIGHBOR = 3 };
 
 static void get_row(int kind, const void *rows, int32_t token_bytes, int64_t stride,
                     uint64_t seed, uint64_t c, int64_t local, int32_t T, int32_t *row)
 {
     if (kind == OR_RANDOM) { or_random_row(seed, c, T, row); return; }
     if (kind == OR_ENUM) { or_enum_row(c, T, row); return; }
+    if (kind == OR_NEIGHBOR) {       /* rows = the base row, stride = k (number of moves) */
+        int32_t *b = (int32_t *)malloc(sizeof(int32_t) * (size_t)T);
+        for (int32_t s = 0; s < T; ++s)
+            b[s] = token_bytes == 1 ? ((const uint8_t *)rows)[s] : ((const uint16_t *)rows)[s];
+        or_neighbor_row(b, T, seed, c, (int32_t)stride, row);
+        free(b);
+        return;
+    }
     const uint8_t *base = (const uint8_t *)rows + local * stride;
     for (int32_t s = 0; s < T; ++s)
         row[s] = token_bytes == 1 ? base[s] : ((const uint16_t *)base)[s];

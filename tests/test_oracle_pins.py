@@ -417,3 +417,51 @@ def test_mc_vs_gaussian_within_clt_scale():
     vmc = cnt / T_mc
     se = np.sqrt(np.maximum(v * (1 - v), 1e-4) / T_mc)
     assert np.all(np.abs(vmc - v) <= 0.03 + 5 * se)
+
+
+# ------------------------------------------------------- NEIGHBOR rows (R18, N1)
+@pytest.mark.parametrize("T", [4, 17, 71])
+def test_neighbor_rows_are_nearby_permutations(T):
+    base = O.random_row(3, 5, T)
+    assert np.array_equal(O.neighbor_row(base, 9, 123, 0), base)      # k = 0: the base row
+    for k in (1, 2, 5):
+        for c in range(200):
+            row = O.neighbor_row(base, 9, c, k)
+            assert sorted(row) == list(range(T))
+            assert np.count_nonzero(row != base) <= 2 * k
+            assert np.count_nonzero(row != base) != 1                  # a transposition moves 0 or 2
+
+
+def test_neighbor_single_move_uniform_over_pairs():
+    # k = 1: positions i, j uniform and independent -> P(i == j) = 1/T, and each
+    # unordered pair {i, j}, i != j, has probability 2/T^2.
+    T, N = 5, 20000
+    base = np.arange(T)
+    counts = {}
+    for c in range(N):
+        d = tuple(np.nonzero(O.neighbor_row(base, 4, c, 1) != base)[0])
+        counts[d] = counts.get(d, 0) + 1
+    pairs = list(itertools.combinations(range(T), 2))
+    obs = [counts.get((), 0)] + [counts.get(p, 0) for p in pairs]
+    exp = [N / T] + [N * 2 / T**2] * len(pairs)
+    assert sum(obs) == N
+    assert stats.chisquare(obs, exp).pvalue > 1e-3
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_local_search_reaches_brute_force_optimum(seed):
+    # SURVEY 8(f) N1 on instances small enough for exhaustive search (ENUM over
+    # all T! rows): iterated best-of-N over 2-move neighbourhoods, started from
+    # the identity row, ends at the brute-force minimum of the (S1, S2) key.
+    rng = np.random.default_rng(300 + seed)
+    G, Q = int(rng.integers(4, 7)), int(rng.integers(1, 3))
+    p = make_random_problem(rng, G, Q, 2, 1, backlog=bool(seed % 2))
+    o = O.Oracle(p)
+    T = p.T
+    r = o.score_range(O.ENUM, 0, math.factorial(T))
+    best = O.key32(*min(zip(r["s1"], r["s2"]), key=lambda x: O.key32(*x)))
+    row, key, adopted = O.local_search(o, np.arange(T), seed=seed + 1, moves=2, per_iter=48, iters=40)
+    assert key == best
+    s1, s2, _ = o.score(row)
+    assert O.key32(s1, s2) == key
+    assert sorted(row) == list(range(T))
