@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define QLM_ABI_VERSION 1
+#define QLM_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define QLM_API __attribute__((visibility("default")))
@@ -101,7 +101,8 @@ typedef struct {
  * a permutation of 0..T-1; token < G is a request group, token >= G a
  * queue separator.  Queue q holds the groups between the q-th and the
  * (q+1)-th separator, in order (position j of Eq. 6).                       */
-enum { QLM_CAND_EXPLICIT = 0, QLM_CAND_RANDOM = 1, QLM_CAND_ENUM = 2 };
+enum { QLM_CAND_EXPLICIT = 0, QLM_CAND_RANDOM = 1, QLM_CAND_ENUM = 2, QLM_CAND_NEIGHBOR = 3 };
+#define QLM_MAX_MOVES 8
 
 /* Best-candidate record, device-resident (16 bytes).  key orders
  * candidates lexicographically by (fp32 S1, fp32 S2) (R11); ties go to the
@@ -111,18 +112,28 @@ typedef struct {
     int64_t index;   /* global candidate index                                      */
 } qlm_record;
 
+/* Candidate kinds (R10, R18):
+ *   EXPLICIT  rows given by the caller;
+ *   RANDOM    candidate c = Fisher-Yates permutation from Philox(seed, c);
+ *   ENUM      candidate c = the c-th permutation in lexicographic order (T <= 20);
+ *   NEIGHBOR  candidate c = the base row `rows` (one row of T tokens) with
+ *             `moves` Philox(seed, c)-drawn transpositions (R18; SURVEY 8(f) N1,
+ *             the neighbourhood of an incumbent ordering for local search).   */
 typedef struct {
     int32_t kind;          /* QLM_CAND_*                                             */
-    int32_t token_bytes;   /* EXPLICIT: 1 (needs T <= 256) or 2                       */
-    const void *rows;      /* EXPLICIT: device [count][stride] bytes, 16-B aligned   */
+    int32_t token_bytes;   /* EXPLICIT / NEIGHBOR: 1 (needs T <= 256) or 2            */
+    const void *rows;      /* EXPLICIT: device [count][stride] bytes, 16-B aligned;
+                              NEIGHBOR: device base row, T tokens, 16-B aligned       */
     int64_t stride;        /* EXPLICIT: bytes per row, multiple of 16, >= T*token_bytes */
-    uint64_t seed;         /* RANDOM: Philox key                                      */
-    int64_t first;         /* global index of the first candidate (RANDOM/ENUM)      */
+    uint64_t seed;         /* RANDOM / NEIGHBOR: Philox key                           */
+    int64_t first;         /* global index of the first candidate (RANDOM/ENUM/NEIGHBOR) */
     int64_t count;         /* number of candidates, >= 0                              */
     const qlm_record *first_from; /* optional device record: if non-NULL, count must be
                               1 and the candidate index is read on the device from
                               first_from->index at kernel time (no host sync); an
                               index < 0 makes the call a no-op on the device.        */
+    int32_t moves;         /* NEIGHBOR: transpositions per candidate, 0..QLM_MAX_MOVES */
+    int32_t reserved;      /* must be 0                                               */
 } qlm_candidates;
 
 typedef struct {
@@ -174,6 +185,29 @@ QLM_API int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, 
  * queue_of_group[G] / pos_of_group[G] (both nullable).                      */
 QLM_API int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
                       int32_t *queue_of_group, int32_t *pos_of_group, void *stream);
+
+/* Local-search step (R18), asynchronous on `stream`:
+ * if *rec (e.g. from qlm_best_ordering_async over NEIGHBOR candidates of
+ * base row cand->rows) has index >= 0 and a key strictly below
+ * incumbent->key, the winning candidate's row is materialised into
+ * cand->rows (in place, it becomes the new base row) and *incumbent = *rec;
+ * otherwise nothing changes.  cand must be NEIGHBOR; rec and incumbent are
+ * device records; the decision is taken on the device (no host sync).      */
+QLM_API int qlm_adopt_best(qlm_ctx *ctx, const qlm_candidates *cand, const qlm_record *rec,
+                   qlm_record *incumbent, void *stream);
+
+/* Iterated best-of-N local search (R18), entirely asynchronous on `stream`:
+ * scores the device row `row` (T tokens of token_bytes each, 16-B aligned)
+ * into *incumbent, then for it = 0..iters-1 scores NEIGHBOR candidates
+ * [it*per_iter, (it+1)*per_iter) of the current row (seed, moves) and adopts
+ * the argmin if it improves the key (qlm_adopt_best).  On completion `row`
+ * holds the best ordering found and *incumbent its key (index = the
+ * candidate index it was adopted from, -1 if the start row was kept).
+ * Errors: QLM_EINVAL (moves outside 1..QLM_MAX_MOVES, per_iter < 1,
+ * iters < 0, NULL pointers, misaligned row).                               */
+QLM_API int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves,
+                     int64_t per_iter, int32_t iters, uint64_t seed, qlm_record *incumbent,
+                     void *stream);
 
 /* Bulk per-group estimates for every candidate (Eq. 2/3/10), group-major:
  * device fp32 [G][count] arrays, element [g][k] = group g in candidate

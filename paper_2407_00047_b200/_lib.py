@@ -14,7 +14,8 @@ LIB_PATH = os.environ.get("QLM_LIB_PATH") or os.path.join(os.path.dirname(os.pat
                                                           "libqlm.so")
 
 QLM_OK, QLM_EINVAL, QLM_ENOMEM, QLM_ECUDA, QLM_EBADORDER, QLM_ERANGE = 0, 1, 2, 3, 5, 6
-CAND_EXPLICIT, CAND_RANDOM, CAND_ENUM = 0, 1, 2
+CAND_EXPLICIT, CAND_RANDOM, CAND_ENUM, CAND_NEIGHBOR = 0, 1, 2, 3
+MAX_MOVES = 8
 
 # numpy mirrors of the C structs (layout asserted in tests/test_abi.py)
 GROUP_DTYPE = np.dtype([("model", "<i4"), ("n_req", "<i4"), ("slo_s", "<f8"), ("mu_out", "<f8"),
@@ -45,7 +46,8 @@ class Record(C.Structure):
 class Candidates(C.Structure):
     _fields_ = [("kind", C.c_int32), ("token_bytes", C.c_int32), ("rows", C.c_void_p),
                 ("stride", C.c_int64), ("seed", C.c_uint64), ("first", C.c_int64),
-                ("count", C.c_int64), ("first_from", C.c_void_p)]
+                ("count", C.c_int64), ("first_from", C.c_void_p), ("moves", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class Best(C.Structure):
@@ -76,6 +78,8 @@ SIGNATURES = {
     "qlm_check_rows": (C.c_int, [_vp, C.POINTER(Candidates), C.POINTER(C.c_int64), _vp]),
     "qlm_dims": (C.c_int, [_vp] + [C.POINTER(C.c_int32)] * 5),
     "qlm_kernel_launches": (C.c_int64, []),
+    "qlm_adopt_best": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp]),
+    "qlm_local_search": (C.c_int, [_vp, _vp, _i32, _i32, _i64, _i32, _u64, _vp, _vp]),
     "qlm_abi_version": (C.c_int, []),
 }
 

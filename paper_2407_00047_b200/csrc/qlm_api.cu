@@ -53,6 +53,7 @@ struct qlm_ctx {
     qlm_record *d_block_recs = nullptr;
     unsigned int *d_counter = nullptr;
     qlm_record *d_rec = nullptr;           // sync best_ordering
+    qlm_record *d_ls_rec = nullptr;        // local search: per-iteration winner
     int32_t *d_dec_out = nullptr;          // [2][G] sync decode
     unsigned long long *d_bad = nullptr;
     int max_blocks = 0;
@@ -122,6 +123,19 @@ int check_cand(const qlm_ctx *ctx, const qlm_candidates *c) {
         if (c->count > 0 && c->first > INT64_MAX - c->count)
             return fail(QLM_ERANGE, "cand.first + cand.count overflows");
         break;
+    case QLM_CAND_NEIGHBOR:
+        if (c->token_bytes != 1 && c->token_bytes != 2)
+            return fail(QLM_EINVAL, "cand.token_bytes=%d must be 1 or 2", c->token_bytes);
+        if (c->token_bytes == 1 && T > 256)
+            return fail(QLM_EINVAL, "cand.token_bytes=1 needs T=%d <= 256", T);
+        if (!c->rows) return fail(QLM_EINVAL, "cand.rows (NEIGHBOR base row) is NULL");
+        if (((uintptr_t)c->rows & 15) != 0) return fail(QLM_EINVAL, "cand.rows not 16-B aligned");
+        if (c->moves < 0 || c->moves > QLM_MAX_MOVES)
+            return fail(QLM_EINVAL, "cand.moves=%d must lie in [0, %d]", c->moves, QLM_MAX_MOVES);
+        if (c->first < 0) return fail(QLM_EINVAL, "cand.first=%lld < 0", (long long)c->first);
+        if (c->count > 0 && c->first > INT64_MAX - c->count)
+            return fail(QLM_ERANGE, "cand.first + cand.count overflows");
+        break;
     case QLM_CAND_ENUM: {
         if (T > 20) return fail(QLM_ERANGE, "ENUM needs T=%d <= 20", T);
         uint64_t f = 1;
@@ -148,6 +162,7 @@ Cand to_cand(const qlm_candidates *c) {
     d.first = c->first;
     d.count = c->count;
     d.first_from = c->first_from;
+    d.moves = c->kind == QLM_CAND_NEIGHBOR ? c->moves : 0;
     return d;
 }
 
@@ -345,6 +360,7 @@ int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int3
         cudaMalloc(&ctx->d_block_recs, ctx->max_blocks * sizeof(qlm_record)) != cudaSuccess ||
         cudaMalloc(&ctx->d_counter, 64) != cudaSuccess ||
         cudaMalloc(&ctx->d_rec, 64) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ls_rec, 64) != cudaSuccess ||
         cudaMalloc(&ctx->d_dec_out, 2 * (size_t)G * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&ctx->d_bad, 64) != cudaSuccess) {
         qlm_destroy(ctx);
@@ -392,7 +408,8 @@ void qlm_destroy(qlm_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     void *ptrs[] = {ctx->d_raw, ctx->d_tab, ctx->d_block_recs, ctx->d_counter, ctx->d_rec,
-                    ctx->d_dec_out, ctx->d_bad, ctx->d_X, ctx->d_ilv, ctx->d_chunk_recs};
+                    ctx->d_dec_out, ctx->d_bad, ctx->d_X, ctx->d_ilv, ctx->d_chunk_recs,
+                    ctx->d_ls_rec};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete ctx;
@@ -617,6 +634,61 @@ int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, voi
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "check_rows");
     *n_bad = (int64_t)h;
+    return QLM_OK;
+}
+
+int qlm_adopt_best(qlm_ctx *ctx, const qlm_candidates *cand, const qlm_record *rec,
+                   qlm_record *incumbent, void *stream) {
+    if (!ctx || !rec || !incumbent) return fail(QLM_EINVAL, "ctx, rec or incumbent is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (cand->kind != QLM_CAND_NEIGHBOR) return fail(QLM_EINVAL, "qlm_adopt_best needs NEIGHBOR candidates");
+    cudaError_t e = launch_adopt(ctx->dm, to_cand(cand), rec, incumbent, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "adopt kernel");
+}
+
+int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves, int64_t per_iter,
+                     int32_t iters, uint64_t seed, qlm_record *incumbent, void *stream) {
+    if (!ctx || !row || !incumbent) return fail(QLM_EINVAL, "ctx, row or incumbent is NULL");
+    if (moves < 1 || moves > QLM_MAX_MOVES)
+        return fail(QLM_EINVAL, "moves=%d must lie in [1, %d]", moves, QLM_MAX_MOVES);
+    if (per_iter < 1) return fail(QLM_EINVAL, "per_iter=%lld < 1", (long long)per_iter);
+    if (iters < 0) return fail(QLM_EINVAL, "iters=%d < 0", iters);
+    if (iters > 0 && per_iter > INT64_MAX / iters) return fail(QLM_ERANGE, "iters * per_iter overflows");
+    int rc = check_dev(ctx);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int T = ctx->dm.T;
+    // score the start row (EXPLICIT, one candidate) into the incumbent record
+    qlm_candidates ex;
+    memset(&ex, 0, sizeof ex);
+    ex.kind = QLM_CAND_EXPLICIT;
+    ex.token_bytes = token_bytes;
+    ex.rows = row;
+    ex.stride = (((int64_t)T * token_bytes) + 15) / 16 * 16;
+    ex.count = 1;
+    if ((rc = check_cand(ctx, &ex))) return rc;
+    ScanParams p0 = base_params(ctx, &ex);
+    p0.out_rec = incumbent;
+    cudaError_t e = launch_any_scan(p0, st);
+    if (e == cudaSuccess)             // index -1: the start row is the incumbent
+        e = cudaMemsetAsync(&incumbent->index, 0xFF, sizeof(int64_t), st);
+    if (e != cudaSuccess) return cuda_fail(e, "local search: start row");
+    qlm_candidates nb = ex;
+    nb.kind = QLM_CAND_NEIGHBOR;
+    nb.stride = 0;
+    nb.seed = seed;
+    nb.moves = moves;
+    nb.count = per_iter;
+    for (int32_t it = 0; it < iters; ++it) {
+        nb.first = (int64_t)it * per_iter;
+        if ((rc = check_cand(ctx, &nb))) return rc;
+        ScanParams p = base_params(ctx, &nb);
+        p.out_rec = ctx->d_ls_rec;
+        if ((e = launch_any_scan(p, st)) != cudaSuccess) return cuda_fail(e, "local search: scores");
+        if ((e = launch_adopt(ctx->dm, to_cand(&nb), ctx->d_ls_rec, incumbent, st)) != cudaSuccess)
+            return cuda_fail(e, "local search: adopt");
+    }
     return QLM_OK;
 }
 

@@ -48,6 +48,7 @@ struct Cand {               // device view of qlm_candidates
     uint64_t seed;
     int64_t first, count;
     const qlm_record *first_from;
+    int moves;              // NEIGHBOR: transpositions per candidate (R18)
 };
 
 // ---- Philox4x32-10 (Salmon et al. SC'11) ------------------------------------
@@ -70,6 +71,8 @@ __device__ __forceinline__ uint32_t pick4(uint4 w, int k) {
 constexpr uint32_t kRowTag = 0x514C4D00u;
 // MC stream (R13): key = mc_seed, counter = (r/4, group, trial, 'MC\0\0').
 constexpr uint32_t kMcTag = 0x4D430000u;
+// NEIGHBOR stream (R18): key = seed, counter = (m/2, c_lo, c_hi, 'NBHR').
+constexpr uint32_t kNbrTag = 0x4E424852u;
 
 // ---- per-thread Fisher-Yates scratch in shared memory ----------------------
 // Element i of thread `tid` lives in 32-bit word (i / EPW) * blk + tid, byte
@@ -178,6 +181,66 @@ __device__ __forceinline__ void tokens_scratch(const uint8_t *scratch, int blk, 
             if (s0 + k >= T) break;
             f(EPW == 4 ? (int)((w >> (8 * k)) & 0xFFu) : (int)((w >> (16 * k)) & 0xFFFFu));
         }
+    }
+}
+
+// ---- NEIGHBOR rows (R18): base row with k Philox-drawn transpositions -------
+// Move m of candidate c swaps positions (i_m, j_m) = (mulhi(u0, T), mulhi(u1, T)),
+// (u0, u1) = words 2(m%2), 2(m%2)+1 of Philox(key = seed, ctr = (m/2, c, 'NBHR')).
+__device__ __forceinline__ void nbr_moves(const Cand &cd, int T, uint64_t c, int *mi, int *mj) {
+    const uint2 key = make_uint2((uint32_t)cd.seed, (uint32_t)(cd.seed >> 32));
+    uint4 wd = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int m = 0; m < QLM_MAX_MOVES; ++m) {
+        if (m >= cd.moves) break;
+        if ((m & 1) == 0) wd = philox10(make_uint4((uint32_t)(m >> 1), (uint32_t)c, (uint32_t)(c >> 32), kNbrTag), key);
+        mi[m] = (int)__umulhi((m & 1) ? wd.z : wd.x, (uint32_t)T);
+        mj[m] = (int)__umulhi((m & 1) ? wd.w : wd.y, (uint32_t)T);
+    }
+}
+
+template <typename TOK>
+__device__ __forceinline__ int base_token(const Cand &cd, int p) {
+    return (int)__ldg(reinterpret_cast<const TOK *>(cd.rows) + p);
+}
+
+// Streaming generator for one thread: the row differs from the base row in at
+// most 2k positions; they are resolved once (apply the k swaps to the touched
+// positions only) and sorted, then the row streams from the base row (all
+// lanes read the same position: a broadcast) with the touched values spliced
+// in.  No per-thread row scratch, so any T runs at full occupancy.
+template <typename TOK, typename F>
+__device__ __forceinline__ void tokens_neighbor(const Cand &cd, int T, uint64_t c, F &&f) {
+    int mi[QLM_MAX_MOVES], mj[QLM_MAX_MOVES];
+    nbr_moves(cd, T, c, mi, mj);
+    int P[2 * QLM_MAX_MOVES], V[2 * QLM_MAX_MOVES];
+    int n = 0;
+    auto slot = [&](int pos) {
+        for (int x = 0; x < n; ++x)
+            if (P[x] == pos) return x;
+        P[n] = pos;
+        V[n] = base_token<TOK>(cd, pos);
+        return n++;
+    };
+    for (int m = 0; m < cd.moves; ++m) {
+        const int xi = slot(mi[m]), xj = slot(mj[m]);
+        const int t = V[xi]; V[xi] = V[xj]; V[xj] = t;
+    }
+    for (int a = 1; a < n; ++a) {                       // insertion sort by position
+        const int pa = P[a], va = V[a];
+        int b = a - 1;
+        while (b >= 0 && P[b] > pa) { P[b + 1] = P[b]; V[b + 1] = V[b]; --b; }
+        P[b + 1] = pa; V[b + 1] = va;
+    }
+    int idx = 0, nextp = n > 0 ? P[0] : T;
+    for (int pos = 0; pos < T; ++pos) {
+        int tok = base_token<TOK>(cd, pos);
+        if (pos == nextp) {
+            tok = V[idx];
+            ++idx;
+            nextp = idx < n ? P[idx] : T;
+        }
+        f(tok);
     }
 }
 

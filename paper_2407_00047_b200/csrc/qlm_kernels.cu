@@ -101,6 +101,8 @@ __device__ __forceinline__ void for_tokens(const Cand &cd, int T, uint8_t *scrat
         tokens_scratch<TOK>(scratch, blk, threadIdx.x, T, f);
     } else if constexpr (KIND == QLM_CAND_EXPLICIT) {
         tokens_explicit<TOK>(cd.rows + loc * cd.stride, T, f);
+    } else if constexpr (KIND == QLM_CAND_NEIGHBOR) {
+        tokens_neighbor<TOK>(cd, T, (uint64_t)c, f);
     } else if constexpr (KIND == KIND_ILV) {
         // word-interleaved rows: consecutive candidates read consecutive words
         constexpr int EPW = 4 / (int)sizeof(TOK);
@@ -511,6 +513,19 @@ __device__ __forceinline__ void warp_gen_row(const Cand &cd, int T, uint64_t c, 
             int s = 0;
             tokens_enum(c, T, [&](int tok) { srow[s++] = (uint16_t)tok; });
         }
+    } else if (cd.kind == QLM_CAND_NEIGHBOR) {
+        for (int s = lane; s < T; s += 32)
+            srow[s] = cd.tb == 1 ? (uint16_t)base_token<uint8_t>(cd, s) : (uint16_t)base_token<uint16_t>(cd, s);
+        __syncwarp();
+        if (lane == 0) {
+            int mi[QLM_MAX_MOVES], mj[QLM_MAX_MOVES];
+            nbr_moves(cd, T, c, mi, mj);
+            for (int m = 0; m < cd.moves; ++m) {
+                const uint16_t t = srow[mi[m]];
+                srow[mi[m]] = srow[mj[m]];
+                srow[mj[m]] = t;
+            }
+        }
     } else {
         const uint8_t *row = cd.rows + loc * cd.stride;
         for (int s = lane; s < T; s += 32)
@@ -566,6 +581,35 @@ __global__ void __launch_bounds__(32) row_warp_kernel(const ScanParams p, uint16
             if (queue_of) queue_of[loc * G + tok] = q;
             if (pos_of) pos_of[loc * G + tok] = pos;
         });
+}
+
+// Local-search step (R18): adopt the winning NEIGHBOR candidate if its key
+// beats the incumbent's.  One block; the base row is rewritten in place.
+__global__ void __launch_bounds__(256) adopt_kernel(Dims dm, Cand cd, const qlm_record *rec,
+                                                    qlm_record *inc) {
+    extern __shared__ __align__(16) uint16_t arow[];
+    const qlm_record r = *rec, cur = *inc;
+    if (r.index < 0 || r.key >= cur.key) return;                 // uniform: keep the incumbent
+    const int T = dm.T;
+    for (int s = threadIdx.x; s < T; s += blockDim.x)
+        arow[s] = cd.tb == 1 ? (uint16_t)base_token<uint8_t>(cd, s) : (uint16_t)base_token<uint16_t>(cd, s);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int mi[QLM_MAX_MOVES], mj[QLM_MAX_MOVES];
+        nbr_moves(cd, T, (uint64_t)r.index, mi, mj);
+        for (int m = 0; m < cd.moves; ++m) {
+            const uint16_t t = arow[mi[m]];
+            arow[mi[m]] = arow[mj[m]];
+            arow[mj[m]] = t;
+        }
+    }
+    __syncthreads();
+    uint8_t *rows = const_cast<uint8_t *>(cd.rows);
+    for (int s = threadIdx.x; s < T; s += blockDim.x) {
+        if (cd.tb == 1) rows[s] = (uint8_t)arow[s];
+        else reinterpret_cast<uint16_t *>(rows)[s] = arow[s];
+    }
+    if (threadIdx.x == 0) *inc = r;
 }
 
 // =============================================================================
@@ -955,7 +999,8 @@ cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st) {
     cudaError_t e = launch_ws(p, st);
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();
-    if (p.cd.kind == QLM_CAND_EXPLICIT && p.cd.tb == 2 && wide_first(p)) {
+    if ((p.cd.kind == QLM_CAND_EXPLICIT || p.cd.kind == QLM_CAND_NEIGHBOR) && p.cd.tb == 2 &&
+        wide_first(p)) {
         e = launch_wide(p, st);
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();
@@ -974,6 +1019,9 @@ cudaError_t launch_scan(ScanParams p, cudaStream_t st) {
     case QLM_CAND_EXPLICIT:
         return p.cd.tb == 1 ? launch_scan_k<QLM_CAND_EXPLICIT, uint8_t>(p, st)
                             : launch_scan_k<QLM_CAND_EXPLICIT, uint16_t>(p, st);
+    case QLM_CAND_NEIGHBOR:
+        return p.cd.tb == 1 ? launch_scan_k<QLM_CAND_NEIGHBOR, uint8_t>(p, st)
+                            : launch_scan_k<QLM_CAND_NEIGHBOR, uint16_t>(p, st);
     default:
         return launch_scan_k<QLM_CAND_ENUM, uint8_t>(p, st);
     }
@@ -1022,9 +1070,22 @@ cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_
     case QLM_CAND_EXPLICIT:
         return p.cd.tb == 1 ? launch_rows_t<QLM_CAND_EXPLICIT, uint8_t>(p, rows, qo, po, st)
                             : launch_rows_t<QLM_CAND_EXPLICIT, uint16_t>(p, rows, qo, po, st);
+    case QLM_CAND_NEIGHBOR:
+        return p.cd.tb == 1 ? launch_rows_t<QLM_CAND_NEIGHBOR, uint8_t>(p, rows, qo, po, st)
+                            : launch_rows_t<QLM_CAND_NEIGHBOR, uint16_t>(p, rows, qo, po, st);
     default:
         return launch_rows_t<QLM_CAND_ENUM, uint8_t>(p, rows, qo, po, st);
     }
+}
+
+cudaError_t launch_adopt(const Dims &dm, const Cand &cd, const qlm_record *rec, qlm_record *inc,
+                         cudaStream_t st) {
+    const size_t smem = (size_t)((dm.T + 7) & ~7) * 2;
+    cudaError_t e = prep(adopt_kernel, smem);
+    if (e != cudaSuccess) return e;
+    adopt_kernel<<<1, 256, smem, st>>>(dm, cd, rec, inc);
+    ++g_launches;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_reduce_records(const qlm_record *recs, int n, qlm_record *out,

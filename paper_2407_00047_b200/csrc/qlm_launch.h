@@ -33,7 +33,7 @@ struct ScanParams {
 
 // Internal candidate kind: rows materialised word-interleaved by fy_rows_kernel
 // (word w of chunk-local candidate l at rows[(w * stride + l) * 4]).
-constexpr int KIND_ILV = 3;
+constexpr int KIND_ILV = 7;
 
 extern std::atomic<int64_t> g_launches;
 int sm_count();
@@ -46,6 +46,8 @@ cudaError_t launch_scan(ScanParams p, cudaStream_t st);
 cudaError_t launch_ws(ScanParams p, cudaStream_t st);      // warp-specialised fast path
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st);   // ws, else scan
 cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per candidate (large G)
+cudaError_t launch_adopt(const Dims &dm, const Cand &cd, const qlm_record *rec, qlm_record *inc,
+                         cudaStream_t st);                          // local-search step (R18)
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,
                         cudaStream_t st);
 cudaError_t launch_reduce_records(const qlm_record *recs, int n, qlm_record *out,

@@ -62,6 +62,23 @@ __device__ __forceinline__ void wide_stage_rows(const Cand &cd, int T, int64_t c
                 if (i < n) s32[k * ldw + w] = v[u];
             }
         }
+    } else if constexpr (KIND == QLM_CAND_NEIGHBOR) {    // base row (u16) + k swaps per row
+        const uint32_t *b32 = reinterpret_cast<const uint32_t *>(cd.rows);
+        for (int i = threadIdx.x; i < nw * kWideCands; i += blockDim.x) {
+            const int k = i / nw, w = i - k * nw;
+            s32[k * ldw + w] = __ldg(b32 + w);
+        }
+        __syncthreads();
+        if (threadIdx.x < nv) {
+            uint16_t *r = srow + threadIdx.x * ldr;
+            int mi[QLM_MAX_MOVES], mj[QLM_MAX_MOVES];
+            nbr_moves(cd, T, (uint64_t)(cd.first + c0 + threadIdx.x), mi, mj);
+            for (int m = 0; m < cd.moves; ++m) {
+                const uint16_t t = r[mi[m]];
+                r[mi[m]] = r[mj[m]];
+                r[mj[m]] = t;
+            }
+        }
     } else {                                   // EXPLICIT u16: row-major, 4-B words
         for (int i = threadIdx.x; i < nw * kWideCands; i += blockDim.x) {
             const int k = i / nw, w = i - k * nw;
@@ -300,9 +317,12 @@ cudaError_t launch_wide(const ScanParams &p, cudaStream_t st) {
     if (p.cd.first_from || p.cd.count < 1) return cudaErrorNotSupported;
     const bool ilv = p.cd.kind == KIND_ILV;
     const bool ex16 = p.cd.kind == QLM_CAND_EXPLICIT && p.cd.tb == 2;
-    if (!ilv && !ex16) return cudaErrorNotSupported;
+    const bool nb16 = p.cd.kind == QLM_CAND_NEIGHBOR && p.cd.tb == 2;
+    if (!ilv && !ex16 && !nb16) return cudaErrorNotSupported;
     const bool score = p.s1 || p.s2 || p.n_over || p.out_rec;
     if (ilv) return score ? launch_wide_t<KIND_ILV, true>(p, st) : launch_wide_t<KIND_ILV, false>(p, st);
+    if (nb16)
+        return score ? launch_wide_t<QLM_CAND_NEIGHBOR, true>(p, st) : launch_wide_t<QLM_CAND_NEIGHBOR, false>(p, st);
     return score ? launch_wide_t<QLM_CAND_EXPLICIT, true>(p, st) : launch_wide_t<QLM_CAND_EXPLICIT, false>(p, st);
 }
 

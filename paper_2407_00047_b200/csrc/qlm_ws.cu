@@ -87,6 +87,27 @@ __device__ __forceinline__ void produce_row(const Cand &cd, int T, uint8_t *slot
     } else if constexpr (KIND == QLM_CAND_ENUM) {
         int s = 0;
         tokens_enum((uint64_t)c, T, [&](int tok) { *fy_elem<TOK>(slot, s++, 32, lane) = (TOK)tok; });
+    } else if constexpr (KIND == QLM_CAND_NEIGHBOR) {
+        // base row words (every lane reads the same word: a broadcast), then
+        // the candidate's k transpositions in the lane's column (R18)
+        constexpr int EPW = 4 / (int)sizeof(TOK);
+        const uint32_t *b32 = reinterpret_cast<const uint32_t *>(cd.rows);
+        uint32_t *w32 = reinterpret_cast<uint32_t *>(slot);
+        if (cd.tb == (int)sizeof(TOK)) {
+            for (int w = 0; w < (T + EPW - 1) / EPW; ++w) w32[w * 32 + lane] = __ldg(b32 + w);
+        } else {
+            for (int i = 0; i < T; ++i)
+                *fy_elem<TOK>(slot, i, 32, lane) =
+                    (TOK)(cd.tb == 1 ? base_token<uint8_t>(cd, i) : base_token<uint16_t>(cd, i));
+        }
+        int mi[QLM_MAX_MOVES], mj[QLM_MAX_MOVES];
+        nbr_moves(cd, T, (uint64_t)c, mi, mj);
+        for (int m = 0; m < cd.moves; ++m) {
+            TOK *pi = fy_elem<TOK>(slot, mi[m], 32, lane), *pj = fy_elem<TOK>(slot, mj[m], 32, lane);
+            const TOK t = *pi;
+            *pi = *pj;
+            *pj = t;
+        }
     } else {
         int s = 0;
         const uint8_t *row = cd.rows + loc * cd.stride;
@@ -561,6 +582,9 @@ cudaError_t launch_ws(ScanParams p, cudaStream_t st) {
     case QLM_CAND_EXPLICIT:
         return p.dm.T <= 256 ? launch_ws_k<QLM_CAND_EXPLICIT, uint8_t>(p, st)
                              : launch_ws_k<QLM_CAND_EXPLICIT, uint16_t>(p, st);
+    case QLM_CAND_NEIGHBOR:
+        return p.dm.T <= 256 ? launch_ws_k<QLM_CAND_NEIGHBOR, uint8_t>(p, st)
+                             : launch_ws_k<QLM_CAND_NEIGHBOR, uint16_t>(p, st);
     default:
         return launch_ws_k<QLM_CAND_ENUM, uint8_t>(p, st);
     }

@@ -31,7 +31,9 @@ class Cand:
     count: int = 0
     seed: int = 0
     rows: torch.Tensor | None = None        # EXPLICIT: uint8/int16 device [count, stride]
+                                            # NEIGHBOR: the base row, uint8/int16 device [>= T]
     first_from: torch.Tensor | None = None  # device record (int64[2]); count must be 1
+    moves: int = 0                          # NEIGHBOR: transpositions per candidate (R18)
 
     def c(self) -> L.Candidates:
         tb, stride, rows = 1, 0, None
@@ -40,8 +42,12 @@ class Cand:
             tb = r.element_size()
             stride = r.stride(0) * tb
             rows = r.data_ptr()
+        elif self.kind == L.CAND_NEIGHBOR:
+            tb = self.rows.element_size()
+            rows = self.rows.data_ptr()
         ff = None if self.first_from is None else self.first_from.data_ptr()
-        return L.Candidates(self.kind, tb, rows, stride, self.seed, self.first, self.count, ff)
+        return L.Candidates(self.kind, tb, rows, stride, self.seed, self.first, self.count, ff,
+                            self.moves, 0)
 
 
 def groups_array(model, n_req, slo, mu, var, dist=None) -> np.ndarray:
@@ -120,6 +126,38 @@ class RwtEstimator:
     def explicit(self, rows: torch.Tensor, first: int = 0) -> Cand:
         """rows: device uint8 (T <= 256) or int16 tensor [count, >= T], row stride a multiple of 16 B."""
         return Cand(L.CAND_EXPLICIT, first, rows.shape[0], rows=rows)
+
+    def neighbor(self, base: torch.Tensor, first: int, count: int, seed: int, moves: int) -> Cand:
+        """NEIGHBOR candidates (R18): `base` with `moves` Philox-drawn transpositions each.
+        base: device uint8 (T <= 256) / int16 tensor of >= T tokens, 16-B aligned, padded
+        to a multiple of 16 B (see row_buffer)."""
+        return Cand(L.CAND_NEIGHBOR, first, count, seed, rows=base, moves=moves)
+
+    def row_buffer(self, row, token_bytes: int | None = None) -> torch.Tensor:
+        """A device row in the layout NEIGHBOR / qlm_local_search expect (padded to 16 B)."""
+        tb = token_bytes or (1 if self.T <= 256 else 2)
+        n = -(-self.T * tb // 16) * 16 // tb
+        buf = torch.zeros(n, dtype=torch.uint8 if tb == 1 else torch.int16, device=self.device)
+        r = torch.as_tensor(np.asarray(row, np.int64))
+        buf[: self.T] = r.to(buf.dtype).to(self.device)
+        return buf
+
+    def adopt_best(self, cand: Cand, rec: torch.Tensor, incumbent: torch.Tensor, stream=None):
+        """Device-side local-search step: cand.rows <- winner row if rec beats incumbent."""
+        L.check(L.lib().qlm_adopt_best(self._h, C.byref(cand.c()), rec.data_ptr(), incumbent.data_ptr(),
+                                       self._stream(stream)), "qlm_adopt_best")
+
+    def local_search(self, row, moves: int = 2, per_iter: int = 1 << 16, iters: int = 16,
+                     seed: int = 1, stream=None):
+        """Iterated best-of-N over NEIGHBOR candidates (R18), asynchronous on the stream.
+        row: start ordering (host sequence or a row_buffer tensor, updated in place).
+        Returns (row buffer, incumbent record int64[2] = (key bits, adopted index))."""
+        buf = row if isinstance(row, torch.Tensor) else self.row_buffer(row)
+        inc = self._empty(2, torch.int64)
+        L.check(L.lib().qlm_local_search(self._h, C.c_void_p(buf.data_ptr()), buf.element_size(), moves,
+                                         per_iter, iters, seed, C.c_void_p(inc.data_ptr()),
+                                         self._stream(stream)), "qlm_local_search")
+        return buf, inc
 
     def from_record(self, rec: torch.Tensor, kind: int = L.CAND_RANDOM, seed: int = 0) -> Cand:
         """The single candidate named by a device record (no host sync)."""

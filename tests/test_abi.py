@@ -57,9 +57,9 @@ int main(void) {
   printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(qlm_group), sizeof(qlm_queue),
          sizeof(qlm_profile), sizeof(qlm_len_tables), sizeof(qlm_options), sizeof(qlm_record),
          sizeof(qlm_candidates), sizeof(qlm_best));
-  printf("%zu %zu %zu %zu %zu\n", offsetof(qlm_group, slo_s), offsetof(qlm_group, dist_id),
+  printf("%zu %zu %zu %zu %zu %zu\n", offsetof(qlm_group, slo_s), offsetof(qlm_group, dist_id),
          offsetof(qlm_queue, backlog_mean_s), offsetof(qlm_candidates, first_from),
-         offsetof(qlm_candidates, seed));
+         offsetof(qlm_candidates, seed), offsetof(qlm_candidates, moves));
   return 0;
 }''')
     exe = tmp_path / "probe"
@@ -72,7 +72,7 @@ int main(void) {
     offs = [int(x) for x in b.split()]
     assert offs == [L.GROUP_DTYPE.fields["slo_s"][1], L.GROUP_DTYPE.fields["dist_id"][1],
                     L.QUEUE_DTYPE.fields["backlog_mean_s"][1], L.Candidates.first_from.offset,
-                    L.Candidates.seed.offset]
+                    L.Candidates.seed.offset, L.Candidates.moves.offset]
 
 
 def _create(lib, groups, queues, D=1, M=1, theta=1000.0, swap_diag=0.0, K=None, opt=None):
@@ -152,5 +152,7 @@ def test_null_context_calls_fail_cleanly(lib):
     assert lib.qlm_score_orderings(None, C.byref(cand), None, None, None, None) == L.QLM_EINVAL
     assert lib.qlm_rwt_estimate(None, C.byref(cand), None, None, None, None) == L.QLM_EINVAL
     assert lib.qlm_dims(None, None, None, None, None, None) == L.QLM_EINVAL
+    assert lib.qlm_adopt_best(None, C.byref(cand), None, None, None) == L.QLM_EINVAL
+    assert lib.qlm_local_search(None, None, 1, 2, 64, 1, 1, None, None) == L.QLM_EINVAL
     lib.qlm_destroy(None)
-    assert lib.qlm_abi_version() == 1
+    assert lib.qlm_abi_version() == 2

@@ -485,3 +485,126 @@ def test_wide_kernel_bulk_large_G(G, Q, D, backlog, n):
     s1 = r["s1"].cpu().numpy()[:4096]
     s2 = r["s2"].cpu().numpy()[:4096]
     check_scores(s1, s2, ref, p)
+
+
+# ------------------------------------------------------- NEIGHBOR candidates / local search (R18)
+@pytest.mark.parametrize("cfg,n", [("C2", 700), ("C3", 3000), ("C5", 300)])
+def test_neighbor_rows_bit_exact(cfg, n):
+    p = make_config(cfg)
+    e = est_of(p)
+    base_np = O.random_row(7, 3, p.T)
+    base = e.row_buffer(base_np)
+    for moves in (1, 3, 8):
+        rows = e.rows(e.neighbor(base, 100, n, seed=11, moves=moves)).cpu().numpy().astype(np.int64)
+        ref = np.stack([O.neighbor_row(base_np, 11, 100 + c, moves) for c in range(n)])
+        assert np.array_equal(rows & 0xFFFF, ref), (cfg, moves)
+
+
+@pytest.mark.parametrize("cfg,n,moves", [("C2", 20_000, 2), ("C3", 9000, 1), ("C3", 5000, 8)])
+def test_neighbor_scores_and_bulk(cfg, n, moves, monkeypatch):
+    """Scores (thread-per-candidate streaming generator) and bulk estimates
+    (warp-specialised producer) of NEIGHBOR candidates vs the oracle, and the
+    two kernels agree bit for bit."""
+    p = make_config(cfg)
+    e = est_of(p)
+    base_np = O.random_row(2, 9, p.T)
+    base = e.row_buffer(base_np)
+    cand = e.neighbor(base, 5, n, seed=3, moves=moves)
+    o = O.Oracle(p)
+    s1, s2, no = e.score_orderings(cand)
+    m = min(n, 2500)
+    ref = o.score_range(O.NEIGHBOR, 5, m, seed=3, rows=base_np, moves=moves)
+    check_scores(s1[:m].cpu().numpy(), s2[:m].cpu().numpy(), ref, p)
+    res = {}
+    for no_ws in ("1", "0"):
+        monkeypatch.setenv("QLM_NO_WS", no_ws)
+        rec = torch.empty(2, dtype=torch.int64, device="cuda")
+        bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+        res[no_ws] = (e.score_estimate(cand, out=bufs, rec=rec), rec)
+    (a, ra), (b, rb) = res["1"], res["0"]
+    for k in ("wt", "sd", "v", "s1", "s2"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(ra, rb)
+    est = o.estimate_range(O.NEIGHBOR, 5, 400, seed=3, rows=base_np, moves=moves)
+    check_estimates({k: b[k][:, :400] for k in ("wt", "sd", "v")}, est)
+    assert torch.equal(b["s1"], s1) and torch.equal(b["s2"], s2)
+
+
+def test_neighbor_bulk_large_G():
+    p = make_config("C5")
+    e = est_of(p)
+    base_np = O.random_row(2, 9, p.T)
+    cand = e.neighbor(e.row_buffer(base_np), 0, 4100, seed=3, moves=4)
+    bufs = {k: torch.empty((p.G, 4100), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+    r = e.score_estimate(cand, out=bufs)
+    o = O.Oracle(p)
+    est = o.estimate_range(O.NEIGHBOR, 0, 40, seed=3, rows=base_np, moves=4)
+    check_estimates({k: r[k][:, :40] for k in ("wt", "sd", "v")}, est)
+    ref = o.score_range(O.NEIGHBOR, 0, 300, seed=3, rows=base_np, moves=4)
+    check_scores(r["s1"][:300].cpu().numpy(), r["s2"][:300].cpu().numpy(), ref, p)
+
+
+def test_adopt_best_updates_only_on_improvement():
+    p = make_config("C3")
+    e = est_of(p)
+    base_np = O.random_row(4, 4, p.T)
+    base = e.row_buffer(base_np)
+    cand = e.neighbor(base, 0, 4096, seed=8, moves=2)
+    rec = e.best_ordering_async(cand)
+    worse = torch.tensor([-1, 0], dtype=torch.int64, device="cuda")        # key 0xFFFF...: everything beats it
+    better = torch.tensor([0, 0], dtype=torch.int64, device="cuda")        # key 0: nothing beats it
+    e.adopt_best(cand, rec, better)
+    assert np.array_equal(base.cpu().numpy()[: p.T], base_np)
+    assert better.cpu().numpy().tolist() == [0, 0]
+    e.adopt_best(cand, rec, worse)
+    idx = int(rec.cpu().numpy()[1])
+    assert np.array_equal(base.cpu().numpy()[: p.T].astype(np.int64), O.neighbor_row(base_np, 8, idx, 2))
+    assert torch.equal(worse, rec)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_local_search_matches_oracle(seed):
+    """qlm_local_search (all iterations asynchronous on the device) follows the
+    oracle's iterated best-of-N (oracle.local_search) on small instances, and
+    reaches the brute-force optimum there."""
+    rng = np.random.default_rng(300 + seed)
+    G, Q = int(rng.integers(4, 7)), int(rng.integers(1, 3))
+    p = make_random_problem(rng, G, Q, 2, 1, backlog=bool(seed % 2))
+    e = est_of(p)
+    o = O.Oracle(p)
+    row_o, key_o, _ = O.local_search(o, np.arange(p.T), seed=seed + 1, moves=2, per_iter=48, iters=40)
+    buf, inc = e.local_search(np.arange(p.T), moves=2, per_iter=48, iters=40, seed=seed + 1)
+    row_g = buf.cpu().numpy()[: p.T].astype(np.int64)
+    s1, s2, _ = o.score(row_g)
+    assert O.key32(s1, s2) == key_o, (row_g, row_o)
+    r = o.score_range(O.ENUM, 0, math.factorial(p.T))
+    best = O.key32(*min(zip(r["s1"], r["s2"]), key=lambda x: O.key32(*x)))
+    assert O.key32(s1, s2) == best
+
+
+def test_local_search_improves_c3():
+    p = make_config("C3")
+    e = est_of(p)
+    o = O.Oracle(p)
+    start = O.random_row(1, 0, p.T)
+    k0 = O.key32(*o.score(start)[:2])
+    buf, inc = e.local_search(start, moves=2, per_iter=1 << 14, iters=12, seed=5)
+    row = buf.cpu().numpy()[: p.T].astype(np.int64)
+    assert sorted(row) == list(range(p.T))
+    k1 = O.key32(*o.score(row)[:2])
+    assert k1 <= k0
+    rec = inc.cpu().numpy()
+    assert rec[1] >= 0                          # something was adopted
+    dev_s1 = np.frombuffer(np.uint32(np.uint64(rec[0]) >> np.uint64(32)).tobytes(), np.float32)[0]
+    assert abs(dev_s1 - o.score(row)[0]) <= 1e-5
+
+
+def test_neighbor_validation_messages():
+    p = make_config("C2")
+    e = est_of(p)
+    base = e.row_buffer(np.arange(p.T))
+    from paper_2407_00047_b200 import _lib as L
+    with pytest.raises(RuntimeError, match="cand.moves=9"):
+        e.score_orderings(e.neighbor(base, 0, 10, seed=1, moves=9))
+    with pytest.raises(RuntimeError, match="moves=0"):
+        e.local_search(np.arange(p.T), moves=0)
