@@ -266,6 +266,33 @@ def balanced_row(G: int, Q: int) -> np.ndarray:
     return np.asarray(toks, dtype=dt)
 
 
+def queue_row(order, G: int, Q: int, queue_of=None) -> np.ndarray:
+    """Token row from a group order: group order[k] goes to queue queue_of[k]
+    (default k mod Q), keeping the order within each queue."""
+    qs = [[] for _ in range(Q)]
+    for k, g in enumerate(order):
+        qs[(k % Q) if queue_of is None else int(queue_of[k])].append(int(g))
+    toks = []
+    for q in range(Q):
+        toks.extend(qs[q])
+        if q < Q - 1:
+            toks.append(G + q)
+    T = G + Q - 1
+    return np.asarray(toks, dtype=np.uint8 if T <= 256 else np.uint16)
+
+
+def fcfs_row(p: "Problem") -> np.ndarray:
+    """Comparator: groups in arrival (index) order, dealt round-robin over the
+    queues (FCFS baseline of P:L790-791)."""
+    return queue_row(range(p.G), p.G, p.Q)
+
+
+def edf_row(p: "Problem") -> np.ndarray:
+    """Comparator: earliest deadline (SLO) first, dealt round-robin over the
+    queues (EDF baseline of P:L790-791)."""
+    return queue_row(np.argsort(p.slo, kind="stable"), p.G, p.Q)
+
+
 # name -> (problem factory, candidate kind, candidate count / trials)
 CONFIGS = {
     "C1": dict(desc="4 groups, 1 model, 1 queue: all 24 orderings (ENUM)",
