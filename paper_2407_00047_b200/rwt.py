@@ -159,9 +159,11 @@ class RwtEstimator:
                                          self._stream(stream)), "qlm_local_search")
         return buf, inc
 
-    def from_record(self, rec: torch.Tensor, kind: int = L.CAND_RANDOM, seed: int = 0) -> Cand:
-        """The single candidate named by a device record (no host sync)."""
-        return Cand(kind, 0, 1, seed, first_from=rec)
+    def from_record(self, rec: torch.Tensor, kind: int = L.CAND_RANDOM, seed: int = 0,
+                    base: torch.Tensor | None = None, moves: int = 0) -> Cand:
+        """The single candidate named by a device record (no host sync); NEIGHBOR
+        records also need the base row and the number of moves."""
+        return Cand(kind, 0, 1, seed, rows=base, first_from=rec, moves=moves)
 
     # -- hot path -------------------------------------------------------------
     def update_groups(self, groups: np.ndarray | torch.Tensor, stream=None):

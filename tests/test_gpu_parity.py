@@ -608,3 +608,24 @@ def test_neighbor_validation_messages():
         e.score_orderings(e.neighbor(base, 0, 10, seed=1, moves=9))
     with pytest.raises(RuntimeError, match="moves=0"):
         e.local_search(np.arange(p.T), moves=0)
+
+
+def test_neighbor_decode_and_mc_from_device_record():
+    """The winner of a NEIGHBOR argmin decodes (queue, position) and runs MC
+    straight from the device record, as the RANDOM path does."""
+    p = make_config("C4")
+    e = est_of(p)
+    base_np = balanced_row(p.G, p.Q).astype(np.int64)
+    base = e.row_buffer(base_np)
+    cand = e.neighbor(base, 0, 5000, seed=2, moves=3)
+    rec = e.best_ordering_async(cand)
+    one = e.from_record(rec, kind=3, seed=2, base=base, moves=3)
+    q, pos = e.decode(one)
+    idx = int(rec.cpu().numpy()[1])
+    row = O.neighbor_row(base_np, 2, idx, 3)
+    dec = O.Oracle(p).estimate(row)
+    assert np.array_equal(q.cpu().numpy()[0], dec["queue"]) and np.array_equal(pos.cpu().numpy()[0], dec["pos"])
+    cnt = e.mc_estimate(one, mc_seed=4, trials=200).cpu().numpy().astype(np.uint32)
+    X = O.Oracle(p).mc_sample(4, 0, 200)
+    ref = O.Oracle(p).mc_count(O.EXPLICIT, 0, 1, X, rows=row[None, :].astype(np.uint16))
+    assert np.array_equal(cnt, ref)
