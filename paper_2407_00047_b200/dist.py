@@ -51,3 +51,28 @@ def sum_counts(counts: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     return counts
+
+
+def local_search(est, row, moves: int = 2, per_iter: int = 1 << 16, iters: int = 16, seed: int = 1,
+                 group=None):
+    """Sharded iterated best-of-N over NEIGHBOR candidates (DESIGN R18).
+
+    Iteration it's candidates [it*per_iter, (it+1)*per_iter) are split over
+    the ranks with shard_range; each rank scores its slice, the iteration's
+    winner is the global min-loc (global_best: one 16-B all-gather + reduce),
+    and every rank adopts it with the same device-side rule, so the
+    incumbent row stays identical on all ranks.  Equal to est.local_search on
+    one rank.  Returns (row buffer, incumbent record).
+    """
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, n = shard_range(per_iter, rank, world)
+    buf = est.row_buffer(row)
+    inc = est.best_ordering_async(est.explicit(buf.view(1, -1)))
+    inc[1:].fill_(-1)                                 # index -1: the start row is the incumbent
+    for it in range(iters):
+        cand = est.neighbor(buf, it * per_iter + lo, n, seed, moves)
+        rec = est.best_ordering_async(cand)
+        best = global_best(rec, est.reduce_records, group)
+        est.adopt_best(cand, best, inc)
+    return buf, inc

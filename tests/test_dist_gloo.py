@@ -121,3 +121,77 @@ def test_two_rank_gloo_global_argmin_and_mc_sum():
     ref = o4.mc_count(O.EXPLICIT, 0, 1, o4.mc_sample(2, 0, 60), rows=row)
     for _, _, cnt in res:
         np.testing.assert_array_equal(cnt, ref.astype(np.int64))
+
+
+# ------------------------------------------------- sharded local search (R18)
+class OracleEstimator:
+    """CPU stand-in for RwtEstimator in the plumbing test: the same method
+    names dist.local_search calls, each computed with the oracle."""
+
+    def __init__(self, p):
+        self.p, self.o, self.T = p, O.Oracle(p), p.T
+
+    def row_buffer(self, row):
+        return torch.tensor(np.asarray(row, np.int64))
+
+    def explicit(self, rows):
+        return ("explicit", rows)
+
+    def neighbor(self, base, first, count, seed, moves):
+        return ("neighbor", base, first, count, seed, moves)
+
+    def best_ordering_async(self, cand):
+        if cand[0] == "explicit":
+            s1, s2, _ = self.o.score(cand[1][0].numpy())
+            return torch.tensor([to_i64(pack_key(s1, s2)), 0], dtype=torch.int64)
+        _, base, first, count, seed, moves = cand
+        if count == 0:
+            return torch.tensor([-1, -1], dtype=torch.int64)
+        r = self.o.score_range(O.NEIGHBOR, first, count, seed=seed, rows=base.numpy(), moves=moves)
+        i = O.argmin_key(r["s1"], r["s2"])
+        return torch.tensor([to_i64(pack_key(r["s1"][i], r["s2"][i])), first + i], dtype=torch.int64)
+
+    def reduce_records(self, recs):
+        return cpu_reduce(recs)
+
+    def adopt_best(self, cand, rec, inc):
+        _, base, _, _, seed, moves = cand
+        u = lambda v: v & ((1 << 64) - 1)                                     # noqa: E731
+        if rec[1] >= 0 and u(int(rec[0])) < u(int(inc[0])):
+            base[:] = torch.tensor(O.neighbor_row(base.numpy(), seed, int(rec[1]), moves))
+            inc[:] = rec
+
+
+def _search_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2407_00047_b200.dist import local_search
+        p = make_config("C1r")
+        buf, inc = local_search(OracleEstimator(p), np.arange(p.T), moves=2, per_iter=13, iters=12,
+                                seed=5)
+        q.put((rank, buf.tolist(), inc.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharded_local_search():
+    """Each iteration's candidates split over 2 ranks + global min-loc + the
+    same adoption on every rank == the single-process oracle local search."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_search_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = make_config("C1r")
+    row, key, _ = O.local_search(O.Oracle(p), np.arange(p.T), seed=5, moves=2, per_iter=13, iters=12)
+    for _, b, inc in res:
+        assert b == row.tolist()
+        s1, s2, _ = O.Oracle(p).score(np.array(b))
+        assert O.key32(s1, s2) == key

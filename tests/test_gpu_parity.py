@@ -411,6 +411,14 @@ def test_nccl_plumbing_single_rank():
         assert torch.equal(e.reduce_records(g), rec)
         cnt = torch.arange(16, dtype=torch.int32, device="cuda")
         assert torch.equal(sum_counts(cnt.clone()), cnt)
+        # sharded local search (R18) on one rank == the library's own loop
+        from paper_2407_00047_b200.dist import local_search
+        p3 = make_config("C3")
+        e3 = est_of(p3)
+        start = O.random_row(1, 0, p3.T)
+        b1, i1 = local_search(e3, start, moves=2, per_iter=8192, iters=6, seed=3)
+        b2, i2 = e3.local_search(start, moves=2, per_iter=8192, iters=6, seed=3)
+        assert torch.equal(b1, b2) and torch.equal(i1, i2)
     finally:
         dist.destroy_process_group()
 
