@@ -66,6 +66,10 @@ def lib():
         _lib.or_estimate_range.argtypes = [P, C.c_int, vp, i32, i64, u64, u64, i64, dp, dp, dp]
         _lib.or_estimate_range.restype = i64
         _lib.or_mc_sample.argtypes = [P, u64, i64, i64, vp]
+        _lib.or_request_violations_row.argtypes = [P, vp, dp, dp]
+        _lib.or_request_violations_row.restype = C.c_int
+        _lib.or_request_violations_range.argtypes = [P, C.c_int, vp, i32, i64, u64, u64, i64, dp, dp]
+        _lib.or_request_violations_range.restype = i64
         _lib.or_mc_count.argtypes = [P, C.c_int, vp, i32, i64, u64, u64, i64, vp, i64, vp]
         _lib.or_mc_count.restype = i64
     return _lib
@@ -158,6 +162,21 @@ class Oracle:
         bad = lib().or_estimate_range(C.byref(self.p), kind, _ptr(rows), tb, stride, seed, first,
                                       count, _ptr(wt), _ptr(sd), _ptr(v))
         return dict(wt=wt, sd=sd, v=v, bad=bad)
+
+    def request_violations(self, row):
+        """R19: per-group violating fraction over the group's requests, and S1_req."""
+        row = np.ascontiguousarray(row, np.int32)
+        frac, s1 = np.zeros(self.G), C.c_double()
+        if lib().or_request_violations_row(C.byref(self.p), _ptr(row), _ptr(frac), C.byref(s1)) != 0:
+            raise ValueError("row is not a permutation of 0..T-1 (Eq. 6)")
+        return frac, s1.value
+
+    def request_violations_range(self, kind, first, count, seed=0, rows=None, moves=0):
+        rows, tb, stride = self._rows_args(kind, rows, moves)
+        frac, s1 = np.zeros((count, self.G)), np.zeros(count)
+        bad = lib().or_request_violations_range(C.byref(self.p), kind, _ptr(rows), tb, stride, seed,
+                                                first, count, _ptr(frac), _ptr(s1))
+        return dict(frac=frac, s1=s1, bad=bad)
 
     def mc_sample(self, mc_seed, trial_first, trial_count):
         X = np.zeros((trial_count, self.G), np.uint32)

@@ -314,6 +314,40 @@ int64_t or_estimate_range(const or_problem *p, int kind, const void *rows, int32
     return bad;
 }
 
+/* ---- request-level violations (R19) ----------------------
+ * Request r = 0..n_i-1 of group i waits for the group's start plus the r
+ * requests of the group ahead of it (Eq. 2 with q running over requests,
+ * P:L616-619; Eq. 3 for the variance):
+ *   mean_r = wt_i + r * (mu_i / Theta),   var_r = V_i + r * (var_i / Theta^2)
+ * with Theta = Theta[d][m_i] of the group's queue device.  Its violation
+ * probability follows R8/R9 (or_violation); the group's violating fraction
+ * is f_i = (1/n_i) sum_r v_r and the candidate's S1_req = sum n_i f_i / sum n_i. */
+int or_request_violations_row(const or_problem *p, const int32_t *row, double *frac, double *s1)
+{
+    int32_t G = p->G;
+    double *wt = (double *)malloc(sizeof(double) * (size_t)G);
+    double *V = (double *)malloc(sizeof(double) * (size_t)G);
+    int32_t *q = (int32_t *)malloc(sizeof(int32_t) * (size_t)G);
+    int rc = or_estimate_row(p, row, wt, V, q, NULL);
+    if (rc == 0) {
+        double num = 0.0, den = 0.0;
+        for (int32_t i = 0; i < G; ++i) {
+            int32_t d = p->q_device[q[i]];
+            double th = p->theta[d * p->M + p->model[i]];
+            double a = p->mu[i] / th, b = p->var[i] / (th * th);
+            double sum = 0.0;
+            for (int32_t r = 0; r < p->n_req[i]; ++r)
+                sum = sum + or_violation(wt[i] + (double)r * a, V[i] + (double)r * b, p->slo[i], p->z_clamp);
+            frac[i] = sum / (double)p->n_req[i];
+            num = num + (double)p->n_req[i] * frac[i];
+            den = den + (double)p->n_req[i];
+        }
+        *s1 = num / den;
+    }
+    free(wt); free(V); free(q);
+    return rc;
+}
+
 /* ---- Monte-Carlo mode (R13) ----------------------------------------------
  * Output lengths are sampled per request: for trial t, group k, request r,
  *   w    = Philox4x32-10(key = mc_seed, ctr = (r/8, k, t, 0x4D430000))[(r/2) % 4]
@@ -395,6 +429,23 @@ int64_t or_mc_count(const or_problem *p, int kind, const void *rows, int32_t tok
                 prev = m; first_slot = 0;
             }
         }
+    }
+    free(row);
+    return bad;
+}
+
+/* Request-level violations of candidates first..first+count-1: frac
+ * [count][G], s1 [count].  Returns #invalid rows.                           */
+int64_t or_request_violations_range(const or_problem *p, int kind, const void *rows,
+                                    int32_t token_bytes, int64_t stride, uint64_t seed,
+                                    uint64_t first, int64_t count, double *frac, double *s1)
+{
+    int32_t T = p->G + p->Q - 1;
+    int32_t *row = (int32_t *)malloc(sizeof(int32_t) * (size_t)T);
+    int64_t bad = 0;
+    for (int64_t k = 0; k < count; ++k) {
+        get_row(kind, rows, token_bytes, stride, seed, first + (uint64_t)k, k, T, row);
+        if (or_request_violations_row(p, row, frac + k * p->G, &s1[k]) != 0) { s1[k] = NAN; ++bad; }
     }
     free(row);
     return bad;

@@ -465,3 +465,53 @@ def test_local_search_reaches_brute_force_optimum(seed):
     s1, s2, _ = o.score(row)
     assert O.key32(s1, s2) == key
     assert sorted(row) == list(range(T))
+
+
+# ------------------------------------------- request-level violations (R19, N2)
+def test_request_violations_single_request_groups_equal_group_level():
+    # n_i = 1: the only request is the group's first, so f_i = v_i and S1_req = S1.
+    rng = np.random.default_rng(5)
+    p = make_random_problem(rng, 12, 3, 3, 2, backlog=True)
+    p.n_req[:] = 1
+    o = O.Oracle(p)
+    for c in range(20):
+        row = O.random_row(2, c, p.T)
+        e = o.estimate(row)
+        f, s1 = o.request_violations(row)
+        v = np.array([O.violation(e["wt"][i], e["V"][i], p.slo[i]) for i in range(p.G)])
+        assert np.array_equal(f, v)
+        assert s1 == pytest.approx(o.score(row)[0], abs=1e-15)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_request_violations_deterministic_step_count(seed):
+    # sigma = 0: request r violates iff wt + r * mu/Theta > slo, so the fraction
+    # is a closed-form count of the requests past the deadline.
+    rng = np.random.default_rng(40 + seed)
+    G = int(rng.integers(2, 9))
+    n = rng.integers(1, 400, G)
+    mu = rng.uniform(10, 500, G)
+    theta = 1500.0
+    slo = rng.uniform(0.5, 60.0, G)
+    p = hand_problem([0] * G, n, mu, 0.0, slo, theta=theta)
+    o = O.Oracle(p)
+    row = rng.permutation(G)
+    e = o.estimate(row)
+    f, _ = o.request_violations(row)
+    for i in range(G):
+        a = mu[i] / theta
+        ok = (slo[i] - e["wt"][i]) / a          # requests r <= ok meet the SLO
+        met = 0 if ok < 0 else min(n[i], int(np.floor(ok)) + 1)
+        assert f[i] == pytest.approx((n[i] - met) / n[i], abs=1e-12)
+
+
+def test_request_violations_bounds():
+    p = make_config("C3")
+    o = O.Oracle(p)
+    for c in range(10):
+        row = O.random_row(1, c, p.T)
+        e = o.estimate(row)
+        f, s1r = o.request_violations(row)
+        v = np.array([O.violation(e["wt"][i], e["V"][i], p.slo[i]) for i in range(p.G)])
+        assert np.all(f >= v - 1e-15) and np.all(f <= 1.0)     # later requests wait longer
+        assert s1r >= o.score(row)[0] - 1e-15
