@@ -186,6 +186,16 @@ QLM_API int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, 
 QLM_API int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
                       int32_t *queue_of_group, int32_t *pos_of_group, void *stream);
 
+/* Request-level violating fractions (R19), asynchronous:
+ * request r of group i waits wt_i + r*mu_i/Theta (variance V_i +
+ * r*var_i/Theta^2); frac[g][k] = the fraction of group g's requests whose
+ * SLO is violated in candidate first + k (mean of the per-request R8/R9
+ * probabilities), device fp32 [G][count]; s1_req[k] = sum n_i f_i / sum n_i,
+ * device fp32 [count].  Both nullable.  One warp per candidate, O(sum n_i)
+ * work per candidate: meant for evaluating winners and short lists.        */
+QLM_API int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac,
+                           float *s1_req, void *stream);
+
 /* Local-search step (R18), asynchronous on `stream`:
  * if *rec (e.g. from qlm_best_ordering_async over NEIGHBOR candidates of
  * base row cand->rows) has index >= 0 and a key strictly below

@@ -79,6 +79,7 @@ SIGNATURES = {
     "qlm_dims": (C.c_int, [_vp] + [C.POINTER(C.c_int32)] * 5),
     "qlm_kernel_launches": (C.c_int64, []),
     "qlm_adopt_best": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp]),
+    "qlm_request_violations": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp]),
     "qlm_local_search": (C.c_int, [_vp, _vp, _i32, _i32, _i64, _i32, _u64, _vp, _vp]),
     "qlm_abi_version": (C.c_int, []),
 }

@@ -692,4 +692,15 @@ int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves
     return QLM_OK;
 }
 
+int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac, float *s1_req,
+                           void *stream) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (cand->count == 0 || (!frac && !s1_req)) return QLM_OK;
+    ScanParams p = base_params(ctx, cand);
+    cudaError_t e = launch_req(p, ctx->d_groups, frac, s1_req, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "request-violations kernel");
+}
+
 }  // extern "C"

@@ -473,92 +473,6 @@ __global__ void check_rows_kernel(const Cand cd, int T, unsigned long long *n_ba
 // MC).  RANDOM: the lanes compute the row's Philox blocks in parallel, then
 // lane 0 runs the Fisher-Yates swaps from shared memory (same permutation as
 // fy_materialise).  Returns with srow[0..T) valid for all lanes.
-// Materialise one candidate row into srow[0..T) with a warp (R9/R10).  For
-// RANDOM, the lanes first compute every swap target j_i = i + mulhi(u_i, T-i)
-// in parallel (they depend only on the Philox words, not on the row), then
-// lane 0 runs the forward Fisher-Yates swaps with one shared-memory round trip
-// per step: the value at position i+1 is loaded together with row[j_i] (the
-// only store of step i that can touch position i+1 is row[j_i] = row[i]).
-__device__ __forceinline__ void warp_gen_row(const Cand &cd, int T, uint64_t c, int64_t loc,
-                                             uint16_t *srow, uint16_t *sJ) {
-    const int lane = threadIdx.x & 31;
-    if (cd.kind == QLM_CAND_RANDOM) {
-        const int nb = (T - 1 + 3) / 4;
-        const uint2 key = make_uint2((uint32_t)cd.seed, (uint32_t)(cd.seed >> 32));
-        for (int b = lane; b < nb; b += 32) {
-            const uint4 wd = philox10(make_uint4((uint32_t)b, (uint32_t)c, (uint32_t)(c >> 32), kRowTag), key);
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int i = 4 * b + h;
-                if (i + 1 < T) sJ[i] = (uint16_t)(i + (int)__umulhi(pick4(wd, h), (uint32_t)(T - i)));
-            }
-        }
-        for (int s = lane; s < T; s += 32) srow[s] = (uint16_t)s;
-        __syncwarp();
-        if (lane == 0 && T > 1) {
-            uint32_t ti = srow[0];
-            int j = sJ[0];
-            for (int i = 0; i + 1 < T; ++i) {
-                const int jn = i + 2 < T ? sJ[i + 1] : 0;
-                const uint32_t tj = srow[j];
-                const uint32_t nx = srow[i + 1];
-                srow[j] = (uint16_t)ti;
-                srow[i] = (uint16_t)tj;
-                ti = (j == i + 1) ? ti : nx;
-                j = jn;
-            }
-        }
-    } else if (cd.kind == QLM_CAND_ENUM) {
-        if (lane == 0) {
-            int s = 0;
-            tokens_enum(c, T, [&](int tok) { srow[s++] = (uint16_t)tok; });
-        }
-    } else if (cd.kind == QLM_CAND_NEIGHBOR) {
-        for (int s = lane; s < T; s += 32)
-            srow[s] = cd.tb == 1 ? (uint16_t)base_token<uint8_t>(cd, s) : (uint16_t)base_token<uint16_t>(cd, s);
-        __syncwarp();
-        if (lane == 0) {
-            int mi[QLM_MAX_MOVES], mj[QLM_MAX_MOVES];
-            nbr_moves(cd, T, c, mi, mj);
-            for (int m = 0; m < cd.moves; ++m) {
-                const uint16_t t = srow[mi[m]];
-                srow[mi[m]] = srow[mj[m]];
-                srow[mj[m]] = t;
-            }
-        }
-    } else {
-        const uint8_t *row = cd.rows + loc * cd.stride;
-        for (int s = lane; s < T; s += 32)
-            srow[s] = cd.tb == 1 ? row[s] : reinterpret_cast<const uint16_t *>(row)[s];
-    }
-    __syncwarp();
-}
-
-// Walk a materialised row in 32-token chunks with warp ballots: for each
-// group token, its queue q (separators before it, capped at Q-1, R9), its
-// position within the queue and its slot index (groups before it).
-template <typename F>
-__device__ __forceinline__ void warp_slots(const uint16_t *srow, int T, int G, int Q, F &&f) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
-    int nsep = 0, lastsep = -1;
-    for (int s0 = 0; s0 < T; s0 += 32) {
-        const int s = s0 + lane;
-        const int tok = s < T ? srow[s] : 0;
-        const bool sep = s < T && tok >= G;
-        const uint32_t bs = __ballot_sync(0xFFFFFFFFu, sep);
-        const uint32_t below = bs & lt;
-        const int before = nsep + __popc(below);
-        const int ls = below ? s0 + 31 - __clz(below) : lastsep;
-        if (s < T && !sep) {
-            const int q = before < Q - 1 ? before : Q - 1;
-            f(tok, q, s - ls - 1, s - before);
-        }
-        nsep += __popc(bs);
-        if (bs) lastsep = s0 + 31 - __clz(bs);
-    }
-}
-
 // Rows / decode with one warp per candidate (small counts).
 __global__ void __launch_bounds__(32) row_warp_kernel(const ScanParams p, uint16_t *rows_out,
                                                       int32_t *queue_of, int32_t *pos_of) {

@@ -46,6 +46,8 @@ cudaError_t launch_scan(ScanParams p, cudaStream_t st);
 cudaError_t launch_ws(ScanParams p, cudaStream_t st);      // warp-specialised fast path
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st);   // ws, else scan
 cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per candidate (large G)
+cudaError_t launch_req(const ScanParams &p, const qlm_group *groups, float *frac, float *s1r,
+                       cudaStream_t st);                            // request-level (R19)
 cudaError_t launch_adopt(const Dims &dm, const Cand &cd, const qlm_record *rec, qlm_record *inc,
                          cudaStream_t st);                          // local-search step (R18)
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,

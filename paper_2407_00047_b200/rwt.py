@@ -142,6 +142,15 @@ class RwtEstimator:
         buf[: self.T] = r.to(buf.dtype).to(self.device)
         return buf
 
+    def request_violations(self, cand: Cand, stream=None):
+        """R19: (frac [G, count], s1_req [count]) -- per-group fraction of SLO-violating
+        requests and the request-granular S1 of each candidate."""
+        frac = self._empty((self.G, cand.count), torch.float32)
+        s1r = self._empty(cand.count, torch.float32)
+        L.check(L.lib().qlm_request_violations(self._h, C.byref(cand.c()), frac.data_ptr(), s1r.data_ptr(),
+                                               self._stream(stream)), "qlm_request_violations")
+        return frac, s1r
+
     def adopt_best(self, cand: Cand, rec: torch.Tensor, incumbent: torch.Tensor, stream=None):
         """Device-side local-search step: cand.rows <- winner row if rec beats incumbent."""
         L.check(L.lib().qlm_adopt_best(self._h, C.byref(cand.c()), rec.data_ptr(), incumbent.data_ptr(),

@@ -637,3 +637,36 @@ def test_neighbor_decode_and_mc_from_device_record():
     X = O.Oracle(p).mc_sample(4, 0, 200)
     ref = O.Oracle(p).mc_count(O.EXPLICIT, 0, 1, X, rows=row[None, :].astype(np.uint16))
     assert np.array_equal(cnt, ref)
+
+
+# ------------------------------------------------------- request-level violations (R19, N2)
+@pytest.mark.parametrize("cfg,kind,n", [("C2", "random", 300), ("C3", "random", 200), ("C4", "explicit", 20),
+                                         ("C5h", "random", 12), ("C1r", "enum", 24)])
+def test_request_violations_vs_oracle(cfg, kind, n):
+    p = make_config(cfg)
+    e = est_of(p)
+    o = O.Oracle(p)
+    if kind == "random":
+        cand, ref = e.random(17, n, seed=2), o.request_violations_range(O.RANDOM, 17, n, seed=2)
+    elif kind == "enum":
+        cand, ref = e.enum(0, n), o.request_violations_range(O.ENUM, 0, n)
+    else:
+        rows = np.stack([O.random_row(6, c, p.T) for c in range(n)])
+        cand = e.explicit(rows_tensor(rows, token_bytes=p.token_bytes))
+        ref = o.request_violations_range(O.EXPLICIT, 0, n, rows=rows.astype(np.uint16 if p.token_bytes == 2 else np.uint8))
+    frac, s1r = e.request_violations(cand)
+    f = frac.cpu().numpy().T.astype(np.float64)
+    assert np.abs(f - ref["frac"]).max() <= 1e-5
+    assert np.abs(s1r.cpu().numpy() - ref["s1"]).max() <= 1e-5
+
+
+def test_request_violations_of_neighbor_winner_record():
+    p = make_config("C3")
+    e = est_of(p)
+    base_np = O.random_row(3, 3, p.T)
+    base = e.row_buffer(base_np)
+    rec = e.best_ordering_async(e.neighbor(base, 0, 8192, seed=1, moves=2))
+    frac, s1r = e.request_violations(e.from_record(rec, kind=3, seed=1, base=base, moves=2))
+    row = O.neighbor_row(base_np, 1, int(rec.cpu().numpy()[1]), 2)
+    f, s1 = O.Oracle(p).request_violations(row)
+    assert np.abs(frac.cpu().numpy()[:, 0] - f).max() <= 1e-5 and abs(float(s1r[0]) - s1) <= 1e-5

@@ -3,7 +3,8 @@
     python tools/search_bench.py C3 [per_iter] [iters]
 Starts from the FCFS and the EDF comparator rows, runs
 qlm_local_search (2 transpositions per candidate), and prints the objective
-(S1 = expected violating fraction, S2 = sum of slacks) of the comparators,
+(S1 = expected violating fraction, S2 = sum of slacks, and the request-level
+S1_req of R19) of the comparators,
 of the best of as many RANDOM candidates, and of the search result, plus
 candidates/s of the search timed with CUDA events.
 """
@@ -29,8 +30,10 @@ def main():
 
     def score(row):
         b = e.row_buffer(row)
-        s1, s2, _ = e.score_orderings(e.explicit(b.view(1, -1)))
-        return float(s1[0]), float(s2[0])
+        ex = e.explicit(b.view(1, -1))
+        s1, s2, _ = e.score_orderings(ex)
+        _, s1r = e.request_violations(ex)          # request-granular S1 (R19)
+        return float(s1[0]), float(s2[0]), float(s1r[0])
 
     out = {"config": cfg, "per_iter": per_iter, "iters": iters}
     for name, row in (("fcfs", fcfs_row(p)), ("edf", edf_row(p))):
@@ -50,6 +53,18 @@ def main():
         out[name] = score(res)
         out[name + "_ms"] = round(ms, 3)
         out[name + "_cand_per_s"] = per_iter * iters / ms * 1e3
+    # request-level evaluation rate (R19) over 65536 RANDOM candidates
+    cand = e.random(0, 65536, seed=3)
+    e.request_violations(cand)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    e.request_violations(cand)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    out["request_violations_65536_ms"] = round(ms, 3)
+    out["request_evals_per_s"] = 65536 * float(p.n_req.sum()) / ms * 1e3
     print(out)
 
 
