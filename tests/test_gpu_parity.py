@@ -1,6 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element
 by element on the same seeded inputs.  Tolerances: tests/parity.py."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -670,3 +671,33 @@ def test_request_violations_of_neighbor_winner_record():
     row = O.neighbor_row(base_np, 1, int(rec.cpu().numpy()[1]), 2)
     f, s1 = O.Oracle(p).request_violations(row)
     assert np.abs(frac.cpu().numpy()[:, 0] - f).max() <= 1e-5 and abs(float(s1r[0]) - s1) <= 1e-5
+
+
+def test_neighbor_u16_paths_c4_and_local_search_c5():
+    """u16 rows: NEIGHBOR bulk through the warp-specialised kernel at T = 263
+    (C4) equals the general kernel bit for bit, and a short C5 local search
+    (u16 base row) returns a valid, not worse ordering."""
+    p = make_config("C4")
+    e = est_of(p)
+    base_np = balanced_row(p.G, p.Q).astype(np.int64)
+    base = e.row_buffer(base_np)
+    assert base.dtype == torch.int16
+    cand = e.neighbor(base, 0, 4608, seed=6, moves=5)
+    res = {}
+    for no_ws in ("1", "0"):
+        os.environ["QLM_NO_WS"] = no_ws
+        bufs = {k: torch.empty((p.G, 4608), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+        res[no_ws] = e.score_estimate(cand, out=bufs)
+    os.environ.pop("QLM_NO_WS", None)
+    for k in ("wt", "sd", "v", "s1", "s2"):
+        assert torch.equal(res["0"][k], res["1"][k]), k
+    est = O.Oracle(p).estimate_range(O.NEIGHBOR, 0, 64, seed=6, rows=base_np, moves=5)
+    check_estimates({k: res["0"][k][:, :64] for k in ("wt", "sd", "v")}, est)
+    p5 = make_config("C5")
+    e5 = est_of(p5)
+    o5 = O.Oracle(p5)
+    start = O.random_row(1, 0, p5.T)
+    buf, inc = e5.local_search(start, moves=3, per_iter=4096, iters=3, seed=2)
+    row = buf.cpu().numpy()[: p5.T].astype(np.int64) & 0xFFFF
+    assert sorted(row) == list(range(p5.T))
+    assert O.key32(*o5.score(row)[:2]) <= O.key32(*o5.score(start)[:2])
