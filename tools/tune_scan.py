@@ -45,6 +45,8 @@ def main():
     for cfgd in configs:
         blk, rs = cfgd, ""
         for k, v in ((k, cfgd.get(k)) for k in keys):
+            if quick:
+                break                       # quick mode: keep the caller's environment
             if v is None:
                 os.environ.pop(k, None)
             else:
