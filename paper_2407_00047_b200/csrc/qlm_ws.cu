@@ -128,6 +128,9 @@ __device__ __forceinline__ void produce_row(const Cand &cd, int T, uint8_t *slot
 // trash row, so a separator slot runs the same straight-line code as a group
 // slot; the queue table is padded to T entries so the queue counter needs no
 // clamp.
+// Transition entries are 8 B: a 64-bit shared load is served per half-warp
+// (16 lanes), so 16 interleaved replicas make it conflict-free.
+constexpr int kTrRs = 4;
 struct alignas(16) WsG {      // 16 B (one LDS.128), replicated 1 << RS times
     double slo;
     float nf;                // n_i as float (S1 numerator, exact below 2^24)
@@ -196,7 +199,13 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
         isbar[k] = tok >= G && !pad;
         tg[k] = pad ? G : min(tok, G);
         q += isbar[k];
-        g[k] = sgl[tg[k] << RS];
+        {   // one 128-bit load (two 64-bit loads of 8-way replicated 16-B records conflict)
+            const double2 raw = *reinterpret_cast<const double2 *>(sgl + (tg[k] << RS));
+            g[k].slo = raw.x;
+            const unsigned long long hi = (unsigned long long)__double_as_longlong(raw.y);
+            g[k].nf = __uint_as_float((uint32_t)hi);
+            g[k].model = (int)(uint32_t)(hi >> 32);
+        }
         if (isbar[k]) r[k] = sq[q];                          // only separator lanes read
         else { r[k].bmean = 0.0; r[k].bvar = 0.0; r[k].prow0 = 0; r[k].dG = 0; r[k].dbase = 0; }
     }
@@ -220,7 +229,7 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         ab[k] = sabl[(dk[k] + tg[k]) << RS];
-        tr[k] = str[(pk[k] + g[k].model) << RS];             // replicated: conflict-free
+        tr[k] = str[(pk[k] + g[k].model) << kTrRs];          // 16 replicas: conflict-free
     }
     // (iv) the Eq. 10 chain (operation order identical to the sequential definition)
     double wt[K], V[K];
@@ -311,8 +320,8 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         sq[i] = r;
     }
     double *str = reinterpret_cast<double *>(smem + p.off_tr);
-    for (int i = tid; i < ((D * 2 * M * M) << RS); i += blockDim.x) {
-        const int e = i >> RS;
+    for (int i = tid; i < ((D * 2 * M * M) << kTrRs); i += blockDim.x) {
+        const int e = i >> kTrRs;
         const int m = e % M, pp = (e / M) % (2 * M), d = e / (2 * M * M);
         const int from = pp < M ? pp : pp - M;
         const double sw = p.tb.swap[(d * M + from) * M + m];
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
     } else {
         const WsG *sgl = sg + (lane & ((1 << RS) - 1));
         const double2 *sabl = sab + (lane & ((1 << RS) - 1));
-        const double *strl = str + (lane & ((1 << RS) - 1));
+        const double *strl = str + (lane & ((1 << kTrRs) - 1));
         const float zc2f = (float)p.zc2;
         const float alpha = p.alpha;
         const double den = *p.tb.den;
@@ -477,7 +486,7 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
     p.off_grec = (int)off; off = a16(off + ((size_t)(dm.G + 1) << rs) * sizeof(WsG));
     p.off_ab = (int)off;   off = a16(off + ((size_t)dm.D * (dm.G + 1) << rs) * sizeof(double2));
     p.off_q = (int)off;    off = a16(off + (size_t)(dm.T + 1) * sizeof(WsQ));
-    p.off_tr = (int)off;   off = a16(off + ((size_t)dm.D * 2 * dm.M * dm.M << rs) * sizeof(double));
+    p.off_tr = (int)off;   off = a16(off + ((size_t)dm.D * 2 * dm.M * dm.M << kTrRs) * sizeof(double));
     const int epw = 4 / tok_bytes;
     w.tw = (dm.T + epw - 1) / epw;
     w.off_rows = (int)off; off = a16(off + (size_t)2 * W * w.tw * 128);
