@@ -298,6 +298,7 @@ struct SlotTables {
     const double *str;     // [D * 2M * M]     tail part + swap part (one transition term)
     const QRec *sq;        // [Q]
     int G, Q, M, rs, rl;   // rl = lane & ((1 << rs) - 1)
+    int trs, trl;          // transition table: 1 << trs replicas, trl = lane & ((1 << trs) - 1)
 };
 
 struct ScanState {
@@ -315,10 +316,16 @@ __device__ __forceinline__ void start_queue(const SlotTables &t, ScanState &s, i
 // One group slot: returns its (wt, V) and record.
 __device__ __forceinline__ void group_slot(const SlotTables &t, ScanState &s, int tok,
                                            double &wt, double &V, GRec &g) {
-    g = t.sg[(tok << t.rs) + t.rl];
+    {   // one 128-bit load of the 16-B record (two 64-bit loads conflict across replicas)
+        const double2 raw = *reinterpret_cast<const double2 *>(t.sg + (tok << t.rs) + t.rl);
+        const unsigned long long hi = (unsigned long long)__double_as_longlong(raw.y);
+        g.slo = raw.x;
+        g.n = (int32_t)(uint32_t)hi;
+        g.model = (int32_t)(uint32_t)(hi >> 32);
+    }
     const double2 ab = t.sab[((s.d * t.G + tok) << t.rs) + t.rl];
     const int m = g.model;
-    s.A = __dadd_rn(s.A, t.str[(s.d * 2 * t.M + s.prev) * t.M + m]);   // C - W ahead + swap S
+    s.A = __dadd_rn(s.A, t.str[(((s.d * 2 * t.M + s.prev) * t.M + m) << t.trs) + t.trl]);   // C - W ahead + swap S
     wt = s.A;
     V = s.B;                                         // exclusive (R5)
     s.A = __dadd_rn(s.A, ab.x);

@@ -136,8 +136,10 @@ __device__ __forceinline__ SlotTables stage_tables(const ScanParams &p, uint8_t 
     for (int i = tid; i < dm.Q; i += blk) sq[i] = p.tb.qrec[i];
     double *str = reinterpret_cast<double *>(smem + p.off_tr);
     const int M = dm.M;
-    for (int i = tid; i < dm.D * 2 * M * M; i += blk) {
-        const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
+    const int trs = p.tr_shift;
+    for (int i = tid; i < (dm.D * 2 * M * M) << trs; i += blk) {
+        const int e = i >> trs;
+        const int m = e % M, pp = (e / M) % (2 * M), d = e / (2 * M * M);
         const int from = pp < M ? pp : pp - M;
         const double sw = p.tb.swap[(d * M + from) * M + m];
         const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
@@ -146,6 +148,7 @@ __device__ __forceinline__ SlotTables stage_tables(const ScanParams &p, uint8_t 
     SlotTables t;
     t.sg = sg; t.sab = sab; t.str = str; t.sq = sq;
     t.G = dm.G; t.Q = dm.Q; t.M = dm.M; t.rs = rs; t.rl = tid & ((1 << rs) - 1);
+    t.trs = trs; t.trl = tid & ((1 << trs) - 1);
     return t;
 }
 
@@ -774,7 +777,9 @@ static size_t plan_smem(ScanParams &p, int rep_shift, int kind, int tok_bytes, i
     p.off_grec = (int)off; off = align16(off + ((size_t)dm.G << rep_shift) * sizeof(GRec));
     p.off_ab = (int)off;   off = align16(off + ((size_t)dm.D * dm.G << rep_shift) * sizeof(double2));
     p.off_q = (int)off;    off = align16(off + (size_t)dm.Q * sizeof(QRec));
-    p.off_tr = (int)off;   off = align16(off + (size_t)dm.D * 2 * dm.M * dm.M * sizeof(double));
+    // transition entries (8 B) may be replicated (QLM_TR_SHIFT) for conflict-free 64-bit loads
+    p.tr_shift = env_int("QLM_TR_SHIFT", 0);   // measured: no gain in the thread-per-candidate scan
+    p.off_tr = (int)off;   off = align16(off + ((size_t)dm.D * 2 * dm.M * dm.M << p.tr_shift) * sizeof(double));
     p.off_scratch = (int)off;
     if (kind == QLM_CAND_RANDOM) {
         const int epw = 4 / tok_bytes;

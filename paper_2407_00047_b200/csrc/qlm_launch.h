@@ -24,6 +24,7 @@ struct ScanParams {
     int use_tma;               // staged outputs leave through bulk async copies
     int n_out;                 // number of non-null bulk outputs
     int rep_shift;             // group tables replicated 1 << rep_shift times in smem
+    int tr_shift;              // transition table replicated 1 << tr_shift times (scan kernel)
     int off_grec, off_ab, off_q, off_tr, off_scratch, off_stage;
     int64_t ld_out;            // leading dimension of the bulk outputs (0 = count)
     uint32_t *ilv;             // large-T RANDOM: word-interleaved row scratch [words][ilv_cap]

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
     __syncthreads();
     SlotTables tab;
     tab.sg = sg; tab.sab = sab; tab.str = str; tab.sq = sq;
-    tab.G = G; tab.Q = Q; tab.M = M; tab.rs = 0; tab.rl = 0;
+    tab.G = G; tab.Q = Q; tab.M = M; tab.rs = 0; tab.rl = 0; tab.trs = 0; tab.trl = 0;
 
     const Cand cd = p.cd;
     const int64_t count = cd.count;
