@@ -77,12 +77,15 @@ constexpr uint32_t kNbrTag = 0x4E424852u;
 // ---- per-thread Fisher-Yates scratch in shared memory ----------------------
 // Element i of thread `tid` lives in 32-bit word (i / EPW) * blk + tid, byte
 // lane i % EPW: a warp touching any elements hits 32 distinct banks.
+// Byte offset = 4 (w blk + tid) + (i mod EPW) sizeof(TOK) with w = i / EPW,
+// written as i sizeof(TOK) + w (4 blk - 4) + 4 tid: one shift and one
+// multiply-add per element (4 tid is loop-invariant).
 template <typename TOK>
 __device__ __forceinline__ TOK *fy_elem(uint8_t *base, int i, int blk, int tid) {
     constexpr int EPW = 4 / (int)sizeof(TOK);
     const unsigned u = (unsigned)i;
-    return reinterpret_cast<TOK *>(base + ((size_t)((u / EPW) * (unsigned)blk + (unsigned)tid) << 2) +
-                                   (u % EPW) * sizeof(TOK));
+    return reinterpret_cast<TOK *>(base + 4u * (unsigned)tid +
+                                   (u * (unsigned)sizeof(TOK) + (u / EPW) * (4u * (unsigned)blk - 4u)));
 }
 
 // Forward Fisher-Yates over T tokens (R10); calls f(token) for positions
