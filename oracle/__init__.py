@@ -42,6 +42,10 @@ class _Problem(C.Structure):
     ]
 
 
+class _Tiers(C.Structure):
+    _fields_ = [("mem", C.c_void_p), ("cap", C.c_void_p), ("load", C.c_void_p)]
+
+
 _lib = None
 
 
@@ -72,6 +76,13 @@ def lib():
         _lib.or_request_violations_range.restype = i64
         _lib.or_mc_count.argtypes = [P, C.c_int, vp, i32, i64, u64, u64, i64, vp, i64, vp]
         _lib.or_mc_count.restype = i64
+        T = C.POINTER(_Tiers)
+        _lib.or_estimate_row_tiered.argtypes = [P, T, vp, dp, dp, vp]
+        _lib.or_estimate_row_tiered.restype = C.c_int
+        _lib.or_score_row_tiered.argtypes = [P, T, vp, dp, dp, vp, dp, dp]
+        _lib.or_score_row_tiered.restype = C.c_int
+        _lib.or_tiered_range.argtypes = [P, T, C.c_int, vp, i32, i64, u64, u64, i64, dp, dp, vp, dp, dp]
+        _lib.or_tiered_range.restype = i64
     return _lib
 
 
@@ -177,6 +188,47 @@ class Oracle:
         bad = lib().or_request_violations_range(C.byref(self.p), kind, _ptr(rows), tb, stride, seed,
                                                 first, count, _ptr(frac), _ptr(s1))
         return dict(frac=frac, s1=s1, bad=bad)
+
+    # -- two-tier model swapping (R20) -------------------------
+    def _tiers(self, tiers):
+        """tiers: dict(mem=int32 [M], cap=int32 [D], load=f64 [D, M]) (workloads.make_tiers)."""
+        k = (np.ascontiguousarray(tiers["mem"], np.int32), np.ascontiguousarray(tiers["cap"], np.int32),
+             np.ascontiguousarray(tiers["load"], np.float64))
+        return k, _Tiers(*[_ptr(a) for a in k])
+
+    def estimate_tiered(self, row, tiers):
+        row = np.ascontiguousarray(row, np.int32)
+        keep, t = self._tiers(tiers)
+        wt, V, cold = np.zeros(self.G), np.zeros(self.G), np.zeros(self.G, np.int32)
+        if lib().or_estimate_row_tiered(C.byref(self.p), C.byref(t), _ptr(row), _ptr(wt), _ptr(V),
+                                        _ptr(cold)) != 0:
+            raise ValueError("row is not a permutation of 0..T-1 (Eq. 6)")
+        return dict(wt=wt, V=V, cold=cold)
+
+    def score_tiered(self, row, tiers):
+        row = np.ascontiguousarray(row, np.int32)
+        keep, t = self._tiers(tiers)
+        s1, s2, no = C.c_double(), C.c_double(), C.c_int32()
+        if lib().or_score_row_tiered(C.byref(self.p), C.byref(t), _ptr(row), C.byref(s1), C.byref(s2),
+                                     C.byref(no), None, None) != 0:
+            raise ValueError("row is not a permutation of 0..T-1 (Eq. 6)")
+        return s1.value, s2.value, no.value
+
+    def tiered_range(self, tiers, kind, first, count, seed=0, rows=None, moves=0, estimates=True):
+        rows, tb, stride = self._rows_args(kind, rows, moves)
+        keep, t = self._tiers(tiers)
+        G = self.G
+        s1, s2, no = np.zeros(count), np.zeros(count), np.zeros(count, np.int32)
+        wt = np.zeros((count, G)) if estimates else None
+        V = np.zeros((count, G)) if estimates else None
+        bad = lib().or_tiered_range(C.byref(self.p), C.byref(t), kind, _ptr(rows), tb, stride, seed,
+                                    first, count, _ptr(s1), _ptr(s2), _ptr(no), _ptr(wt), _ptr(V))
+        out = dict(s1=s1, s2=s2, n_over=no, bad=bad)
+        if estimates:
+            out.update(wt=wt, V=V, sd=np.sqrt(V),
+                       v=np.array([[violation(wt[k, i], V[k, i], self.prob.slo[i]) for i in range(G)]
+                                   for k in range(count)]) if count * G <= 200000 else None)
+        return out
 
     def mc_sample(self, mc_seed, trial_first, trial_count):
         X = np.zeros((trial_count, self.G), np.uint32)

@@ -30,6 +30,11 @@
  *                      SPT (min S2) and Moore-Hodgson (min S1) vs brute force.
  *   or_mc_sample       closed form for constant tables, CLT normality test.
  *   or_mc_count        deterministic-table special case == step function.
+ *   or_estimate_row_tiered (R20, N3)  load = 0 and cap >= sum mem reduce to
+ *                      or_estimate_row bit-exactly; cap = 0 equals
+ *                      or_estimate_row with swap + load folded into the swap
+ *                      table; hand-worked golden (prefix-not-first-fit,
+ *                      re-entry keeps its tier); wt monotone in cap.
  */
 #include <math.h>
 #include <stdint.h>
@@ -446,6 +451,134 @@ int64_t or_request_violations_range(const or_problem *p, int kind, const void *r
     for (int64_t k = 0; k < count; ++k) {
         get_row(kind, rows, token_bytes, stride, seed, first + (uint64_t)k, k, T, row);
         if (or_request_violations_row(p, row, frac + k * p->G, &s1[k]) != 0) { s1[k] = NAN; ++bad; }
+    }
+    free(row);
+    return bad;
+}
+
+/* ---- two-tier (warm / cold) model swapping (R20) ---------
+ * every model served from the registry goes storage -> CPU
+ * memory -> GPU memory.  "Models present later in the virtual queue are
+ * warm and placed in the CPU memory until all the CPU memory is exhausted.
+ * The remaining models (cold models) are not swapped out from the LLM model
+ * registry."  Reading R20, per queue q on device d:
+ *   - the queue's swap targets, in order of their first transition (Eq. 9:
+ *     slots with m != previous model, m_{-1} = resident, R4), are taken in
+ *     turn; target m is warm while cum + mem[m] <= cap[d] (cum += mem[m]),
+ *     and from the first target that does not fit on, CPU memory is
+ *     exhausted: that target and every later new target are cold;
+ *   - a model keeps its tier for every later transition into it;
+ *   - the transition term of Eq. 10 (R1/R2) becomes
+ *       trans = swap[d][prev][m]             (CPU -> GPU, warm)
+ *       trans = swap[d][prev][m] + load[d][m] (storage -> CPU first, cold)
+ *     then tail(prev) + trans as in or_estimate_row.
+ * With load = 0, or cap >= sum of all mem, this is or_estimate_row exactly. */
+typedef struct {
+    const int32_t *mem;    /* [M] model size in integer units (e.g. GB), >= 1  */
+    const int32_t *cap;    /* [D] CPU memory of a device-d instance, same units */
+    const double *load;    /* [D][M] storage -> CPU load time of model m, s    */
+} or_tiers;
+
+int or_estimate_row_tiered(const or_problem *p, const or_tiers *t, const int32_t *row,
+                           double *wt, double *V, int32_t *cold_of)
+{
+    int32_t T = p->G + p->Q - 1;
+    char seen[4096], tier[64];            /* tier: 0 = not a target yet, 1 warm, 2 cold */
+    if (T > 4096 || p->M > 64) return -1;
+    memset(seen, 0, (size_t)T);
+    for (int32_t s = 0; s < T; ++s) {
+        if (row[s] < 0 || row[s] >= T || seen[row[s]]) return -1;
+        seen[row[s]] = 1;
+    }
+    int32_t q = 0;
+    int32_t d = p->q_device[0], prev = p->q_resident[0], first = 1;
+    double A = p->q_bmean[0], B = p->q_bvar[0];
+    int64_t cum = 0;
+    int exhausted = 0;
+    memset(tier, 0, sizeof tier);
+    for (int32_t s = 0; s < T; ++s) {
+        int32_t tok = row[s];
+        if (tok >= p->G) {                       /* queue separator: new queue, new CPU memory */
+            ++q;
+            d = p->q_device[q]; prev = p->q_resident[q]; first = 1;
+            A = p->q_bmean[q]; B = p->q_bvar[q];
+            cum = 0; exhausted = 0;
+            memset(tier, 0, sizeof tier);
+            continue;
+        }
+        int32_t i = tok, m = p->model[i];
+        int32_t cold = 0;
+        if (m != prev) {                                     /* t = 1, Eq. 9 */
+            if (tier[m] == 0) {                              /* first transition into m */
+                if (!exhausted && cum + t->mem[m] <= t->cap[d]) { tier[m] = 1; cum += t->mem[m]; }
+                else { tier[m] = 2; exhausted = 1; }
+            }
+            int backlog = p->q_bmean[q] > 0.0;
+            double trans = p->swap[(d * p->M + prev) * p->M + m];
+            if (tier[m] == 2) { trans = trans + t->load[d * p->M + m]; cold = 1; }
+            if (!first || backlog) trans = tail_of(p, d, prev) + trans;
+            A = A + trans;
+        }
+        wt[i] = A;
+        V[i] = B;
+        if (cold_of) cold_of[i] = cold;
+        double th = p->theta[d * p->M + m];
+        A = A + ((double)p->n_req[i] * p->mu[i]) / th;
+        B = B + ((double)p->n_req[i] * p->var[i]) / (th * th);
+        prev = m; first = 0;
+    }
+    return 0;
+}
+
+/* Scores (R11) and per-group estimates ([G] each, nullable) of one row
+ * under R20; same sums and order as or_score_row.                          */
+int or_score_row_tiered(const or_problem *p, const or_tiers *t, const int32_t *row,
+                        double *s1, double *s2, int32_t *n_over, double *wt_out, double *V_out)
+{
+    int32_t G = p->G, T = p->G + p->Q - 1;
+    double *wt = (double *)malloc(sizeof(double) * (size_t)G);
+    double *V = (double *)malloc(sizeof(double) * (size_t)G);
+    int rc = or_estimate_row_tiered(p, t, row, wt, V, NULL);
+    if (rc == 0) {
+        double num = 0.0, den = 0.0, pen = 0.0;
+        int32_t over = 0;
+        for (int32_t s = 0; s < T; ++s) {
+            int32_t i = row[s];
+            if (i >= G) continue;
+            double v = or_violation(wt[i], V[i], p->slo[i], p->z_clamp);
+            num = num + (double)p->n_req[i] * v;
+            den = den + (double)p->n_req[i];
+            pen = pen + (wt[i] - p->slo[i]);
+            if (v > p->alpha) ++over;
+        }
+        *s1 = num / den;
+        *s2 = pen;
+        if (n_over) *n_over = over;
+        for (int32_t i = 0; i < G; ++i) {
+            if (wt_out) wt_out[i] = wt[i];
+            if (V_out) V_out[i] = V[i];
+        }
+    }
+    free(wt); free(V);
+    return rc;
+}
+
+/* Range form: s1, s2 [count], n_over [count] and wt, V [count][G] (each
+ * nullable except s1, s2).  Returns #invalid rows.                          */
+int64_t or_tiered_range(const or_problem *p, const or_tiers *t, int kind, const void *rows,
+                        int32_t token_bytes, int64_t stride, uint64_t seed, uint64_t first,
+                        int64_t count, double *s1, double *s2, int32_t *n_over, double *wt,
+                        double *V)
+{
+    int32_t G = p->G, T = p->G + p->Q - 1;
+    int32_t *row = (int32_t *)malloc(sizeof(int32_t) * (size_t)T);
+    int64_t bad = 0;
+    for (int64_t k = 0; k < count; ++k) {
+        get_row(kind, rows, token_bytes, stride, seed, first + (uint64_t)k, k, T, row);
+        if (or_score_row_tiered(p, t, row, &s1[k], &s2[k], n_over ? &n_over[k] : NULL,
+                                wt ? wt + k * G : NULL, V ? V + k * G : NULL) != 0) {
+            s1[k] = NAN; s2[k] = NAN; ++bad;
+        }
     }
     free(row);
     return bad;

@@ -515,3 +515,86 @@ def test_request_violations_bounds():
         v = np.array([O.violation(e["wt"][i], e["V"][i], p.slo[i]) for i in range(p.G)])
         assert np.all(f >= v - 1e-15) and np.all(f <= 1.0)     # later requests wait longer
         assert s1r >= o.score(row)[0] - 1e-15
+
+
+# ---------------------------------------------------------------- N3: two-tier swapping (R20)
+def _tier_hand():
+    p = hand_problem([1, 2, 1, 3, 0], 25, 200.0, 0.0, 1e4, theta=1000.0, prefill=0.5, eps=1.0,
+                     dtok=0.5, max_out=1.0, swap=20.0, M=4)
+    tiers = dict(mem=np.array([5, 2, 3, 1], np.int32), cap=np.array([4], np.int32),
+                 load=np.array([[10.0, 20.0, 30.0, 40.0]]))
+    return p, tiers
+
+
+def test_tiers_hand_golden_N3():
+    g = gold("n3_tiers.json")
+    p, tiers = _tier_hand()
+    o = O.Oracle(p)
+    row = [0, 1, 2, 3, 4]
+    e = o.estimate_tiered(row, tiers)
+    assert list(e["wt"]) == g["wt_by_group"]
+    assert list(e["cold"]) == g["cold_by_group"]
+    assert list(o.estimate(row)["wt"]) == g["wt_untiered"]
+    big = dict(tiers, cap=np.array([11], np.int32))          # every model fits: all warm
+    assert list(o.estimate_tiered(row, big)["wt"]) == g["wt_all_warm"]
+    zero = dict(tiers, cap=np.array([0], np.int32))          # no CPU memory: all cold
+    assert list(o.estimate_tiered(row, zero)["wt"]) == g["wt_all_cold"]
+
+
+def _rand_tier_case(seed):
+    rng = np.random.default_rng(9000 + seed)
+    G, Q, M, D = int(rng.integers(4, 24)), int(rng.integers(1, 5)), int(rng.integers(2, 6)), int(rng.integers(1, 3))
+    p = make_random_problem(rng, G, Q, M, D, backlog=bool(seed % 2))
+    from workloads.synth import make_random_tiers
+    return rng, p, make_random_tiers(rng, M, D)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_tiers_reduce_to_untiered_when_all_warm_or_free(seed):
+    # cap >= sum(mem): every target warm -> the R1-R7 estimator, bit for bit;
+    # load = 0: the tier never changes the cost -> the same.
+    rng, p, tiers = _rand_tier_case(seed)
+    o = O.Oracle(p)
+    allwarm = dict(tiers, cap=np.full(p.D, int(tiers["mem"].sum()), np.int32))
+    free = dict(tiers, load=np.zeros_like(tiers["load"]))
+    for c in range(20):
+        row = o.random_row(7, c)
+        base = o.estimate(row)
+        for t in (allwarm, free):
+            e = o.estimate_tiered(row, t)
+            assert np.array_equal(e["wt"], base["wt"]) and np.array_equal(e["V"], base["V"])
+        assert o.score_tiered(row, allwarm) == o.score(row)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_tiers_all_cold_equals_folded_swap_table(seed):
+    # cap = 0: every transition is cold, i.e. the untiered estimator with
+    # swap'[d][a][b] = swap[d][a][b] + load[d][b] (same single addition).
+    import dataclasses
+    rng, p, tiers = _rand_tier_case(seed)
+    cold = dict(tiers, cap=np.zeros(p.D, np.int32))
+    sw = p.swap + tiers["load"][:, None, :]
+    for d in range(p.D):
+        np.fill_diagonal(sw[d], 0.0)
+    o, of = O.Oracle(p), O.Oracle(dataclasses.replace(p, swap=sw))
+    for c in range(20):
+        row = o.random_row(11, c)
+        e, f = o.estimate_tiered(row, cold), of.estimate(row)
+        assert np.array_equal(e["wt"], f["wt"]) and np.array_equal(e["V"], f["V"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tiers_wait_monotone_in_cpu_memory(seed):
+    # More CPU memory only lengthens the warm prefix: no wait can grow.
+    rng, p, tiers = _rand_tier_case(seed)
+    o = O.Oracle(p)
+    total = int(tiers["mem"].sum())
+    for c in range(10):
+        row = o.random_row(5, c)
+        prev = None
+        for cap in range(0, total + 2, max(1, total // 12)):
+            e = o.estimate_tiered(row, dict(tiers, cap=np.full(p.D, cap, np.int32)))
+            if prev is not None:
+                assert np.all(e["wt"] <= prev + 1e-9 * np.maximum(1.0, prev))
+            prev = e["wt"]
+            assert np.all(e["cold"] <= 1)

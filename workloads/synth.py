@@ -293,6 +293,32 @@ def edf_row(p: "Problem") -> np.ndarray:
     return queue_row(np.argsort(p.slo, kind="stable"), p.G, p.Q)
 
 
+# Two-tier model swapping (R20) [SYNTHETIC]:
+# fp16 weights (2 B/param) of the 7B / 13B / 70B-like models, the host CPU
+# memory an A100-like / A10-like instance can give to warm models, and the
+# registry (storage) read bandwidth that a cold model pays before its swap.
+MODEL_MEM_GB = (14, 26, 140, 140)
+CPU_CAP_GB = (200, 96)
+DISK_GBPS = (2.0, 1.0)
+
+
+def make_tiers(models=(0, 1, 2, 3), dev_rows=(0,)) -> dict:
+    """Tier inputs of qlm_set_tiers / the oracle: mem int32 [M] (GB), cap int32
+    [D] (GB), load f64 [D, M] = mem / disk bandwidth (s)."""
+    mem = np.array([MODEL_MEM_GB[m] for m in models], np.int32)
+    cap = np.array([CPU_CAP_GB[d] for d in dev_rows], np.int32)
+    load = np.array([[MODEL_MEM_GB[m] / DISK_GBPS[d] for m in models] for d in dev_rows])
+    return dict(mem=mem, cap=cap, load=load)
+
+
+def make_random_tiers(rng: np.random.Generator, M: int, D: int) -> dict:
+    """Random tier inputs: sizes 1..40 units, budgets 0..(sum of sizes), loads 0..60 s."""
+    mem = rng.integers(1, 41, M).astype(np.int32)
+    cap = rng.integers(0, int(mem.sum()) + 1, D).astype(np.int32)
+    load = rng.uniform(0.0, 60.0, (D, M))
+    return dict(mem=mem, cap=cap, load=load)
+
+
 # name -> (problem factory, candidate kind, candidate count / trials)
 CONFIGS = {
     "C1": dict(desc="4 groups, 1 model, 1 queue: all 24 orderings (ENUM)",
