@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define QLM_ABI_VERSION 2
+#define QLM_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define QLM_API __attribute__((visibility("default")))
@@ -195,6 +195,37 @@ QLM_API int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best
  * work per candidate: meant for evaluating winners and short lists.        */
 QLM_API int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac,
                            float *s1_req, void *stream);
+
+/* Two-tier (warm / cold) model swapping (R20):
+ * every model goes storage -> CPU memory -> GPU memory; "models present
+ * later in the virtual queue are warm and placed in the CPU memory until all
+ * the CPU memory is exhausted", the rest are cold.  Per queue on device d,
+ * the swap targets in order of their first transition (Eq. 9, m_{-1} =
+ * resident) are warm while the sizes taken so far plus model_mem[m] fit in
+ * cpu_cap[d]; from the first target that does not fit, CPU memory is
+ * exhausted and every new target is cold.  A cold transition adds
+ * load_s[d][m] to the swap: trans = tail + (swap + load) (R1/R2).        */
+typedef struct {
+    const int32_t *model_mem; /* host [M] >= 1: model size (integer units, e.g. GB) */
+    const int32_t *cpu_cap;   /* host [D] >= 0: CPU memory of a device-d instance    */
+    const double *load_s;     /* host [D][M] >= 0: storage -> CPU load time (s)      */
+} qlm_tiers;
+
+/* Set (deep copy, synchronous) or clear (tiers = NULL) the context's tier
+ * tables.  Errors: QLM_EINVAL (M > 32, a NULL array, a size < 1, a negative
+ * cap, a negative or non-finite load; the message names it), QLM_ERANGE
+ * (sum of model_mem > 2^24).                                               */
+QLM_API int qlm_set_tiers(qlm_ctx *ctx, const qlm_tiers *tiers);
+
+/* qlm_score_estimate under two-tier swapping (R20): bulk estimates
+ * (group-major fp32 [G][count]), per-candidate s1 / s2 / n_over ([count])
+ * and the argmin record, every output nullable.  Asynchronous.  One thread
+ * per candidate; wt / V follow the oracle's operation order.  Errors:
+ * QLM_EINVAL if qlm_set_tiers has not been called, else as
+ * qlm_score_estimate.                                                      */
+QLM_API int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
+                              float *wt_std, float *viol, float *s1, float *s2, int32_t *n_over,
+                              qlm_record *rec, void *stream);
 
 /* Local-search step (R18), asynchronous on `stream`:
  * if *rec (e.g. from qlm_best_ordering_async over NEIGHBOR candidates of

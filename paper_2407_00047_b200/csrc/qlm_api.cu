@@ -63,6 +63,8 @@ struct qlm_ctx {
     double *d_X = nullptr;             // MC: (X / Theta)[D][G][trials]
     int64_t mc_trials = -1;            // trials of the last qlm_mc_sample
     size_t X_cap = 0;
+    void *d_tier = nullptr;            // two-tier swapping (R20): mem [M] | cap [D] | load [D][M]
+    bool has_tiers = false;
     std::vector<qlm_group> groups;
     std::vector<qlm_queue> queues;
     std::vector<double> prof;              // theta|prefill|eps|dec|maxo [D*M] each, swap [D*M*M]
@@ -409,7 +411,7 @@ void qlm_destroy(qlm_ctx *ctx) {
     cudaSetDevice(ctx->device);
     void *ptrs[] = {ctx->d_raw, ctx->d_tab, ctx->d_block_recs, ctx->d_counter, ctx->d_rec,
                     ctx->d_dec_out, ctx->d_bad, ctx->d_X, ctx->d_ilv, ctx->d_chunk_recs,
-                    ctx->d_ls_rec};
+                    ctx->d_ls_rec, ctx->d_tier};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     delete ctx;
@@ -701,6 +703,80 @@ int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac
     ScanParams p = base_params(ctx, cand);
     cudaError_t e = launch_req(p, ctx->d_groups, frac, s1_req, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "request-violations kernel");
+}
+
+int qlm_set_tiers(qlm_ctx *ctx, const qlm_tiers *tiers) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    int rc = check_dev(ctx);
+    if (rc) return rc;
+    if (!tiers) {
+        ctx->has_tiers = false;
+        return QLM_OK;
+    }
+    const int D = ctx->dm.D, M = ctx->dm.M;
+    if (M > 32) return fail(QLM_EINVAL, "two-tier swapping needs M=%d <= 32", M);
+    if (!tiers->model_mem || !tiers->cpu_cap || !tiers->load_s)
+        return fail(QLM_EINVAL, "tiers.model_mem / cpu_cap / load_s must be non-NULL");
+    int64_t total = 0;
+    for (int m = 0; m < M; ++m) {
+        if (tiers->model_mem[m] < 1)
+            return fail(QLM_EINVAL, "tiers.model_mem[%d]=%d must be >= 1", m, tiers->model_mem[m]);
+        total += tiers->model_mem[m];
+    }
+    if (total > (1 << 24)) return fail(QLM_ERANGE, "sum of tiers.model_mem=%lld > 2^24", (long long)total);
+    for (int d = 0; d < D; ++d)
+        if (tiers->cpu_cap[d] < 0)
+            return fail(QLM_EINVAL, "tiers.cpu_cap[%d]=%d must be >= 0", d, tiers->cpu_cap[d]);
+    for (int k = 0; k < D * M; ++k)
+        if (!(tiers->load_s[k] >= 0.0) || !is_fin(tiers->load_s[k]))
+            return fail(QLM_EINVAL, "tiers.load_s[%d][%d]=%g must be >= 0 and finite", k / M, k % M,
+                        tiers->load_s[k]);
+    const size_t o_cap = a16((size_t)M * 4), o_load = a16(o_cap + (size_t)D * 4);
+    const size_t bytes = o_load + (size_t)D * M * 8;
+    if (!ctx->d_tier) {
+        cudaError_t e = cudaMalloc(&ctx->d_tier, bytes);
+        if (e != cudaSuccess) {
+            ctx->d_tier = nullptr;
+            return fail(QLM_ENOMEM, "tier tables: %s", cudaGetErrorString(e));
+        }
+    }
+    std::vector<uint8_t> h(bytes, 0);
+    memcpy(h.data(), tiers->model_mem, (size_t)M * 4);
+    memcpy(h.data() + o_cap, tiers->cpu_cap, (size_t)D * 4);
+    memcpy(h.data() + o_load, tiers->load_s, (size_t)D * M * 8);
+    cudaError_t e = cudaMemcpy(ctx->d_tier, h.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "upload tier tables");
+    ctx->has_tiers = true;
+    return QLM_OK;
+}
+
+int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
+                              float *wt_std, float *viol, float *s1, float *s2, int32_t *n_over,
+                              qlm_record *rec, void *stream) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    if (!ctx->has_tiers) return fail(QLM_EINVAL, "no tier tables: call qlm_set_tiers first");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cand->count == 0) {
+        if (!rec) return QLM_OK;
+        const qlm_record none = {~0ull, -1};
+        cudaError_t e = cudaMemcpyAsync(rec, &none, sizeof none, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e == cudaSuccess ? QLM_OK : cuda_fail(e, "empty record");
+    }
+    if (!wt_mean && !wt_std && !viol && !s1 && !s2 && !n_over && !rec) return QLM_OK;
+    ScanParams p = base_params(ctx, cand);
+    p.wt = wt_mean; p.sd = wt_std; p.vo = viol;
+    p.s1 = s1; p.s2 = s2; p.n_over = n_over; p.out_rec = rec;
+    const int M = ctx->dm.M, D = ctx->dm.D;
+    const size_t o_cap = a16((size_t)M * 4), o_load = a16(o_cap + (size_t)D * 4);
+    uint8_t *t = static_cast<uint8_t *>(ctx->d_tier);
+    p.t_mem = reinterpret_cast<const int32_t *>(t);
+    p.t_cap = reinterpret_cast<const int32_t *>(t + o_cap);
+    p.t_load = reinterpret_cast<const double *>(t + o_load);
+    cudaError_t e = launch_tier(p, st);
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "tier kernel");
 }
 
 }  // extern "C"

@@ -30,6 +30,9 @@ struct ScanParams {
     uint32_t *ilv;             // large-T RANDOM: word-interleaved row scratch [words][ilv_cap]
     int64_t ilv_cap;           // candidates per chunk that fit the scratch
     qlm_record *chunk_recs;    // [2] running argmin across chunks
+    const int32_t *t_mem;      // two-tier swapping (R20): model sizes [M]
+    const int32_t *t_cap;      // CPU memory per device row [D]
+    const double *t_load;      // storage -> CPU load time [D][M]
 };
 
 // Internal candidate kind: rows materialised word-interleaved by fy_rows_kernel
@@ -45,10 +48,12 @@ cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
                          const Tables &tb, cudaStream_t st);
 cudaError_t launch_scan(ScanParams p, cudaStream_t st);
 cudaError_t launch_ws(ScanParams p, cudaStream_t st);      // warp-specialised fast path
+cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st); // same, two-tier swapping (R20)
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st);   // ws, else scan
 cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per candidate (large G)
 cudaError_t launch_req(const ScanParams &p, const qlm_group *groups, float *frac, float *s1r,
                        cudaStream_t st);                            // request-level (R19)
+cudaError_t launch_tier(const ScanParams &p, cudaStream_t st);     // two-tier swapping (R20)
 cudaError_t launch_adopt(const Dims &dm, const Cand &cd, const qlm_record *rec, qlm_record *inc,
                          cudaStream_t st);                          // local-search step (R18)
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,

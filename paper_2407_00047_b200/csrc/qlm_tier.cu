@@ -1,0 +1,258 @@
+// qlm_tier.cu -- two-tier (warm / cold) model swapping in the Eq. 10 scan
+// (DESIGN R20).
+//
+// Models later in a virtual queue are warm in the instance's CPU memory
+// until it is exhausted; the rest are cold in the registry and pay a
+// storage -> CPU load before their CPU -> GPU swap.  Per queue, the swap
+// targets in order of their first transition take CPU memory while it lasts
+// (strict prefix); a model keeps its tier for every later transition into it.
+//
+// One thread per candidate, like the general scan kernel: the row streams
+// through the candidate generators of qlm_device.cuh, the thread walks it
+// once, carrying the queue's tier state in four registers (seen / warm model
+// bit masks, CPU memory taken, exhausted flag).  Each transition adds ONE
+// precomputed fp64 term -- tail + swap (warm) or tail + (swap + load)
+// (cold) -- in the oracle's operation order, so wt / V are bit-identical to
+// or_estimate_row_tiered; with every target warm the kernel reproduces the
+// untiered scan kernel bit for bit (same S1 accumulators, same order).
+// Bulk outputs are staged per block ([3][G][blk] fp32) and leave as
+// coalesced 128-B warp stores, or go straight to HBM when no tile fits.
+#include <cuda_runtime.h>
+
+#include "qlm_device.cuh"
+#include "qlm_launch.h"
+#include "qlm_argmin.cuh"
+
+namespace qlm {
+
+struct TierSmem {
+    int off_g, off_ab, off_q, off_trw, off_trc, off_mem, off_cap, off_scratch, off_stage;
+    int blk, stage;
+};
+
+template <int KIND, typename TOK, typename F>
+__device__ __forceinline__ void tier_tokens(const Cand &cd, int T, uint8_t *scratch, int blk,
+                                            int64_t loc, int64_t c, F &&f) {
+    if constexpr (KIND == QLM_CAND_RANDOM) {
+        fy_materialise<TOK>(scratch, blk, threadIdx.x, T, cd.seed, (uint64_t)c);
+        tokens_scratch<TOK>(scratch, blk, threadIdx.x, T, f);
+    } else if constexpr (KIND == QLM_CAND_EXPLICIT) {
+        tokens_explicit<TOK>(cd.rows + loc * cd.stride, T, f);
+    } else if constexpr (KIND == QLM_CAND_NEIGHBOR) {
+        tokens_neighbor<TOK>(cd, T, (uint64_t)c, f);
+    } else {
+        tokens_enum((uint64_t)c, T, f);
+    }
+}
+
+template <int KIND, typename TOK>
+__global__ void __launch_bounds__(128) tier_kernel(const ScanParams p, const TierSmem L) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int tid = threadIdx.x, blk = blockDim.x;
+    const Dims dm = p.dm;
+    const int G = dm.G, Q = dm.Q, T = dm.T, M = dm.M, D = dm.D;
+
+    // ---- tables -> shared memory ----
+    GRec *sg = reinterpret_cast<GRec *>(smem + L.off_g);
+    for (int i = tid; i < G; i += blk) sg[i] = p.tb.grec[i];
+    double2 *sab = reinterpret_cast<double2 *>(smem + L.off_ab);
+    for (int i = tid; i < D * G; i += blk) sab[i] = p.tb.ab[i];
+    QRec *sq = reinterpret_cast<QRec *>(smem + L.off_q);
+    for (int i = tid; i < Q; i += blk) sq[i] = p.tb.qrec[i];
+    // transition terms, rows p' < M: previous model p'; p' >= M: nothing ran
+    // yet on resident p' - M (R4).  warm: tail + swap; cold: tail + (swap + load)
+    double *trw = reinterpret_cast<double *>(smem + L.off_trw);
+    double *trc = reinterpret_cast<double *>(smem + L.off_trc);
+    for (int i = tid; i < D * 2 * M * M; i += blk) {
+        const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
+        const int from = pp < M ? pp : pp - M;
+        const double sw = p.tb.swap[(d * M + from) * M + m];
+        const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
+        const double ld = m != from ? p.t_load[d * M + m] : 0.0;
+        trw[i] = __dadd_rn(tl, sw);
+        trc[i] = __dadd_rn(tl, __dadd_rn(sw, ld));
+    }
+    int *smem_m = reinterpret_cast<int *>(smem + L.off_mem);
+    for (int i = tid; i < M; i += blk) smem_m[i] = p.t_mem[i];
+    int *scap = reinterpret_cast<int *>(smem + L.off_cap);
+    for (int i = tid; i < D; i += blk) scap[i] = p.t_cap[i];
+    uint8_t *scratch = smem + L.off_scratch;
+    __syncthreads();
+
+    const Cand cd = p.cd;
+    int64_t first = cd.first;
+    bool none = false;
+    if (cd.first_from) {
+        first = cd.first_from->index;
+        none = first < 0;
+    }
+    const double zc2 = p.zc2;
+    const float alpha = p.alpha;
+    const int64_t count = none ? 0 : cd.count;
+    float *const gout[3] = {p.wt, p.sd, p.vo};
+    float *st[3] = {nullptr, nullptr, nullptr};
+    if (L.stage) {
+        st[0] = reinterpret_cast<float *>(smem + L.off_stage);
+        st[1] = st[0] + (size_t)G * blk;
+        st[2] = st[1] + (size_t)G * blk;
+    }
+    const bool bulk = p.wt || p.sd || p.vo;
+    const double den = *p.tb.den;
+    uint64_t bkey = ~0ull;
+    int64_t bidx = -1;
+    const int64_t ntiles = (count + blk - 1) / blk;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t c0 = tile * blk, loc = c0 + tid;
+        const int nvalid = (int)min((int64_t)blk, count - c0);
+        if (tid < nvalid) {
+            // queue state (R4/R12) and tier state (R20)
+            int q = 0, d = sq[0].d, prow = sq[0].backlog ? sq[0].r : M + sq[0].r;
+            double A = sq[0].bmean, B = sq[0].bvar, S2 = 0.0;
+            uint32_t seen = 0u, warm = 0u;
+            int cum = 0;
+            bool exh = false;
+            float acc1 = 0.0f, acc2 = 0.0f;
+            int over = 0;
+            tier_tokens<KIND, TOK>(cd, T, scratch, blk, loc, first + loc, [&](int tok) {
+                if (tok >= G) {                              // separator: next queue, fresh CPU memory
+                    q = q + 1 < Q ? q + 1 : Q - 1;
+                    const QRec r = sq[q];
+                    d = r.d; prow = r.backlog ? r.r : M + r.r;
+                    A = r.bmean; B = r.bvar;
+                    seen = 0u; warm = 0u; cum = 0; exh = false;
+                    return;
+                }
+                const GRec g = sg[tok];
+                const int m = g.model;
+                const int pm = prow < M ? prow : prow - M;
+                bool cold = false;
+                if (m != pm) {                               // a transition (Eq. 9)
+                    const uint32_t bit = 1u << m;
+                    if (!(seen & bit)) {                     // first transition into m
+                        seen |= bit;
+                        if (!exh && cum + smem_m[m] <= scap[d]) { warm |= bit; cum += smem_m[m]; }
+                        else exh = true;
+                    }
+                    cold = !(warm & bit);
+                }
+                const int ti = (d * 2 * M + prow) * M + m;
+                A = __dadd_rn(A, cold ? trc[ti] : trw[ti]);
+                const double wt = A, V = B;                  // exclusive (R5)
+                const double2 ab = sab[d * G + tok];
+                A = __dadd_rn(A, ab.x);
+                B = __dadd_rn(B, ab.y);
+                prow = m;
+                const double slack = __dsub_rn(g.slo, wt);
+                bool clamped;
+                const float v = violation(slack, V, zc2, clamped);
+                S2 = __dsub_rn(S2, slack);
+                if (clamped) acc1 = fmaf((float)g.n, v, acc1);
+                else acc2 = fmaf((float)g.n, v, acc2);
+                over += v > alpha;
+                if (bulk) {
+                    const float Vf = (float)V;
+                    const float o3[3] = {(float)wt, Vf * rsqrt_approx(fmaxf(Vf, 1e-30f)), v};
+                    if (L.stage) {
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) st[a][tok * blk + tid] = o3[a];
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < 3; ++a)
+                            if (gout[a]) gout[a][(int64_t)tok * count + loc] = o3[a];
+                    }
+                }
+            });
+            const float s1 = (float)(((double)acc1 + (double)acc2) / den);   // R11
+            const float s2 = (float)S2;
+            if (p.s1) p.s1[loc] = s1;
+            if (p.s2) p.s2[loc] = s2;
+            if (p.n_over) p.n_over[loc] = over;
+            const uint64_t key = make_key(s1, s2);
+            if (better(key, first + loc, bkey, bidx)) { bkey = key; bidx = first + loc; }
+        }
+        if (bulk && L.stage) {                               // coalesced copy-out of the tile
+            __syncthreads();
+            if (tid < nvalid)
+                for (int a = 0; a < 3; ++a)
+                    if (gout[a])
+                        for (int g = 0; g < G; ++g) gout[a][(int64_t)g * count + loc] = st[a][g * blk + tid];
+            __syncthreads();
+        }
+    }
+    if (p.out_rec) {
+        if (none) {
+            if (blockIdx.x == 0 && tid == 0) { p.out_rec->key = ~0ull; p.out_rec->index = -1; }
+            return;
+        }
+        block_grid_argmin(p, bkey, bidx);
+    }
+}
+
+template <int KIND, typename TOK>
+static cudaError_t launch_tier_t(const ScanParams &p, cudaStream_t st) {
+    auto kern = tier_kernel<KIND, TOK>;
+    const Dims &dm = p.dm;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const bool bulk = p.wt || p.sd || p.vo;
+    auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+    TierSmem L{};
+    size_t total = 0;
+    for (int blk = 128; blk >= 32; blk >>= 1) {
+        for (int stage = bulk ? 1 : 0; stage >= 0; --stage) {
+            size_t o = 0;
+            L.off_g = (int)o;   o = a16(o + (size_t)dm.G * sizeof(GRec));
+            L.off_ab = (int)o;  o = a16(o + (size_t)dm.D * dm.G * sizeof(double2));
+            L.off_q = (int)o;   o = a16(o + (size_t)dm.Q * sizeof(QRec));
+            L.off_trw = (int)o; o = a16(o + (size_t)dm.D * 2 * dm.M * dm.M * 8);
+            L.off_trc = (int)o; o = a16(o + (size_t)dm.D * 2 * dm.M * dm.M * 8);
+            L.off_mem = (int)o; o = a16(o + (size_t)dm.M * 4);
+            L.off_cap = (int)o; o = a16(o + (size_t)dm.D * 4);
+            L.off_scratch = (int)o;
+            if (KIND == QLM_CAND_RANDOM) o = a16(o + (size_t)((dm.T * sizeof(TOK) + 3) / 4) * 4 * blk);
+            L.off_stage = (int)o;
+            if (stage) o += (size_t)3 * dm.G * blk * 4;
+            L.blk = blk;
+            L.stage = stage;
+            total = o;
+            if (o <= (size_t)optin && (!stage || o <= 110 * 1024)) break;
+            total = 0;
+        }
+        if (total) break;
+    }
+    if (!total) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)total);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L.blk, total);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t ntiles = (p.cd.count + L.blk - 1) / L.blk;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > ntiles) grid = ntiles;
+    if (grid > p.max_blocks) grid = p.max_blocks;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, L.blk, total, st>>>(p, L);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tier(const ScanParams &p, cudaStream_t st) {
+    const cudaError_t ws = launch_ws_tier(p, st);            // warp-specialised fast path
+    if (ws != cudaErrorNotSupported) return ws;
+    const bool u8 = p.dm.T <= 256;
+    switch (p.cd.kind) {
+    case QLM_CAND_RANDOM:
+        return u8 ? launch_tier_t<QLM_CAND_RANDOM, uint8_t>(p, st) : launch_tier_t<QLM_CAND_RANDOM, uint16_t>(p, st);
+    case QLM_CAND_EXPLICIT:
+        return p.cd.tb == 1 ? launch_tier_t<QLM_CAND_EXPLICIT, uint8_t>(p, st)
+                            : launch_tier_t<QLM_CAND_EXPLICIT, uint16_t>(p, st);
+    case QLM_CAND_NEIGHBOR:
+        return p.cd.tb == 1 ? launch_tier_t<QLM_CAND_NEIGHBOR, uint8_t>(p, st)
+                            : launch_tier_t<QLM_CAND_NEIGHBOR, uint16_t>(p, st);
+    default:
+        return launch_tier_t<QLM_CAND_ENUM, uint8_t>(p, st);
+    }
+}
+
+}  // namespace qlm

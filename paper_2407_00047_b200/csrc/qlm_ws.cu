@@ -38,7 +38,7 @@ struct alignas(64) WsParams {
     ScanParams p;
     int pairs;             // W
     int tw;                // 32-bit words per row slot column
-    int off_rows, off_stage, off_bar, off_pend;
+    int off_rows, off_stage, off_bar, off_pend, off_tmem;
     int stage_floats;      // per consumer warp: 3 * G * 32
     int use_tma;
 };
@@ -141,7 +141,7 @@ struct alignas(16) WsQ {      // 32 B (two LDS.128)
     int prow0;               // transition-table row at the queue's start (R4)
     int dG;                  // d * (G + 1): device base into the ab table
     int dbase;               // d * 2M * M: device base into the transition table
-    int pad;
+    int tier;                // R20: (CPU memory cap << 6) | resident model (tiered kernels only)
 };
 
 struct Acc {
@@ -149,6 +149,10 @@ struct Acc {
     float acc1;              // sum n_i v_i over clamped slots (v in {0, 1}: exact)
     float acc2;              // sum n_i v_i over unclamped slots, row order
     int prow, dG, dbase, q, over, npend;
+    // two-tier swapping (R20): previous model, seen / warm target masks,
+    // CPU memory taken, exhausted flag, the queue's CPU memory
+    int pmod, cum, exh, capd;
+    uint32_t seen, warm;
 };
 
 // Unclamped slots (|z| < z_clamp, ~1-2 % of slots) are queued per lane --
@@ -180,12 +184,13 @@ __device__ __forceinline__ void flush_pending(Pend *pq, const WsG *__restrict__ 
     a.npend = 0;
 }
 
-template <typename TOK, int RS, bool SCORE, bool PAD>
+template <typename TOK, int RS, bool SCORE, bool PAD, bool TIER>
 __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const double2 *__restrict__ sabl,
                                              const double *__restrict__ str, const WsQ *__restrict__ sq,
                                              uint32_t word, int nvalid_tok, int G, int M, int lane,
                                              float zc2f, float alpha, float *st, int arr_stride,
-                                             Pend *pq, Acc &a) {
+                                             Pend *pq, Acc &a, const int *__restrict__ smemsz,
+                                             int cold_off) {
     constexpr int K = 4 / (int)sizeof(TOK);
     int isbar[K], tg[K];
     WsG g[K];
@@ -207,17 +212,40 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
             g[k].model = (int)(uint32_t)(hi >> 32);
         }
         if (isbar[k]) r[k] = sq[q];                          // only separator lanes read
-        else { r[k].bmean = 0.0; r[k].bvar = 0.0; r[k].prow0 = 0; r[k].dG = 0; r[k].dbase = 0; }
+        else { r[k].bmean = 0.0; r[k].bvar = 0.0; r[k].prow0 = 0; r[k].dG = 0; r[k].dbase = 0; r[k].tier = 0; }
     }
     // (ii) per-slot transition row and device base
     int pk[K], dk[K];
     int prow = a.prow, dG = a.dG, dbase = a.dbase;
+    bool cold[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         pk[k] = prow;
         dk[k] = dG;
+        cold[k] = false;
         const bool pad = PAD && k >= nvalid_tok;
         if (!pad) {
+            if constexpr (TIER) {
+                // R20: per queue, swap targets in first-transition order are warm
+                // while they fit the CPU memory (strict prefix); branch-free
+                const int m = g[k].model;
+                const uint32_t bit = 1u << m;
+                const bool trn = !isbar[k] && m != a.pmod;
+                const bool firstT = trn && !(a.seen & bit);
+                const int need = a.cum + smemsz[m];
+                const bool fits = !a.exh && need <= a.capd;
+                a.seen |= firstT ? bit : 0u;
+                a.warm |= (firstT && fits) ? bit : 0u;
+                a.cum = (firstT && fits) ? need : a.cum;
+                a.exh = (a.exh || (firstT && !fits)) ? 1 : 0;
+                cold[k] = trn && !(a.warm & bit);
+                a.pmod = isbar[k] ? (r[k].tier & 63) : m;
+                a.capd = isbar[k] ? (r[k].tier >> 6) : a.capd;
+                a.seen = isbar[k] ? 0u : a.seen;
+                a.warm = isbar[k] ? 0u : a.warm;
+                a.cum = isbar[k] ? 0 : a.cum;
+                a.exh = isbar[k] ? 0 : a.exh;
+            }
             prow = isbar[k] ? r[k].prow0 : dbase + g[k].model * M;
             dG = isbar[k] ? r[k].dG : dG;
             dbase = isbar[k] ? r[k].dbase : dbase;
@@ -229,7 +257,8 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         ab[k] = sabl[(dk[k] + tg[k]) << RS];
-        tr[k] = str[(pk[k] + g[k].model) << kTrRs];          // 16 replicas: conflict-free
+        const int ti = (pk[k] + g[k].model) << kTrRs;        // 16 replicas: conflict-free
+        tr[k] = str[TIER && cold[k] ? ti + cold_off : ti];   // R20: cold table follows the warm one
     }
     // (iv) the Eq. 10 chain (operation order identical to the sequential definition)
     double wt[K], V[K];
@@ -280,7 +309,7 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
     }
 }
 
-template <int KIND, typename TOK, bool SCORE, int RS>
+template <int KIND, typename TOK, bool SCORE, int RS, bool TIER>
 __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsParams w) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const ScanParams &p = w.p;
@@ -309,6 +338,12 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         sab[i] = gi < G ? p.tb.ab[d * G + gi] : make_double2(0.0, 0.0);
     }
     WsQ *sq = reinterpret_cast<WsQ *>(smem + p.off_q);
+    int *smemsz = reinterpret_cast<int *>(smem + w.off_tmem);
+    int summem = 0;
+    if constexpr (TIER) {
+        for (int m = 0; m < M; ++m) summem += p.t_mem[m];
+        for (int i = tid; i < M; i += blockDim.x) smemsz[i] = p.t_mem[i];
+    }
     for (int i = tid; i < T + 1; i += blockDim.x) {
         const QRec x = p.tb.qrec[i < Q ? i : Q - 1];
         WsQ r;
@@ -316,17 +351,19 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         r.prow0 = (x.d * 2 * M + (x.backlog ? x.r : M + x.r)) * M;
         r.dG = x.d * (G + 1);
         r.dbase = x.d * 2 * M * M;
-        r.pad = 0;
+        r.tier = TIER ? (min(p.t_cap[x.d], summem) << 6) | x.r : 0;   // cap >= sum(mem) == unbounded
         sq[i] = r;
     }
     double *str = reinterpret_cast<double *>(smem + p.off_tr);
-    for (int i = tid; i < ((D * 2 * M * M) << kTrRs); i += blockDim.x) {
-        const int e = i >> kTrRs;
+    const int ntr = (D * 2 * M * M) << kTrRs;
+    for (int i = tid; i < (TIER ? 2 * ntr : ntr); i += blockDim.x) {
+        const int e = (i % ntr) >> kTrRs;
         const int m = e % M, pp = (e / M) % (2 * M), d = e / (2 * M * M);
         const int from = pp < M ? pp : pp - M;
         const double sw = p.tb.swap[(d * M + from) * M + m];
         const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
-        str[i] = __dadd_rn(tl, sw);                      // one transition term (R2/R3)
+        if (i < ntr) str[i] = __dadd_rn(tl, sw);         // one transition term (R2/R3)
+        else str[i] = __dadd_rn(tl, __dadd_rn(sw, m != from ? p.t_load[d * M + m] : 0.0));   // cold (R20)
     }
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + w.off_bar);
     uint64_t *empty = full + 2 * W;
@@ -387,19 +424,21 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
                 const WsQ r0 = sq[0];
                 a.A = r0.bmean; a.B = r0.bvar; a.prow = r0.prow0; a.dG = r0.dG; a.dbase = r0.dbase;
                 a.q = 0; a.S2 = 0.0; a.acc1 = 0.0f; a.acc2 = 0.0f; a.over = 0; a.npend = 0;
+                a.pmod = r0.tier & 63; a.capd = r0.tier >> 6; a.cum = 0; a.exh = 0; a.seen = 0u; a.warm = 0u;
                 uint32_t cur = w32[lane];
                 for (int wi = 0; wi < full_words; ++wi) {
                     const uint32_t nxt = w32[(wi + 1 < tw ? wi + 1 : wi) * 32 + lane];   // prefetch
-                    consume_word<TOK, RS, SCORE, false>(sgl, sabl, strl, sq, cur, EPW, G,
-                                                        M, lane, zc2f, alpha, st, arr, pq, a);
+                    consume_word<TOK, RS, SCORE, false, TIER>(sgl, sabl, strl, sq, cur, EPW, G,
+                                                              M, lane, zc2f, alpha, st, arr, pq, a,
+                                                              smemsz, ntr);
                     cur = nxt;
                     if (__any_sync(__activemask(), a.npend > kPend - EPW))
                         flush_pending<SCORE, (1 << RS)>(pq, sgl_rs, lane, alpha, st2, a);
                 }
                 if (full_words * EPW < T)
-                    consume_word<TOK, RS, SCORE, true>(sgl, sabl, strl, sq, cur,
-                                                       T - full_words * EPW, G, M, lane, zc2f, alpha,
-                                                       st, arr, pq, a);
+                    consume_word<TOK, RS, SCORE, true, TIER>(sgl, sabl, strl, sq, cur,
+                                                             T - full_words * EPW, G, M, lane, zc2f,
+                                                             alpha, st, arr, pq, a, smemsz, ntr);
                 flush_pending<SCORE, (1 << RS)>(pq, sgl_rs, lane, alpha, st2, a);
                 if constexpr (SCORE) {
                     const float s1 = (float)(((double)a.acc1 + (double)a.acc2) / den);     // R11
@@ -478,7 +517,7 @@ static int env_int_ws(const char *name, int dflt) {
 }
 
 // Shared-memory plan for W pairs; returns total bytes.
-static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
+static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage, bool tier) {
     ScanParams &p = w.p;
     const Dims &dm = p.dm;
     size_t off = 0;
@@ -486,7 +525,8 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage) {
     p.off_grec = (int)off; off = a16(off + ((size_t)(dm.G + 1) << rs) * sizeof(WsG));
     p.off_ab = (int)off;   off = a16(off + ((size_t)dm.D * (dm.G + 1) << rs) * sizeof(double2));
     p.off_q = (int)off;    off = a16(off + (size_t)(dm.T + 1) * sizeof(WsQ));
-    p.off_tr = (int)off;   off = a16(off + ((size_t)dm.D * 2 * dm.M * dm.M << kTrRs) * sizeof(double));
+    p.off_tr = (int)off;   off = a16(off + ((size_t)dm.D * 2 * dm.M * dm.M << kTrRs) * sizeof(double) * (tier ? 2 : 1));
+    w.off_tmem = (int)off; off = a16(off + (tier ? (size_t)dm.M * 4 : 0));
     const int epw = 4 / tok_bytes;
     w.tw = (dm.T + epw - 1) / epw;
     w.off_rows = (int)off; off = a16(off + (size_t)2 * W * w.tw * 128);
@@ -515,9 +555,9 @@ static size_t ws_max_dyn(K kern) {
     return m;
 }
 
-template <int KIND, typename TOK, bool SCORE, int RS>
+template <int KIND, typename TOK, bool SCORE, int RS, bool TIER>
 static cudaError_t launch_ws_rs(WsParams &w, size_t smem, int W, cudaStream_t st) {
-    auto kern = ws_kernel<KIND, TOK, SCORE, RS>;
+    auto kern = ws_kernel<KIND, TOK, SCORE, RS, TIER>;
     static size_t lim = 0;
     if (!lim) lim = ws_max_dyn(kern);
     if (!lim || smem > lim) return cudaErrorNotSupported;
@@ -532,7 +572,7 @@ static cudaError_t launch_ws_rs(WsParams &w, size_t smem, int W, cudaStream_t st
     return cudaGetLastError();
 }
 
-template <int KIND, typename TOK, bool SCORE>
+template <int KIND, typename TOK, bool SCORE, bool TIER>
 static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
     constexpr bool STAGE = true;
     const size_t lim = 227 * 1024 - 2048;
@@ -548,7 +588,7 @@ static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
         for (int W = maxW; W >= 1; --W) {
             if (envW && W != envW) continue;
             WsParams t = w;
-            const size_t sm = plan_ws(t, W, rs, sizeof(TOK), STAGE);
+            const size_t sm = plan_ws(t, W, rs, sizeof(TOK), STAGE, TIER);
             if (sm <= lim) {
                 if (W > bestW) { bestW = W; bestRs = rs; bestSmem = sm; }
                 break;
@@ -557,7 +597,7 @@ static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
         if (bestW >= (STAGE ? 6 : 16)) break;
     }
     if (bestW < (STAGE ? 2 : 4)) return cudaErrorNotSupported;
-    plan_ws(w, bestW, bestRs, sizeof(TOK), STAGE);
+    plan_ws(w, bestW, bestRs, sizeof(TOK), STAGE, TIER);
     if (STAGE) {
         const bool aligned = (p0.cd.count % 4 == 0) && (!p0.wt || ((uintptr_t)p0.wt & 15) == 0) &&
                              (!p0.sd || ((uintptr_t)p0.sd & 15) == 0) &&
@@ -568,8 +608,8 @@ static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
         if (ok && p0.vo) ok = make_map(&w.tmap[2], p0.vo, p0.cd.count, p0.dm.G);
         w.use_tma = ok ? 1 : 0;
     }
-    return bestRs == 3 ? launch_ws_rs<KIND, TOK, SCORE, 3>(w, bestSmem, bestW, st)
-                       : launch_ws_rs<KIND, TOK, SCORE, 0>(w, bestSmem, bestW, st);
+    return bestRs == 3 ? launch_ws_rs<KIND, TOK, SCORE, 3, TIER>(w, bestSmem, bestW, st)
+                       : launch_ws_rs<KIND, TOK, SCORE, 0, TIER>(w, bestSmem, bestW, st);
 }
 
 template <int KIND, typename TOK>
@@ -578,7 +618,25 @@ static cudaError_t launch_ws_k(ScanParams &p, cudaStream_t st) {
     const bool stage = p.wt || p.sd || p.vo;
     if (!stage) return cudaErrorNotSupported;   // score-only: the one-warp-per-32-candidates kernel is faster
     if ((size_t)3 * (p.dm.G + 1) * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
-    return score ? launch_ws_t<KIND, TOK, true>(p, st) : launch_ws_t<KIND, TOK, false>(p, st);
+    return score ? launch_ws_t<KIND, TOK, true, false>(p, st) : launch_ws_t<KIND, TOK, false, false>(p, st);
+}
+
+// Two-tier swapping (R20) through the warp-specialised kernel: RANDOM and
+// EXPLICIT candidates with bulk outputs (the tier kernel covers the rest).
+cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st) {
+    if (p.cd.first_from || p.cd.count < 4096 || env_int_ws("QLM_NO_WS", 0)) return cudaErrorNotSupported;
+    if (!(p.wt || p.sd || p.vo) || p.dm.M > 32) return cudaErrorNotSupported;
+    if ((size_t)3 * (p.dm.G + 1) * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
+    switch (p.cd.kind) {
+    case QLM_CAND_RANDOM:
+        return p.dm.T <= 256 ? launch_ws_t<QLM_CAND_RANDOM, uint8_t, true, true>(p, st)
+                             : launch_ws_t<QLM_CAND_RANDOM, uint16_t, true, true>(p, st);
+    case QLM_CAND_EXPLICIT:
+        return p.dm.T <= 256 ? launch_ws_t<QLM_CAND_EXPLICIT, uint8_t, true, true>(p, st)
+                             : launch_ws_t<QLM_CAND_EXPLICIT, uint16_t, true, true>(p, st);
+    default:
+        return cudaErrorNotSupported;
+    }
 }
 
 // Fast path for large candidate sets; cudaErrorNotSupported -> caller falls back.

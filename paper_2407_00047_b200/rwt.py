@@ -151,6 +151,32 @@ class RwtEstimator:
                                                self._stream(stream)), "qlm_request_violations")
         return frac, s1r
 
+    def set_tiers(self, tiers: dict | None):
+        """Two-tier model swapping (R20): tiers = dict(mem=int32 [M], cap=int32 [D],
+        load=f64 [D, M]) or None to clear."""
+        if tiers is None:
+            L.check(L.lib().qlm_set_tiers(self._h, None), "qlm_set_tiers")
+            return
+        arrs = (np.ascontiguousarray(tiers["mem"], np.int32), np.ascontiguousarray(tiers["cap"], np.int32),
+                np.ascontiguousarray(tiers["load"], np.float64))
+        t = L.Tiers(*[a.ctypes.data for a in arrs])
+        L.check(L.lib().qlm_set_tiers(self._h, C.byref(t)), "qlm_set_tiers")
+
+    def tiered_score_estimate(self, cand: Cand, out=None, scores=True, rec: torch.Tensor | None = None,
+                              stream=None):
+        """qlm_tiered_score_estimate: score_estimate under two-tier swapping (R20)."""
+        out = {} if out is None else out
+        if scores and out.get("s1") is None:
+            out["s1"] = self._empty(cand.count, torch.float32)
+            out["s2"] = self._empty(cand.count, torch.float32)
+        ptr = {k: (out[k].data_ptr() if out.get(k) is not None else None)
+               for k in ("wt", "sd", "v", "s1", "s2", "n_over")}
+        L.check(L.lib().qlm_tiered_score_estimate(self._h, C.byref(cand.c()), ptr["wt"], ptr["sd"], ptr["v"],
+                                                  ptr["s1"], ptr["s2"], ptr["n_over"],
+                                                  None if rec is None else rec.data_ptr(),
+                                                  self._stream(stream)), "qlm_tiered_score_estimate")
+        return out
+
     def adopt_best(self, cand: Cand, rec: torch.Tensor, incumbent: torch.Tensor, stream=None):
         """Device-side local-search step: cand.rows <- winner row if rec beats incumbent."""
         L.check(L.lib().qlm_adopt_best(self._h, C.byref(cand.c()), rec.data_ptr(), incumbent.data_ptr(),

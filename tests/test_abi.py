@@ -155,4 +155,4 @@ def test_null_context_calls_fail_cleanly(lib):
     assert lib.qlm_adopt_best(None, C.byref(cand), None, None, None) == L.QLM_EINVAL
     assert lib.qlm_local_search(None, None, 1, 2, 64, 1, 1, None, None) == L.QLM_EINVAL
     lib.qlm_destroy(None)
-    assert lib.qlm_abi_version() == 2
+    assert lib.qlm_abi_version() == 3

@@ -701,3 +701,131 @@ def test_neighbor_u16_paths_c4_and_local_search_c5():
     row = buf.cpu().numpy()[: p5.T].astype(np.int64) & 0xFFFF
     assert sorted(row) == list(range(p5.T))
     assert O.key32(*o5.score(row)[:2]) <= O.key32(*o5.score(start)[:2])
+
+
+# ------------------------------------------------------------------ N3: two-tier swapping (R20)
+def _tier_out(e, cand):
+    G, n = e.G, cand.count
+    out = {k: torch.full((G, n), -1.0, dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+    out["n_over"] = torch.empty(n, dtype=torch.int32, device="cuda")
+    rec = torch.empty(2, dtype=torch.int64, device="cuda")
+    e.tiered_score_estimate(cand, out=out, rec=rec)
+    torch.cuda.synchronize()
+    return out, rec
+
+
+@pytest.mark.parametrize("cfg,count", [("C2", 3000), ("C3", 1500), ("C5h", 70)])
+def test_tiers_random_vs_oracle(cfg, count):
+    from workloads.synth import make_tiers
+    p = make_config(cfg)
+    tiers = make_tiers((0, 2) if cfg == "C2" else (0, 1, 2, 3), (0, 1) if cfg == "C5h" else (0,))
+    if cfg == "C2":
+        tiers["cap"] = np.array([20], np.int32)      # 14 + 140 GB would all fit the default 200
+    e = est_of(p)
+    e.set_tiers(tiers)
+    first = 777
+    cand = e.random(first, count, seed=1)
+    out, rec = _tier_out(e, cand)
+    ref = O.Oracle(p).tiered_range(tiers, O.RANDOM, first, count, seed=1)
+    # the warp walk follows the oracle's operation order: wt / V bit-identical
+    wt = out["wt"].cpu().numpy().astype(np.float64).T
+    assert np.array_equal(wt, ref["wt"].astype(np.float32).astype(np.float64))
+    if ref["v"] is not None:
+        check_estimates(out, ref)
+    check_scores(out["s1"].cpu().numpy(), out["s2"].cpu().numpy(), ref, p)
+    ok, cstar = argmin_ok(int(rec[1]), ref["s1"], ref["s2"], p, first=first)
+    assert ok, (int(rec[1]), cstar + first)
+    # the tiers matter on these inputs (some candidates pay cold loads)
+    base = O.Oracle(p).estimate_range(O.RANDOM, first, min(count, 200), seed=1)
+    assert np.any(ref["wt"][:200] > base["wt"])
+
+
+def test_tiers_all_warm_equals_untiered_kernel_bit_exact():
+    from workloads.synth import make_tiers
+    p = make_config("C3")
+    t = make_tiers()
+    t["cap"] = np.array([int(t["mem"].sum())], np.int32)
+    e = est_of(p)
+    e.set_tiers(t)
+    cand = e.random(0, 4096, seed=3)
+    out, rec = _tier_out(e, cand)
+    ref = e.score_estimate(cand, out={k: torch.empty((p.G, 4096), device="cuda") for k in ("wt", "sd", "v")},
+                           rec=torch.empty(2, dtype=torch.int64, device="cuda"))
+    torch.cuda.synchronize()
+    for k in ("wt", "sd", "v", "s1", "s2"):
+        assert torch.equal(out[k], ref[k]), k
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_tiers_random_problems_all_kinds(seed):
+    from workloads.synth import make_random_tiers
+    rng = np.random.default_rng(500 + seed)
+    G, Q, M, D = int(rng.integers(3, 40)), int(rng.integers(1, 6)), int(rng.integers(2, 7)), int(rng.integers(1, 3))
+    p = make_random_problem(rng, G, Q, M, D, backlog=bool(seed % 2), sigma_zero=seed == 2)
+    tiers = make_random_tiers(rng, M, D)
+    e = est_of(p)
+    e.set_tiers(tiers)
+    o = O.Oracle(p)
+    n = 700
+    rows = np.stack([O.random_row(9, c, p.T) for c in range(n)])
+    for cand, kw in [(e.random(5, n, seed=2), dict(kind=O.RANDOM, first=5, seed=2)),
+                     (e.explicit(rows_tensor(rows)), dict(kind=O.EXPLICIT, first=0, rows=rows.astype(np.uint8)))]:
+        out, rec = _tier_out(e, cand)
+        ref = o.tiered_range(tiers, kw["kind"], kw["first"], n, seed=kw.get("seed", 0), rows=kw.get("rows"))
+        check_estimates(out, ref)
+        check_scores(out["s1"].cpu().numpy(), out["s2"].cpu().numpy(), ref, p)
+        assert np.array_equal(out["n_over"].cpu().numpy(), ref["n_over"])
+        ok, cstar = argmin_ok(int(rec[1]), ref["s1"], ref["s2"], p, first=kw["first"])
+        assert ok
+
+
+def test_tiers_enum_brute_force_and_edges():
+    from tests.handmade import hand_problem
+    p = hand_problem([1, 2, 1, 3, 0], 25, 200.0, 0.0, 150.0, theta=1000.0, prefill=0.5, eps=1.0,
+                     dtok=0.5, max_out=1.0, swap=20.0, M=4, Q=2)
+    tiers = dict(mem=np.array([5, 2, 3, 1], np.int32), cap=np.array([4], np.int32),
+                 load=np.array([[10.0, 20.0, 30.0, 40.0]]))
+    e = est_of(p)
+    e.set_tiers(tiers)
+    n = math.factorial(p.T)                      # T = 6: all 720 orderings
+    out, rec = _tier_out(e, e.enum(0, n))
+    ref = O.Oracle(p).tiered_range(tiers, O.ENUM, 0, n)
+    check_estimates(out, ref)
+    ok, _ = argmin_ok(int(rec[1]), ref["s1"], ref["s2"], p)
+    assert ok
+    # empty candidate set -> "none" record; errors are named
+    rec2 = torch.zeros(2, dtype=torch.int64, device="cuda")
+    e.tiered_score_estimate(e.random(0, 0, seed=1), rec=rec2)
+    torch.cuda.synchronize()
+    assert int(rec2[1]) == -1
+    from paper_2407_00047_b200 import _lib as L
+    with pytest.raises(L.QlmError, match="model_mem"):
+        e.set_tiers(dict(tiers, mem=np.array([0, 2, 3, 1], np.int32)))
+    e.set_tiers(None)
+    with pytest.raises(L.QlmError, match="qlm_set_tiers"):
+        e.tiered_score_estimate(e.random(0, 10, seed=1))
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_tiers_ws_path_bit_identical_to_thread_kernel(cfg, monkeypatch):
+    # count >= 4096 takes the warp-specialised kernel (TIER variant); QLM_NO_WS
+    # forces the thread-per-candidate tier kernel.  Both add in the oracle's
+    # order and share the S1 accumulator split: outputs must be identical.
+    from workloads.synth import make_tiers
+    p = make_config(cfg)
+    t = make_tiers()
+    e = est_of(p)
+    e.set_tiers(t)
+    n = 8192 + 64
+    cand = e.random(31, n, seed=1)
+    ws, rws = _tier_out(e, cand)
+    monkeypatch.setenv("QLM_NO_WS", "1")
+    th, rth = _tier_out(e, cand)
+    monkeypatch.delenv("QLM_NO_WS")
+    for k in ("wt", "sd", "v", "s1", "s2", "n_over"):
+        assert torch.equal(ws[k], th[k]), k
+    assert torch.equal(rws, rth)
+    ref = O.Oracle(p).tiered_range(t, O.RANDOM, 31, 600, seed=1)
+    wt = ws["wt"][:, :600].cpu().numpy().astype(np.float64).T
+    assert np.array_equal(wt, ref["wt"].astype(np.float32).astype(np.float64))
+    check_scores(ws["s1"][:600].cpu().numpy(), ws["s2"][:600].cpu().numpy(), ref, p)
