@@ -83,6 +83,9 @@ def lib():
         _lib.or_score_row_tiered.restype = C.c_int
         _lib.or_tiered_range.argtypes = [P, T, C.c_int, vp, i32, i64, u64, u64, i64, dp, dp, vp, dp, dp]
         _lib.or_tiered_range.restype = i64
+        _lib.or_form_groups.argtypes = [i32, i32, vp, vp, vp, vp, i32, vp, i32, i32,
+                                        vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]
+        _lib.or_form_groups.restype = i32
     return _lib
 
 
@@ -244,6 +247,30 @@ class Oracle:
         if bad:
             raise ValueError(f"{bad} invalid rows")
         return counts
+
+
+def form_groups(req: dict, M: int, k_per_model, limit: int, max_iter: int = 50) -> dict:
+    """Alg. 1 under reading R21: k-means per model + recursive
+    splitHalf.  req: dict(model int32 [n], slo f64 [n], out int32 [n],
+    feat int32 [n, dims]) in arrival order (workloads.make_requests)."""
+    c = np.ascontiguousarray
+    model, slo = c(req["model"], np.int32), c(req["slo"], np.float64)
+    out, feat = c(req["out"], np.int32), c(req["feat"], np.int32)
+    n, dims = feat.shape
+    k = c(k_per_model, np.int32)
+    label, gof = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    cap = n
+    gm, gn = np.zeros(cap, np.int32), np.zeros(cap, np.int32)
+    gs, gmu, gvar = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+    iters, keff = C.c_int32(), np.zeros(M, np.int32)
+    init = np.full(max(1, int(np.sum(k))), -1, np.int32)
+    G = lib().or_form_groups(n, dims, _ptr(model), _ptr(slo), _ptr(out), _ptr(feat), M, _ptr(k), limit,
+                             max_iter, _ptr(label), _ptr(gof), _ptr(gm), _ptr(gn), _ptr(gs), _ptr(gmu),
+                             _ptr(gvar), cap, C.byref(iters), _ptr(keff), _ptr(init))
+    if G < 0:
+        raise ValueError("invalid requests (model or feature out of range)")
+    return dict(n_groups=G, label=label, group_of=gof, model=gm[:G], n=gn[:G], slo=gs[:G], mu=gmu[:G],
+                var=gvar[:G], iters=iters.value, k_eff=keff, init=init[:int(keff.sum())])
 
 
 def philox4x32_10(ctr, key):

@@ -583,3 +583,167 @@ int64_t or_tiered_range(const or_problem *p, const or_tiers *t, int kind, const 
     free(row);
     return bad;
 }
+
+/* ---- request-group formation (R21; Alg. 1) ----
+ * Alg. 1: groups <- kMeansClustering(requests); every group larger than
+ * avg_batch_size * delta is split in half (splitHalf), the halves appended.
+ * Reading R21:
+ *   - features: dims <= 4 integer coordinates per request in [0, 65535]
+ *     (the caller's quantised model-independent features, e.g. log SLO,
+ *     log input / output tokens: Def. P:L443-447 names them); the model is
+ *     a hard partition: k_m clusters per model m, a request only joins a
+ *     centroid of its own model;
+ *   - initialisation, per model (deterministic farthest point): c_0 = the
+ *     model's first request in arrival order; c_{j+1} = the request with the
+ *     largest squared distance (exact int64) to its nearest chosen centre,
+ *     lowest index on ties; stop early if that distance is 0 (fewer
+ *     distinct points than k_m);
+ *   - Lloyd iterations (at most max_iter): assign every request to the
+ *     nearest centre of its model, d2 = sum_f ((double)x_f - c_f)^2 summed in
+ *     f order, lowest centre index on ties; stop when no label changed;
+ *     otherwise c = (double)(sum of member coords) / (double)count (sums in
+ *     exact integers); an empty cluster keeps its centre;
+ *   - splitHalf (Alg. 1 lines 3-5, applied until no group exceeds the
+ *     limit): a cluster's members in arrival order [lo, hi) with hi - lo >
+ *     limit become [lo, lo + ceil(n/2)) and [lo + ceil(n/2), hi), recursively;
+ *   - groups are numbered cluster by cluster (model, then centre index),
+ *     halves left to right; a group's model is its cluster's, slo = min
+ *     member SLO, mu = S1 / n and var = (n S2 - S1^2) / n^2 with S1, S2 the
+ *     exact integer sums of the members' output tokens and their squares
+ *     ("fitted ... for the request group").
+ * Returns the number of groups (written up to group_cap), -1 on bad input. */
+typedef struct {
+    int32_t *g_model, *g_n;
+    double *g_slo, *g_mu, *g_var;
+} or_group_out;
+
+static int32_t or_emit_halves(const int32_t *members, int32_t lo, int32_t hi, int32_t limit,
+                              const int32_t *out_tok, const double *slo, int32_t model,
+                              int32_t *group_of, const or_group_out *o, int32_t group_cap,
+                              int32_t gid)
+{
+    int32_t n = hi - lo;
+    if (n > limit) {
+        int32_t half = (n + 1) / 2;
+        gid = or_emit_halves(members, lo, lo + half, limit, out_tok, slo, model, group_of, o,
+                             group_cap, gid);
+        return or_emit_halves(members, lo + half, hi, limit, out_tok, slo, model, group_of, o,
+                              group_cap, gid);
+    }
+    int64_t s1 = 0, s2 = 0;
+    double mslo = INFINITY;
+    for (int32_t i = lo; i < hi; ++i) {
+        int32_t r = members[i];
+        group_of[r] = gid;
+        s1 += out_tok[r];
+        s2 += (int64_t)out_tok[r] * out_tok[r];
+        if (slo[r] < mslo) mslo = slo[r];
+    }
+    if (gid < group_cap) {
+        o->g_model[gid] = model;
+        o->g_n[gid] = n;
+        o->g_slo[gid] = mslo;
+        o->g_mu[gid] = (double)s1 / (double)n;
+        o->g_var[gid] = (double)((int64_t)n * s2 - s1 * s1) / ((double)n * (double)n);
+    }
+    return gid + 1;
+}
+
+int32_t or_form_groups(int32_t n, int32_t dims, const int32_t *model, const double *slo,
+                       const int32_t *out_tok, const int32_t *feat, int32_t M,
+                       const int32_t *k_per_model, int32_t limit, int32_t max_iter,
+                       int32_t *label_of, int32_t *group_of, int32_t *g_model, int32_t *g_n,
+                       double *g_slo, double *g_mu, double *g_var, int32_t group_cap,
+                       int32_t *iters_out, int32_t *k_eff_out, int32_t *init_out)
+{
+    if (n < 1 || dims < 1 || dims > 4 || M < 1 || limit < 1) return -1;
+    for (int32_t r = 0; r < n; ++r) {
+        if (model[r] < 0 || model[r] >= M) return -1;
+        for (int32_t f = 0; f < dims; ++f)
+            if (feat[r * dims + f] < 0 || feat[r * dims + f] > 65535) return -1;
+    }
+    /* farthest-point initialisation per model (exact integer distances) */
+    int32_t *ctr_req = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);   /* chosen requests */
+    int32_t *k_eff = (int32_t *)calloc((size_t)M, sizeof(int32_t));
+    int32_t *off = (int32_t *)calloc((size_t)M + 1, sizeof(int32_t));
+    int64_t *mind = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int32_t K = 0;
+    for (int32_t m = 0; m < M; ++m) {
+        off[m] = K;
+        int32_t first = -1;
+        for (int32_t r = 0; r < n; ++r) if (model[r] == m) { first = r; break; }
+        if (first < 0 || k_per_model[m] < 1) continue;
+        ctr_req[K + k_eff[m]++] = first;
+        for (int32_t r = 0; r < n; ++r) mind[r] = INT64_MAX;
+        while (k_eff[m] < k_per_model[m]) {
+            int32_t c = ctr_req[K + k_eff[m] - 1];
+            int64_t best = -1;
+            int32_t arg = -1;
+            for (int32_t r = 0; r < n; ++r) {
+                if (model[r] != m) continue;
+                int64_t d2 = 0;
+                for (int32_t f = 0; f < dims; ++f) {
+                    int64_t t = (int64_t)feat[r * dims + f] - feat[c * dims + f];
+                    d2 += t * t;
+                }
+                if (d2 < mind[r]) mind[r] = d2;
+                if (mind[r] > best) { best = mind[r]; arg = r; }
+            }
+            if (best <= 0) break;                  /* no distinct point left */
+            ctr_req[K + k_eff[m]++] = arg;
+        }
+        K += k_eff[m];
+    }
+    off[M] = K;
+    double *C = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1) * 4);
+    for (int32_t j = 0; j < K; ++j)
+        for (int32_t f = 0; f < dims; ++f) C[j * 4 + f] = (double)feat[ctr_req[j] * dims + f];
+    /* Lloyd iterations */
+    int64_t *sum = (int64_t *)malloc(sizeof(int64_t) * (size_t)(K > 0 ? K : 1) * 5);
+    for (int32_t r = 0; r < n; ++r) label_of[r] = -1;
+    int32_t it = 0;
+    while (it < max_iter) {
+        int changed = 0;
+        for (int32_t r = 0; r < n; ++r) {
+            int32_t m = model[r], arg = -1;
+            double best = INFINITY;
+            for (int32_t j = off[m]; j < off[m] + k_eff[m]; ++j) {
+                double d2 = 0.0;
+                for (int32_t f = 0; f < dims; ++f) {
+                    double t = (double)feat[r * dims + f] - C[j * 4 + f];
+                    d2 = d2 + t * t;
+                }
+                if (d2 < best) { best = d2; arg = j; }
+            }
+            if (arg != label_of[r]) { label_of[r] = arg; changed = 1; }
+        }
+        ++it;
+        if (!changed) break;
+        memset(sum, 0, sizeof(int64_t) * (size_t)(K > 0 ? K : 1) * 5);
+        for (int32_t r = 0; r < n; ++r) {
+            int32_t j = label_of[r];
+            if (j < 0) continue;
+            for (int32_t f = 0; f < dims; ++f) sum[j * 5 + f] += feat[r * dims + f];
+            sum[j * 5 + 4] += 1;
+        }
+        for (int32_t j = 0; j < K; ++j)
+            if (sum[j * 5 + 4] > 0)
+                for (int32_t f = 0; f < dims; ++f)
+                    C[j * 4 + f] = (double)sum[j * 5 + f] / (double)sum[j * 5 + 4];
+    }
+    if (iters_out) *iters_out = it;
+    if (k_eff_out) for (int32_t m = 0; m < M; ++m) k_eff_out[m] = k_eff[m];
+    if (init_out) for (int32_t j = 0; j < K; ++j) init_out[j] = ctr_req[j];   /* initial centres */
+    /* splitHalf and group statistics, cluster by cluster */
+    or_group_out o = { g_model, g_n, g_slo, g_mu, g_var };
+    int32_t *members = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    int32_t gid = 0;
+    for (int32_t j = 0; j < K; ++j) {
+        int32_t cnt = 0, m = 0;
+        for (int32_t r = 0; r < n; ++r) if (label_of[r] == j) { members[cnt++] = r; m = model[r]; }
+        if (cnt > 0)
+            gid = or_emit_halves(members, 0, cnt, limit, out_tok, slo, m, group_of, &o, group_cap, gid);
+    }
+    free(members); free(sum); free(C); free(mind); free(off); free(k_eff); free(ctr_req);
+    return gid;
+}

@@ -598,3 +598,130 @@ def test_tiers_wait_monotone_in_cpu_memory(seed):
                 assert np.all(e["wt"] <= prev + 1e-9 * np.maximum(1.0, prev))
             prev = e["wt"]
             assert np.all(e["cold"] <= 1)
+
+
+# ---------------------------------------------------------------- N4: group formation (R21)
+def _req(model, slo, out, feat):
+    return dict(model=np.asarray(model, np.int32), slo=np.asarray(slo, np.float64),
+                out=np.asarray(out, np.int32), feat=np.asarray(feat, np.int32).reshape(len(model), -1))
+
+
+def test_groups_spec_identical_requests_split_in_half():
+    # S:L199 (Alg. 1 split rule): 8 identical requests, threshold 4 -> two groups of 4
+    r = _req([0] * 8, [20.0] * 8, [100] * 8, [[7, 7]] * 8)
+    g = O.form_groups(r, 1, [3], limit=4)
+    assert g["k_eff"][0] == 1                      # no distinct point for a second centre
+    assert g["n_groups"] == 2 and list(g["n"]) == [4, 4]
+    assert list(g["group_of"]) == [0, 0, 0, 0, 1, 1, 1, 1]   # arrival-order halves
+    assert list(g["mu"]) == [100.0, 100.0] and list(g["var"]) == [0.0, 0.0]
+
+
+def test_groups_spec_models_are_a_hard_partition():
+    # requests of 2 models, k = 2 -> >= 2 groups, none mixing models
+    rng = np.random.default_rng(3)
+    n = 60
+    model = rng.integers(0, 2, n)
+    feat = rng.integers(0, 1000, (n, 2))
+    g = O.form_groups(_req(model, np.full(n, 20.0), rng.integers(1, 500, n), feat), 2, [2, 2], limit=100)
+    assert g["n_groups"] >= 2
+    for k in range(g["n_groups"]):
+        assert len(set(model[g["group_of"] == k])) == 1
+        assert g["model"][k] == model[g["group_of"] == k][0]
+
+
+def test_groups_spec_slo_classes_do_not_overlap():
+    # 100 requests, SLOs {20 s, 3600 s}, k = 2 -> SLO ranges do not overlap
+    rng = np.random.default_rng(4)
+    slo = rng.choice([20.0, 3600.0], 100)
+    feat = np.rint(4096 * np.log2(slo)).astype(np.int32)[:, None]
+    g = O.form_groups(_req(np.zeros(100), slo, np.full(100, 10), feat), 1, [2], limit=1000)
+    assert g["n_groups"] == 2
+    a, b = slo[g["group_of"] == 0], slo[g["group_of"] == 1]
+    assert a.max() < b.min() or b.max() < a.min()
+
+
+def _farthest_point_ok(feat, model, init, k_eff):
+    """Each chosen centre is a farthest point (exact int64) from the centres before it."""
+    off = 0
+    for m, k in enumerate(k_eff):
+        idx = np.where(model == m)[0]
+        if k == 0:
+            continue
+        assert init[off] == idx[0]                           # first request of the model
+        X = feat[idx].astype(np.int64)
+        for j in range(1, k):
+            C = feat[init[off:off + j]].astype(np.int64)
+            mind = ((X[:, None, :] - C[None]) ** 2).sum(-1).min(1)
+            assert mind.max() > 0
+            best = idx[np.flatnonzero(mind == mind.max())[0]]   # lowest index on ties
+            assert init[off + j] == best
+        off += k
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_groups_lloyd_matches_sklearn_from_the_same_start(seed):
+    # Lloyd's algorithm (textbook) as implemented by scikit-learn, started from
+    # the oracle's farthest-point centres: same final partition per model.
+    from sklearn.cluster import KMeans
+    from workloads.synth import make_requests
+    r = make_requests(3000, seed=100 + seed)
+    M, k = 4, [3, 4, 5, 6]
+    g = O.form_groups(r, M, k, limit=10**6, max_iter=300)
+    _farthest_point_ok(r["feat"], r["model"], g["init"], g["k_eff"])
+    assert g["iters"] < 300                               # converged: labels stable
+    off = 0
+    for m in range(M):
+        idx = np.where(r["model"] == m)[0]
+        X = r["feat"][idx].astype(np.float64)
+        init = r["feat"][g["init"][off:off + g["k_eff"][m]]].astype(np.float64)
+        km = KMeans(n_clusters=len(init), init=init, n_init=1, max_iter=300, tol=0.0,
+                    algorithm="lloyd").fit(X)
+        ours = g["label"][idx] - off
+        # same partition (labels index the same initial centres)
+        assert np.array_equal(km.labels_, ours)
+        off += g["k_eff"][m]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_groups_fixed_point_split_and_stats(seed):
+    from workloads.synth import make_requests
+    r = make_requests(5000, seed=200 + seed)
+    L = 97
+    g = O.form_groups(r, 4, [5, 5, 5, 5], limit=L, max_iter=200)
+    feat, model = r["feat"].astype(np.float64), r["model"]
+    lab = g["label"]
+    # Lloyd fixed point: every request sits at its nearest centre of its model,
+    # the centres being the means of the final clusters
+    K = int(g["k_eff"].sum())
+    cent = np.array([feat[lab == j].mean(0) if np.any(lab == j) else np.full(feat.shape[1], np.nan)
+                     for j in range(K)])
+    off = np.concatenate([[0], np.cumsum(g["k_eff"])])
+    for m in range(4):
+        idx = np.where(model == m)[0]
+        d = ((feat[idx][:, None, :] - cent[off[m]:off[m + 1]][None]) ** 2).sum(-1)
+        assert np.all(d[np.arange(len(idx)), lab[idx] - off[m]] <= d.min(1) * (1 + 1e-12))
+    # splitHalf: groups are consecutive arrival-order runs of one cluster, numbered
+    # cluster by cluster; no group exceeds L; halves of a split cluster keep >= ceil(L/2)
+    gid = 0
+    for j in range(K):
+        mem = np.where(lab == j)[0]
+        if len(mem) == 0:
+            continue
+        gs = g["group_of"][mem]
+        assert np.all(np.diff(gs) >= 0) and gs[0] == gid
+        sizes = np.bincount(gs - gid)
+        assert sizes.max() <= L and sizes.sum() == len(mem)
+        if len(mem) > L:
+            assert sizes.min() >= (L + 1) // 2
+        if len(mem) in (L * 2, L * 4):
+            assert np.all(sizes == L)
+        gid += len(sizes)
+    assert gid == g["n_groups"]
+    # group statistics: numpy's mean / population variance / min over the members
+    for k in range(g["n_groups"]):
+        mem = g["group_of"] == k
+        o = r["out"][mem].astype(np.float64)
+        assert g["n"][k] == mem.sum() and g["model"][k] == model[mem][0]
+        assert g["slo"][k] == r["slo"][mem].min()
+        assert g["mu"][k] == pytest.approx(o.mean(), rel=1e-14)
+        assert g["var"][k] == pytest.approx(o.var(), rel=1e-12, abs=1e-9)

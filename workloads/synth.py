@@ -319,6 +319,31 @@ def make_random_tiers(rng: np.random.Generator, M: int, D: int) -> dict:
     return dict(mem=mem, cap=cap, load=load)
 
 
+# Request-group formation (R21; Alg. 1) [SYNTHETIC]:
+# requests in arrival order with a model, an SLO class, an input length and
+# an output length drawn from the (model, class) length table (the
+# "input-output history").  Features (Def. P:L443-447: SLO, input /
+# output token distribution) are quantised logs: round(4096 * log2(x)),
+# which keeps every coordinate in [0, 65535] for x <= 2^15.
+FEAT_SCALE = 4096.0
+GROUP_LIMIT = 256          # delta = 4 x average batch 64
+
+
+def make_requests(n: int, models=(0, 1, 2, 3), *, seed: int = WORKLOAD_SEED) -> dict:
+    rng = np.random.default_rng(seed + 17)
+    tabs = all_length_tables()
+    M = len(models)
+    model = rng.integers(0, M, n).astype(np.int32)
+    cls = rng.choice(3, size=n, p=SLO_MIX)
+    slo = np.array(SLO_CLASSES)[cls]
+    in_len = np.clip(np.rint(np.exp(rng.normal(math.log(400.0), 0.9, n))), 1, 8192)
+    dist = np.array(models)[model] * 3 + cls
+    out = tabs[dist, rng.integers(0, tabs.shape[1], n)].astype(np.int32)
+    cls_mean = np.array([table_moments(tabs[k])[0] for k in range(len(tabs))])[dist]
+    feat = np.stack([np.rint(FEAT_SCALE * np.log2(x)) for x in (slo, in_len, cls_mean)], 1).astype(np.int32)
+    return dict(model=model, slo=slo, out=out, feat=feat, in_len=in_len.astype(np.int32))
+
+
 # name -> (problem factory, candidate kind, candidate count / trials)
 CONFIGS = {
     "C1": dict(desc="4 groups, 1 model, 1 queue: all 24 orderings (ENUM)",
