@@ -227,6 +227,41 @@ QLM_API int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, 
                               float *wt_std, float *viol, float *s1, float *s2, int32_t *n_over,
                               qlm_record *rec, void *stream);
 
+/* ---- request-group formation (R21; Alg. 1) ---- */
+
+/* Requests in arrival order, all arrays device memory.                     */
+typedef struct {
+    int32_t n;                 /* 1 <= n < 2^28                                           */
+    int32_t dims;              /* feature dimensions, 1..4                                */
+    const int32_t *model;      /* [n] in [0, M): a hard partition (Def. P:L443-447)       */
+    const double *slo_s;       /* [n] > 0: the group's SLO is its members' minimum        */
+    const int32_t *out_tokens; /* [n] in [0, 65535]: output tokens from the history */
+    const int32_t *feat;       /* [n][dims] in [0, 65535]: quantised features (SLO, input /
+                                  output token distribution, Def. P:L443-447)             */
+} qlm_requests;
+
+/* Alg. 1 under reading R21, on the device: per model m, k-means with
+ * k_per_model[m] centres (deterministic farthest-point start, Lloyd
+ * iterations in fp64 until no label changes or max_iter), then every
+ * cluster larger than `limit` (= delta x average batch) is split
+ * in half by arrival order, recursively (splitHalf).  Outputs: label_of[n]
+ * (device, cluster of each request), group_of[n] (device, group id;
+ * groups are numbered cluster by cluster, halves left to right) and the
+ * first min(n_groups, group_cap) records of groups[] (device qlm_group:
+ * model, n_req, slo_s = min member SLO, mu_out / var_out = mean /
+ * population variance of the members' out_tokens, dist_id = -1) ready for
+ * qlm_create.  *n_groups (host) = the number of groups, *iters (host,
+ * nullable) = Lloyd iterations run.  Synchronises `stream`; device scratch
+ * is stream-ordered (cudaMallocAsync).  `device` = CUDA ordinal.
+ * Errors: QLM_EINVAL (bad sizes: k_per_model[m] in [1, 1024] with sum <=
+ * 1024, limit in [1, 32768], max_iter in [1, 1000]; a request with a model,
+ * SLO, output length or feature out of range -- checked on the device),
+ * QLM_ERANGE (n_groups > group_cap; *n_groups is still set).               */
+QLM_API int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k_per_model,
+                            int32_t limit, int32_t max_iter, int32_t *label_of, int32_t *group_of,
+                            qlm_group *groups, int32_t group_cap, int32_t *n_groups, int32_t *iters,
+                            int32_t device, void *stream);
+
 /* Local-search step (R18), asynchronous on `stream`:
  * if *rec (e.g. from qlm_best_ordering_async over NEIGHBOR candidates of
  * base row cand->rows) has index >= 0 and a key strictly below

@@ -611,7 +611,9 @@ int64_t or_tiered_range(const or_problem *p, const or_tiers *t, int kind, const 
  *     member SLO, mu = S1 / n and var = (n S2 - S1^2) / n^2 with S1, S2 the
  *     exact integer sums of the members' output tokens and their squares
  *     ("fitted ... for the request group").
- * Returns the number of groups (written up to group_cap), -1 on bad input. */
+ * Returns the number of groups (written up to group_cap), -1 on bad input
+ * (limit outside [1, 32768], a model, feature or output length out of range:
+ * the bounds keep n S2 - S1^2 exact in int64).                             */
 typedef struct {
     int32_t *g_model, *g_n;
     double *g_slo, *g_mu, *g_var;
@@ -656,9 +658,9 @@ int32_t or_form_groups(int32_t n, int32_t dims, const int32_t *model, const doub
                        double *g_slo, double *g_mu, double *g_var, int32_t group_cap,
                        int32_t *iters_out, int32_t *k_eff_out, int32_t *init_out)
 {
-    if (n < 1 || dims < 1 || dims > 4 || M < 1 || limit < 1) return -1;
+    if (n < 1 || dims < 1 || dims > 4 || M < 1 || limit < 1 || limit > 32768) return -1;
     for (int32_t r = 0; r < n; ++r) {
-        if (model[r] < 0 || model[r] >= M) return -1;
+        if (model[r] < 0 || model[r] >= M || out_tok[r] < 0 || out_tok[r] > 65535) return -1;
         for (int32_t f = 0; f < dims; ++f)
             if (feat[r * dims + f] < 0 || feat[r * dims + f] > 65535) return -1;
     }

@@ -54,6 +54,11 @@ class Tiers(C.Structure):
     _fields_ = [("model_mem", C.c_void_p), ("cpu_cap", C.c_void_p), ("load_s", C.c_void_p)]
 
 
+class Requests(C.Structure):
+    _fields_ = [("n", C.c_int32), ("dims", C.c_int32), ("model", C.c_void_p), ("slo_s", C.c_void_p),
+                ("out_tokens", C.c_void_p), ("feat", C.c_void_p)]
+
+
 class Best(C.Structure):
     _fields_ = [("index", C.c_int64), ("s1", C.c_float), ("s2", C.c_float),
                 ("n_over", C.c_int32), ("reserved", C.c_int32)]
@@ -87,6 +92,8 @@ SIGNATURES = {
     "qlm_local_search": (C.c_int, [_vp, _vp, _i32, _i32, _i64, _i32, _u64, _vp, _vp]),
     "qlm_abi_version": (C.c_int, []),
     "qlm_set_tiers": (C.c_int, [_vp, C.POINTER(Tiers)]),
+    "qlm_form_groups": (C.c_int, [C.POINTER(Requests), _i32, _vp, _i32, _i32, _vp, _vp, _vp, _i32,
+                                  C.POINTER(C.c_int32), C.POINTER(C.c_int32), _i32, _vp]),
     "qlm_tiered_score_estimate": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp, _vp, _vp, _vp,
                                             _vp, _vp]),
 }

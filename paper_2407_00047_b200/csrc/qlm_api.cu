@@ -779,4 +779,39 @@ int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *w
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "tier kernel");
 }
 
+int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k_per_model, int32_t limit,
+                    int32_t max_iter, int32_t *label_of, int32_t *group_of, qlm_group *groups,
+                    int32_t group_cap, int32_t *n_groups, int32_t *iters, int32_t device, void *stream) {
+    if (!req || !k_per_model || !n_groups)
+        return fail(QLM_EINVAL, "req, k_per_model and n_groups must be non-NULL");
+    if (req->n < 1 || req->n >= (1 << 28)) return fail(QLM_EINVAL, "req.n=%d not in [1, 2^28)", req->n);
+    if (req->dims < 1 || req->dims > 4) return fail(QLM_EINVAL, "req.dims=%d not in [1, 4]", req->dims);
+    if (!req->model || !req->slo_s || !req->out_tokens || !req->feat)
+        return fail(QLM_EINVAL, "req.model / slo_s / out_tokens / feat must be non-NULL");
+    if (M < 1 || M > 64) return fail(QLM_EINVAL, "M=%d not in [1, 64]", M);
+    int K = 0;
+    for (int m = 0; m < M; ++m) {
+        if (k_per_model[m] < 1 || k_per_model[m] > 1024)
+            return fail(QLM_EINVAL, "k_per_model[%d]=%d not in [1, 1024]", m, k_per_model[m]);
+        K += k_per_model[m];
+    }
+    if (K > 1024) return fail(QLM_EINVAL, "sum of k_per_model=%d > 1024", K);
+    if (limit < 1 || limit > 32768) return fail(QLM_EINVAL, "limit=%d not in [1, 32768]", limit);
+    if (max_iter < 1 || max_iter > 1000) return fail(QLM_EINVAL, "max_iter=%d not in [1, 1000]", max_iter);
+    if (!label_of || !group_of) return fail(QLM_EINVAL, "label_of and group_of must be non-NULL");
+    if (group_cap < 0 || (group_cap > 0 && !groups)) return fail(QLM_EINVAL, "groups is NULL with group_cap > 0");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    int32_t bad = 0, it = 0, G = 0;
+    e = launch_form_groups(req->n, req->dims, M, k_per_model, limit, max_iter, req->model, req->slo_s,
+                           req->out_tokens, req->feat, label_of, group_of, groups, group_cap, &G, &it,
+                           &bad, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "group formation");
+    if (bad) return fail(QLM_EINVAL, "req: %d requests with a model, SLO, output length or feature out of range", bad);
+    *n_groups = G;
+    if (iters) *iters = it;
+    if (G > group_cap) return fail(QLM_ERANGE, "%d groups > group_cap=%d (n_groups is set)", G, group_cap);
+    return QLM_OK;
+}
+
 }  // extern "C"

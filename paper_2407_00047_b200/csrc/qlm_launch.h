@@ -54,6 +54,11 @@ cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per 
 cudaError_t launch_req(const ScanParams &p, const qlm_group *groups, float *frac, float *s1r,
                        cudaStream_t st);                            // request-level (R19)
 cudaError_t launch_tier(const ScanParams &p, cudaStream_t st);     // two-tier swapping (R20)
+cudaError_t launch_form_groups(int n, int dims, int M, const int32_t *k_host, int limit, int max_iter,
+                               const int32_t *model, const double *slo, const int32_t *out,
+                               const int32_t *feat, int32_t *label, int32_t *group_of,
+                               qlm_group *groups, int group_cap, int32_t *n_groups, int32_t *iters,
+                               int32_t *n_bad, cudaStream_t st);  // Alg. 1 (R21)
 cudaError_t launch_adopt(const Dims &dm, const Cand &cd, const qlm_record *rec, qlm_record *inc,
                          cudaStream_t st);                          // local-search step (R18)
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,

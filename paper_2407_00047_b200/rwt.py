@@ -306,6 +306,37 @@ class RwtEstimator:
         return n.value
 
 
+def form_groups(req: dict, M: int, k_per_model, limit: int = 256, max_iter: int = 50,
+                device: int = 0, stream=None) -> dict:
+    """Alg. 1 on the GPU under reading R21 (qlm_form_groups).
+
+    req: dict(model int32 [n], slo f64 [n], out int32 [n], feat int32 [n, dims])
+    in arrival order (host arrays or device tensors).  Returns dict(n_groups,
+    iters, label / group_of: device int32 [n], groups: numpy qlm_group records
+    ready for RwtEstimator / qlm_create)."""
+    dev = torch.device("cuda", device)
+    t = {k: torch.as_tensor(np.ascontiguousarray(req[k]) if not isinstance(req[k], torch.Tensor) else req[k])
+         .to(dev).contiguous() for k in ("model", "slo", "out", "feat")}
+    t["model"], t["out"], t["feat"] = (t["model"].to(torch.int32), t["out"].to(torch.int32),
+                                       t["feat"].to(torch.int32))
+    t["slo"] = t["slo"].to(torch.float64)
+    n = t["model"].numel()
+    dims = t["feat"].shape[1] if t["feat"].dim() == 2 else 1
+    r = L.Requests(n, dims, t["model"].data_ptr(), t["slo"].data_ptr(), t["out"].data_ptr(), t["feat"].data_ptr())
+    k = np.ascontiguousarray(k_per_model, np.int32)
+    label = torch.empty(n, dtype=torch.int32, device=dev)
+    gof = torch.empty(n, dtype=torch.int32, device=dev)
+    cap = n
+    groups = torch.empty(cap * L.GROUP_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    G, it = C.c_int32(), C.c_int32()
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    L.check(L.lib().qlm_form_groups(C.byref(r), M, k.ctypes.data, limit, max_iter, label.data_ptr(),
+                                    gof.data_ptr(), groups.data_ptr(), cap, C.byref(G), C.byref(it), device,
+                                    C.c_void_p(s.cuda_stream)), "qlm_form_groups")
+    recs = groups[: G.value * L.GROUP_DTYPE.itemsize].cpu().numpy().view(L.GROUP_DTYPE)
+    return dict(n_groups=G.value, iters=it.value, label=label, group_of=gof, groups=recs)
+
+
 def kernel_launches() -> int:
     return int(L.lib().qlm_kernel_launches())
 

@@ -60,11 +60,15 @@ int main(void) {
   printf("%zu %zu %zu %zu %zu %zu\n", offsetof(qlm_group, slo_s), offsetof(qlm_group, dist_id),
          offsetof(qlm_queue, backlog_mean_s), offsetof(qlm_candidates, first_from),
          offsetof(qlm_candidates, seed), offsetof(qlm_candidates, moves));
+  printf("%zu %zu %zu %zu\n", sizeof(qlm_tiers), sizeof(qlm_requests), offsetof(qlm_requests, model),
+         offsetof(qlm_requests, feat));
   return 0;
 }''')
     exe = tmp_path / "probe"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(probe), "-o", str(exe)])
-    a, b = subprocess.check_output([str(exe)], text=True).strip().split("\n")
+    a, b, c = subprocess.check_output([str(exe)], text=True).strip().split("\n")
+    assert [int(x) for x in c.split()] == [C.sizeof(L.Tiers), C.sizeof(L.Requests), L.Requests.model.offset,
+                                           L.Requests.feat.offset]
     sizes = [int(x) for x in a.split()]
     assert sizes == [L.GROUP_DTYPE.itemsize, L.QUEUE_DTYPE.itemsize, C.sizeof(L.Profile),
                      C.sizeof(L.LenTables), C.sizeof(L.Options), C.sizeof(L.Record),

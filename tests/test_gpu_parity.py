@@ -829,3 +829,64 @@ def test_tiers_ws_path_bit_identical_to_thread_kernel(cfg, monkeypatch):
     wt = ws["wt"][:, :600].cpu().numpy().astype(np.float64).T
     assert np.array_equal(wt, ref["wt"].astype(np.float32).astype(np.float64))
     check_scores(ws["s1"][:600].cpu().numpy(), ws["s2"][:600].cpu().numpy(), ref, p)
+
+
+# ------------------------------------------------------------------ N4: group formation (R21)
+def _groups_vs_oracle(req, M, k, limit, max_iter=50):
+    from paper_2407_00047_b200 import form_groups
+    g = form_groups(req, M, k, limit=limit, max_iter=max_iter)
+    ref = O.form_groups(req, M, k, limit=limit, max_iter=max_iter)
+    assert g["iters"] == ref["iters"]
+    assert np.array_equal(g["label"].cpu().numpy(), ref["label"])          # bit-exact labels
+    assert g["n_groups"] == ref["n_groups"]
+    assert np.array_equal(g["group_of"].cpu().numpy(), ref["group_of"])    # bit-exact group ids
+    rec = g["groups"]
+    assert np.array_equal(rec["model"], ref["model"]) and np.array_equal(rec["n_req"], ref["n"])
+    for f, r in (("slo_s", "slo"), ("mu_out", "mu"), ("var_out", "var")):
+        assert np.array_equal(rec[f], ref[r]), f                           # exact-integer sums
+    assert np.all(rec["dist_id"] == -1)
+    return g, ref
+
+
+@pytest.mark.parametrize("n,k,limit", [(5000, [4, 4, 4, 4], 97), (1 << 18, [16] * 4, 256),
+                                       (70001, [1, 7, 33, 2], 1), (3333, [50, 50, 50, 50], 32768)])
+def test_groups_vs_oracle(n, k, limit):
+    from workloads.synth import make_requests
+    req = make_requests(n, seed=n)
+    g, ref = _groups_vs_oracle(req, 4, k, limit)
+    assert g["groups"]["n_req"].max() <= limit
+
+
+def test_groups_edge_cases():
+    # identical requests (k collapses to 1), a model without requests, one request
+    req = dict(model=np.array([0] * 9 + [2] * 3, np.int32), slo=np.full(12, 20.0),
+               out=np.arange(12, dtype=np.int32) * 7, feat=np.full((12, 2), 5, np.int32))
+    g, ref = _groups_vs_oracle(req, 3, [4, 4, 4], 4)
+    assert list(ref["k_eff"]) == [1, 0, 1]
+    one = dict(model=np.zeros(1, np.int32), slo=np.ones(1), out=np.ones(1, np.int32), feat=np.zeros((1, 4), np.int32))
+    _groups_vs_oracle(one, 1, [3], 1)
+    from paper_2407_00047_b200 import _lib as L, form_groups
+    bad = dict(req, feat=np.full((12, 2), 70000, np.int32))
+    with pytest.raises(L.QlmError, match="out of range"):
+        form_groups(bad, 3, [2, 2, 2])
+    with pytest.raises(L.QlmError, match="limit"):
+        form_groups(req, 3, [2, 2, 2], limit=0)
+
+
+def test_groups_feed_the_scheduler():
+    # requests -> groups (GPU) -> a scheduling problem -> best ordering (GPU) vs oracle
+    import dataclasses
+    from paper_2407_00047_b200 import form_groups
+    from workloads.synth import make_requests, make_problem
+    req = make_requests(20000, seed=5)
+    g = form_groups(req, 4, [3, 3, 3, 3], limit=256)
+    rec = g["groups"]
+    base = make_problem(8, 4, name="grp")
+    p = dataclasses.replace(base, model=rec["model"].astype(np.int32), n_req=rec["n_req"].astype(np.int32),
+                            slo=rec["slo_s"].copy(), mu=rec["mu_out"].copy(), var=rec["var_out"].copy(),
+                            dist=np.full(len(rec), -1, np.int32), len_tables=None)
+    e = est_of(p)
+    n = 2000
+    s1, s2, _ = e.score_orderings(e.random(0, n, seed=1))
+    ref = O.Oracle(p).score_range(O.RANDOM, 0, n, seed=1)
+    check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)

@@ -666,7 +666,7 @@ def test_groups_lloyd_matches_sklearn_from_the_same_start(seed):
     from workloads.synth import make_requests
     r = make_requests(3000, seed=100 + seed)
     M, k = 4, [3, 4, 5, 6]
-    g = O.form_groups(r, M, k, limit=10**6, max_iter=300)
+    g = O.form_groups(r, M, k, limit=32768, max_iter=300)
     _farthest_point_ok(r["feat"], r["model"], g["init"], g["k_eff"])
     assert g["iters"] < 300                               # converged: labels stable
     off = 0
