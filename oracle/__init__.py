@@ -230,7 +230,7 @@ class Oracle:
         if estimates:
             out.update(wt=wt, V=V, sd=np.sqrt(V),
                        v=np.array([[violation(wt[k, i], V[k, i], self.prob.slo[i]) for i in range(G)]
-                                   for k in range(count)]) if count * G <= 200000 else None)
+                                   for k in range(count)]) if count * G <= 2000000 else None)
         return out
 
     def mc_sample(self, mc_seed, trial_first, trial_count):

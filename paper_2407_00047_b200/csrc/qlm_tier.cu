@@ -19,6 +19,8 @@
 // coalesced 128-B warp stores, or go straight to HBM when no tile fits.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "qlm_device.cuh"
 #include "qlm_launch.h"
 #include "qlm_argmin.cuh"
@@ -237,9 +239,216 @@ static cudaError_t launch_tier_t(const ScanParams &p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// ---- large G: one warp per candidate, one lane per queue -------------------
+// The tier state (R20) is per queue, so a lane that walks one whole queue in
+// row order carries it exactly (and in the oracle's operation order).  Eight
+// warps score eight consecutive candidates; their bulk outputs are staged in
+// a [3][G][9] tile and leave as full 32-B rows of the group-major arrays.
+constexpr int kTwWarps = 8;
+constexpr int kTwPad = kTwWarps + 1;
+
+struct TierWarpSmem {
+    int off_g, off_ab, off_q, off_trw, off_trc, off_mem, off_cap, off_tile, off_rows, off_qbeg;
+    int ldr;
+};
+
+__global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, const TierWarpSmem L) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const Dims dm = p.dm;
+    const int G = dm.G, Q = dm.Q, T = dm.T, M = dm.M, D = dm.D;
+    GRec *sg = reinterpret_cast<GRec *>(smem + L.off_g);
+    for (int i = tid; i < G; i += 256) sg[i] = p.tb.grec[i];
+    double2 *sab = reinterpret_cast<double2 *>(smem + L.off_ab);
+    for (int i = tid; i < D * G; i += 256) sab[i] = p.tb.ab[i];
+    QRec *sq = reinterpret_cast<QRec *>(smem + L.off_q);
+    for (int i = tid; i < Q; i += 256) sq[i] = p.tb.qrec[i];
+    double *trw = reinterpret_cast<double *>(smem + L.off_trw);
+    double *trc = reinterpret_cast<double *>(smem + L.off_trc);
+    for (int i = tid; i < D * 2 * M * M; i += 256) {
+        const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
+        const int from = pp < M ? pp : pp - M;
+        const double sw = p.tb.swap[(d * M + from) * M + m];
+        const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
+        const double ld = m != from ? p.t_load[d * M + m] : 0.0;
+        trw[i] = __dadd_rn(tl, sw);
+        trc[i] = __dadd_rn(tl, __dadd_rn(sw, ld));
+    }
+    int *smemsz = reinterpret_cast<int *>(smem + L.off_mem);
+    for (int i = tid; i < M; i += 256) smemsz[i] = p.t_mem[i];
+    int *scap = reinterpret_cast<int *>(smem + L.off_cap);
+    for (int i = tid; i < D; i += 256) scap[i] = p.t_cap[i];
+    float *tile = reinterpret_cast<float *>(smem + L.off_tile);          // [3][G][kTwPad]
+    uint16_t *srow = reinterpret_cast<uint16_t *>(smem + L.off_rows) + (size_t)warp * 2 * L.ldr;
+    uint16_t *sJ = srow + L.ldr;
+    int *qbeg = reinterpret_cast<int *>(smem + L.off_qbeg) + (size_t)warp * (Q + 1);
+    __syncthreads();
+
+    const Cand cd = p.cd;
+    int64_t first = cd.first;
+    bool none = false;
+    if (cd.first_from) {
+        first = cd.first_from->index;
+        none = first < 0;
+    }
+    const int64_t count = none ? 0 : cd.count;
+    const double zc2 = p.zc2;
+    const float alpha = p.alpha;
+    const double den = *p.tb.den;
+    float *const gout[3] = {p.wt, p.sd, p.vo};
+    const bool bulk = p.wt || p.sd || p.vo;
+    uint64_t bkey = ~0ull;
+    int64_t bidx = -1;
+    const int64_t nbatch = (count + kTwWarps - 1) / kTwWarps;
+    for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
+        const int64_t c0 = bt * kTwWarps, loc = c0 + warp;
+        if (loc < count) {                                    // warp-uniform
+            warp_gen_row(cd, T, (uint64_t)(first + loc), loc, srow, sJ);
+            // queue q covers row positions [qbeg[q], qbeg[q + 1] - 1)
+            if (lane == 0) qbeg[0] = 0;
+            int nsep = 0;
+            for (int s0 = 0; s0 < T; s0 += 32) {
+                const int s = s0 + lane;
+                const bool sep = s < T && srow[s] >= G;
+                const uint32_t bs = __ballot_sync(0xFFFFFFFFu, sep);
+                if (sep) {
+                    const int k = nsep + __popc(bs & ((1u << lane) - 1u));
+                    if (k + 1 <= Q - 1) qbeg[k + 1] = s + 1;
+                }
+                nsep += __popc(bs);
+            }
+            if (lane == 0) qbeg[Q] = T + 1;
+            __syncwarp();
+            double S2 = 0.0, num = 0.0;
+            int over = 0;
+            for (int q = lane; q < Q; q += 32) {
+                const QRec r = sq[q];
+                const int d = r.d;
+                int prow = r.backlog ? r.r : M + r.r;         // R4 / R12
+                double A = r.bmean, B = r.bvar;
+                uint32_t seen = 0u, warm = 0u;
+                int cum = 0;
+                bool exh = false;
+                const int s1 = qbeg[q + 1] - 1;
+                for (int s = qbeg[q]; s < s1; ++s) {
+                    const int tok = srow[s];
+                    const GRec g = sg[tok];
+                    const int m = g.model;
+                    const int pm = prow < M ? prow : prow - M;
+                    bool cold = false;
+                    if (m != pm) {                            // transition (Eq. 9), tier (R20)
+                        const uint32_t bit = 1u << m;
+                        if (!(seen & bit)) {
+                            seen |= bit;
+                            if (!exh && cum + smemsz[m] <= scap[d]) { warm |= bit; cum += smemsz[m]; }
+                            else exh = true;
+                        }
+                        cold = !(warm & bit);
+                    }
+                    const int ti = (d * 2 * M + prow) * M + m;
+                    A = __dadd_rn(A, cold ? trc[ti] : trw[ti]);
+                    const double wt = A, V = B;
+                    const double2 ab = sab[d * G + tok];
+                    A = __dadd_rn(A, ab.x);
+                    B = __dadd_rn(B, ab.y);
+                    prow = m;
+                    const double slack = __dsub_rn(g.slo, wt);
+                    bool clamped;
+                    const float v = violation(slack, V, zc2, clamped);
+                    S2 = __dsub_rn(S2, slack);
+                    num = __dadd_rn(num, (double)g.n * (double)v);
+                    over += v > alpha;
+                    if (bulk) {
+                        const float Vf = (float)V;
+                        float *o = tile + (size_t)tok * kTwPad + warp;
+                        o[0] = (float)wt;
+                        o[(size_t)G * kTwPad] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
+                        o[(size_t)2 * G * kTwPad] = v;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                S2 += __shfl_xor_sync(0xFFFFFFFFu, S2, o);
+                num += __shfl_xor_sync(0xFFFFFFFFu, num, o);
+                over += __shfl_xor_sync(0xFFFFFFFFu, over, o);
+            }
+            const float s1v = (float)(num / den), s2v = (float)S2;   // R11
+            if (lane == 0) {
+                if (p.s1) p.s1[loc] = s1v;
+                if (p.s2) p.s2[loc] = s2v;
+                if (p.n_over) p.n_over[loc] = over;
+            }
+            const uint64_t key = make_key(s1v, s2v);
+            if (lane == 0 && better(key, first + loc, bkey, bidx)) { bkey = key; bidx = first + loc; }
+        }
+        if (bulk) {                                           // full 32-B rows of the outputs
+            __syncthreads();
+            const int nv = (int)min((int64_t)kTwWarps, count - c0);
+            // 8 consecutive lanes write one row's 8 floats: each store instruction
+            // covers 4 whole 32-B sectors (no partial-sector writes)
+            for (int i = tid; i < 3 * G * kTwWarps; i += 256) {
+                const int r = i >> 3, k = i & 7;
+                const int a = r / G, g = r - a * G;
+                if (gout[a] && k < nv) gout[a][(int64_t)g * count + c0 + k] = tile[((size_t)a * G + g) * kTwPad + k];
+            }
+            __syncthreads();
+        }
+    }
+    if (p.out_rec) {
+        if (none) {
+            if (blockIdx.x == 0 && tid == 0) { p.out_rec->key = ~0ull; p.out_rec->index = -1; }
+            return;
+        }
+        block_grid_argmin(p, bkey, bidx);
+    }
+}
+
+static cudaError_t launch_tier_warp(const ScanParams &p, cudaStream_t st) {
+    const Dims &dm = p.dm;
+    auto a16 = [](size_t x) { return (x + 15) & ~size_t(15); };
+    TierWarpSmem L{};
+    L.ldr = (dm.T + 7) & ~7;
+    size_t o = 0;
+    L.off_g = (int)o;    o = a16(o + (size_t)dm.G * sizeof(GRec));
+    L.off_ab = (int)o;   o = a16(o + (size_t)dm.D * dm.G * sizeof(double2));
+    L.off_q = (int)o;    o = a16(o + (size_t)dm.Q * sizeof(QRec));
+    L.off_trw = (int)o;  o = a16(o + (size_t)dm.D * 2 * dm.M * dm.M * 8);
+    L.off_trc = (int)o;  o = a16(o + (size_t)dm.D * 2 * dm.M * dm.M * 8);
+    L.off_mem = (int)o;  o = a16(o + (size_t)dm.M * 4);
+    L.off_cap = (int)o;  o = a16(o + (size_t)dm.D * 4);
+    L.off_tile = (int)o; o = a16(o + ((p.wt || p.sd || p.vo) ? (size_t)3 * dm.G * kTwPad * 4 : 0));
+    L.off_rows = (int)o; o = a16(o + (size_t)kTwWarps * 2 * L.ldr * 2);
+    L.off_qbeg = (int)o; o = a16(o + (size_t)kTwWarps * (dm.Q + 1) * 4);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, tier_warp_kernel);
+    if (e != cudaSuccess) return e;
+    if (o + fa.sharedSizeBytes > (size_t)optin) return cudaErrorNotSupported;
+    if ((e = cudaFuncSetAttribute(tier_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)o)))
+        return e;
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, tier_warp_kernel, 256, o);
+    if (nb < 1) return cudaErrorNotSupported;
+    int64_t grid = (p.cd.count + kTwWarps - 1) / kTwWarps;
+    if (grid > (int64_t)sm_count() * nb) grid = (int64_t)sm_count() * nb;
+    if (grid > p.max_blocks) grid = p.max_blocks;
+    if (grid < 1) grid = 1;
+    tier_warp_kernel<<<(unsigned)grid, 256, o, st>>>(p, L);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_tier(const ScanParams &p, cudaStream_t st) {
     const cudaError_t ws = launch_ws_tier(p, st);            // warp-specialised fast path
     if (ws != cudaErrorNotSupported) return ws;
+    const char *nw = getenv("QLM_NO_TIER_WARP");
+    if (p.dm.G > 256 && !(nw && *nw && *nw != '0')) {        // large G: lane per queue
+        const cudaError_t w = launch_tier_warp(p, st);
+        if (w != cudaErrorNotSupported) return w;
+    }
     const bool u8 = p.dm.T <= 256;
     switch (p.cd.kind) {
     case QLM_CAND_RANDOM:

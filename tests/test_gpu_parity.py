@@ -890,3 +890,88 @@ def test_groups_feed_the_scheduler():
     s1, s2, _ = e.score_orderings(e.random(0, n, seed=1))
     ref = O.Oracle(p).score_range(O.RANDOM, 0, n, seed=1)
     check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)
+
+
+# ------------------------------------------------------------------ full sizes, bench launch configuration
+def test_bench_step_c3_full_size():
+    # bench.py's step at BASELINE.json's C3 size: 1e6 RANDOM candidates through the
+    # fused warp-specialised kernel (bulk wt/sd/v + scores + argmin record).  The
+    # oracle scores all 1e6 candidates (~3 s), so the argmin is checked in full;
+    # bulk estimates on a strided + random sample of candidates.
+    p = make_config("C3")
+    e = est_of(p)
+    N = 1_000_000
+    cand = e.random(0, N, seed=1)
+    out = {k: torch.empty((p.G, N), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+    rec = torch.empty(2, dtype=torch.int64, device="cuda")
+    e.score_estimate(cand, out=out, rec=rec)
+    torch.cuda.synchronize()
+    o = O.Oracle(p)
+    ref = o.score_range(O.RANDOM, 0, N, seed=1)
+    check_scores(out["s1"].cpu().numpy(), out["s2"].cpu().numpy(), ref, p)
+    ok, cstar = argmin_ok(int(rec[1]), ref["s1"], ref["s2"], p)
+    assert ok, (int(rec[1]), cstar)
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([np.arange(0, N, 997), rng.integers(0, N, 500), [int(rec[1]), N - 1]]))
+    wt, sd, v = (out[k][:, idx].cpu().numpy().astype(np.float64).T for k in ("wt", "sd", "v"))
+    for j, c in enumerate(idx):
+        r = o.estimate(O.random_row(1, int(c), p.T))
+        assert np.array_equal(wt[j], r["wt"].astype(np.float32).astype(np.float64))   # bit-exact order
+        np.testing.assert_allclose(sd[j], np.sqrt(r["V"]), rtol=1e-5, atol=0)
+        vv = np.array([O.violation(r["wt"][i], r["V"][i], p.slo[i]) for i in range(p.G)])
+        assert np.max(np.abs(v[j] - vv)) <= 1e-5
+
+
+def test_c5_full_candidate_range_sampled():
+    # C5 (1024 groups, 32 queues) is quoted on 1e8 candidates sharded over GPUs:
+    # score a 1e6-candidate shard far into the index space (two-phase large-T
+    # path) and check a strided sample plus the shard's argmin against the oracle.
+    p = make_config("C5")
+    e = est_of(p)
+    first, N = 7 * 10**7, 1_000_000
+    s1, s2, _ = e.score_orderings(e.random(first, N, seed=1))
+    rec = e.best_ordering_async(e.random(first, N, seed=1))
+    torch.cuda.synchronize()
+    s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
+    k = int(rec[1]) - first
+    assert 0 <= k < N
+    key = O.key32(s1[k], s2[k])
+    assert all(key <= O.key32(a, b) for a, b in zip(s1[::1000], s2[::1000]))
+    idx = np.concatenate([np.arange(0, N, 10_007), [k]])
+    o = O.Oracle(p)
+    for c in idx:
+        r1, r2, _ = o.score(O.random_row(1, first + int(c), p.T))
+        assert abs(s1[c] - r1) <= 1e-5
+        assert abs(s2[c] - r2) <= 1e-5 * abs(r2 + 2 * p.slo.sum()) + 1e-6
+
+
+@pytest.mark.parametrize("G,Q,D,backlog,n,kind", [(1024, 32, 1, False, 203, "random"),
+                                                  (300, 5, 2, True, 157, "explicit"),
+                                                  (600, 40, 2, True, 90, "random")])
+def test_tiers_large_G_lane_per_queue(G, Q, D, backlog, n, kind, monkeypatch):
+    # G > 256 takes the warp-per-candidate / lane-per-queue tier kernel; it must
+    # agree with the oracle and (bit for bit on wt / sd / v) with the thread kernel
+    from workloads.synth import make_random_tiers
+    rng = np.random.default_rng(G + Q)
+    p = make_random_problem(rng, G, Q, 4, D, backlog=backlog)
+    tiers = make_random_tiers(rng, 4, D)
+    e = est_of(p)
+    e.set_tiers(tiers)
+    o = O.Oracle(p)
+    if kind == "random":
+        cand, kw = e.random(11, n, seed=5), dict(kind=O.RANDOM, first=11, seed=5)
+    else:
+        rows = np.stack([O.random_row(3, c, p.T) for c in range(n)])
+        cand, kw = e.explicit(rows_tensor(rows, token_bytes=2)), dict(kind=O.EXPLICIT, first=0,
+                                                                      rows=rows.astype(np.uint16))
+    warp, rw = _tier_out(e, cand)
+    ref = o.tiered_range(tiers, kw["kind"], kw["first"], n, seed=kw.get("seed", 0), rows=kw.get("rows"))
+    check_estimates(warp, ref)
+    check_scores(warp["s1"].cpu().numpy(), warp["s2"].cpu().numpy(), ref, p)
+    assert np.array_equal(warp["n_over"].cpu().numpy(), ref["n_over"])
+    ok, _ = argmin_ok(int(rw[1]), ref["s1"], ref["s2"], p, first=kw["first"])
+    assert ok
+    monkeypatch.setenv("QLM_NO_TIER_WARP", "1")
+    thr, _ = _tier_out(e, cand)
+    for k in ("wt", "sd", "v"):
+        assert torch.equal(warp[k], thr[k]), k
