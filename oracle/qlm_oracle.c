@@ -35,6 +35,10 @@
  *                      or_estimate_row with swap + load folded into the swap
  *                      table; hand-worked golden (prefix-not-first-fit,
  *                      re-entry keeps its tier); wt monotone in cap.
+ *   or_form_groups (R21, N4)  SPEC S:L199-201 examples; Lloyd partition ==
+ *                      scikit-learn KMeans(lloyd, tol=0) from the same start;
+ *                      farthest-point start by brute force; fixed point; split
+ *                      sizes; group stats == numpy mean / var / min.
  */
 #include <math.h>
 #include <stdint.h>

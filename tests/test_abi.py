@@ -160,3 +160,23 @@ def test_null_context_calls_fail_cleanly(lib):
     assert lib.qlm_local_search(None, None, 1, 2, 64, 1, 1, None, None) == L.QLM_EINVAL
     lib.qlm_destroy(None)
     assert lib.qlm_abi_version() == 3
+
+
+def test_form_groups_host_validation(lib):
+    # Alg. 1 entry point (R21): sizes are checked on the host before any CUDA call
+    dummy = C.c_void_p(16)
+    G, it = C.c_int32(), C.c_int32()
+
+    def call(n=10, dims=2, M=2, k=(2, 2), limit=8, max_iter=5, lab=dummy, gof=dummy):
+        r = L.Requests(n, dims, dummy, dummy, dummy, dummy)
+        ka = np.asarray(k, np.int32)
+        rc = lib.qlm_form_groups(C.byref(r), M, ka.ctypes.data, limit, max_iter, lab, gof, dummy, 4,
+                                 C.byref(G), C.byref(it), 0, None)
+        return rc, lib.qlm_last_error().decode()
+
+    for kw, msg in [(dict(n=0), "req.n"), (dict(dims=5), "req.dims"), (dict(M=0, k=()), "M="),
+                    (dict(k=(0, 2)), "k_per_model[0]"), (dict(k=(1000, 1000)), "sum of k_per_model"),
+                    (dict(limit=0), "limit"), (dict(limit=40000), "limit"), (dict(max_iter=0), "max_iter"),
+                    (dict(lab=None), "label_of")]:
+        rc, err = call(**kw)
+        assert rc == L.QLM_EINVAL and msg in err, (kw, rc, err)
