@@ -626,87 +626,97 @@ __global__ void __launch_bounds__(256) mc_sample_kernel(Dims dm, Tables tb, uint
     }
 }
 
-// One warp per (candidate, 32 trials); every lane is one trial.  The warp
-// materialises the candidate's row, then precomputes per group slot (in row
-// order, all trial-independent): the deterministic addend of the Eq. 10 walk
-// at a model change (tail + swap, R2/R3/R4/R12), the SLO, the start value of
-// the queue (backlog mean) and the row of Y to read.  The walk itself is then
-// A = start?; A += tail + swap; count A > slo; A += y  -- branch-free, in
-// the oracle's operation order (+0.0 where no model change: A >= 0, so
-// A + 0.0 == A bit for bit).  y is prefetched 16 slots ahead.
-__global__ void __launch_bounds__(32) mc_count_kernel(Dims dm, Tables tb, Cand cd,
-                                                      const double *Y, int64_t nt,
-                                                      uint32_t *counts) {
+// One block per (candidate, 32 trials); every lane is one trial, and the
+// block's warps split the candidate's queues (queues are independent in Eq.
+// 10, so each warp walks whole queues in row order: the oracle's operation
+// order).  Warp 0 materialises the row and precomputes per group slot (in
+// row order, all trial-independent): the deterministic addend of the walk at
+// a model change (tail + swap, R2/R3/R4/R12), the SLO, the start value of the
+// queue (backlog mean) and the row of Y to read.  The walk itself is then
+// A = start?; A += tail + swap; count A > slo; A += y  -- branch-free
+// (+0.0 where no model change: A >= 0, so A + 0.0 == A bit for bit).
+constexpr int kMcWarps = 8;
+__global__ void __launch_bounds__(32 * kMcWarps) mc_count_kernel(Dims dm, Tables tb, Cand cd,
+                                                                 const double *Y, int64_t nt,
+                                                                 uint32_t *counts) {
     extern __shared__ __align__(16) uint8_t smem[];
     int64_t first = cd.first;
     if (cd.first_from) {
         first = cd.first_from->index;
         if (first < 0) return;
     }
-    const int T = dm.T, G = dm.G, M = dm.M;
+    const int T = dm.T, G = dm.G, M = dm.M, Q = dm.Q;
     double *st = reinterpret_cast<double *>(smem);     // [G] transition addend
     double *sslo = st + G;                              // [G] SLO
     double *sa0 = sslo + G;                             // [G] queue start (backlog mean) or -1
     int32_t *yrow = reinterpret_cast<int32_t *>(sa0 + G);   // [G] d * G + token
-    uint16_t *stok = reinterpret_cast<uint16_t *>(yrow + G);  // [G]
+    int32_t *qs = yrow + G;                             // [Q + 1] first slot of each queue
+    uint16_t *stok = reinterpret_cast<uint16_t *>(qs + ((Q + 1 + 3) & ~3));  // [G]
     uint16_t *sq = stok + G;                            // [G]
     uint16_t *srow = sq + G;                            // [T]
     uint16_t *sJ = srow + ((T + 7) & ~7);               // [T]
     const int64_t loc = blockIdx.y;
-    const int lane = threadIdx.x;
-    warp_gen_row(cd, T, (uint64_t)(first + loc), loc, srow, sJ);
-    warp_slots(srow, T, G, dm.Q, [&](int tok, int q, int, int i) {
-        stok[i] = (uint16_t)tok;
-        sq[i] = (uint16_t)q;
-    });
-    __syncwarp();
-    for (int i = lane; i < G; i += 32) {
-        const int tok = stok[i], q = sq[i];
-        const QRec qr = tb.qrec[q];
-        const GRec g = tb.grec[tok];
-        const bool firsts = i == 0 || sq[i - 1] != q;
-        const int prev = firsts ? qr.r : tb.grec[stok[i - 1]].model;
-        const int d = qr.d, m = g.model;
-        double c = 0.0;                                  // transition term (R2/R3)
-        if (m != prev) {
-            const double t = (firsts && !qr.backlog) ? 0.0 : tb.tail[d * M + prev];
-            c = __dadd_rn(t, tb.swap[(d * M + prev) * M + m]);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (warp == 0) {
+        warp_gen_row(cd, T, (uint64_t)(first + loc), loc, srow, sJ);
+        warp_slots(srow, T, G, Q, [&](int tok, int q, int, int i) {
+            stok[i] = (uint16_t)tok;
+            sq[i] = (uint16_t)q;
+        });
+        __syncwarp();
+        for (int i = lane; i < G; i += 32) {
+            const int tok = stok[i], q = sq[i];
+            const QRec qr = tb.qrec[q];
+            const GRec g = tb.grec[tok];
+            const bool firsts = i == 0 || sq[i - 1] != q;
+            const int prev = firsts ? qr.r : tb.grec[stok[i - 1]].model;
+            const int d = qr.d, m = g.model;
+            double c = 0.0;                              // transition term (R2/R3)
+            if (m != prev) {
+                const double t = (firsts && !qr.backlog) ? 0.0 : tb.tail[d * M + prev];
+                c = __dadd_rn(t, tb.swap[(d * M + prev) * M + m]);
+            }
+            st[i] = c;
+            sslo[i] = g.slo;
+            sa0[i] = firsts ? qr.bmean : -1.0;
+            yrow[i] = d * G + tok;
         }
-        st[i] = c;
-        sslo[i] = g.slo;
-        sa0[i] = firsts ? qr.bmean : -1.0;
-        yrow[i] = d * G + tok;
+        for (int q = lane; q <= Q; q += 32) {            // qs[q] = #slots in queues < q
+            int lo = 0, hi = G;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sq[mid] < q) lo = mid + 1; else hi = mid;
+            }
+            qs[q] = lo;
+        }
     }
-    __syncwarp();
+    __syncthreads();
     const int64_t tl = (int64_t)blockIdx.x * 32 + lane;
     const bool act = tl < nt;
-    constexpr int PF = 16;
-    auto load = [&](int i0, double *y) {
-#pragma unroll
-        for (int k = 0; k < PF; ++k) {
-            const int i = i0 + k < G ? i0 + k : G - 1;
-            y[k] = act ? __ldg(&Y[(int64_t)yrow[i] * nt + tl]) : 0.0;
-        }
-    };
-    double cur[PF], nxt[PF];
-    load(0, cur);
-    double A = 0.0;
     uint32_t *cnt = counts + loc * G;
-    for (int i0 = 0; i0 < G; i0 += PF) {
-        if (i0 + PF < G) load(i0 + PF, nxt);
+    constexpr int PF = 8;
+    for (int q = warp; q < Q; q += nw) {
+        const int i0 = qs[q], i1 = qs[q + 1];
+        double A = 0.0;
+        for (int b = i0; b < i1; b += PF) {
+            double y[PF];
 #pragma unroll
-        for (int k = 0; k < PF; ++k) {
-            const int i = i0 + k;
-            if (i >= G) break;
-            const double a0 = sa0[i];
-            A = a0 >= 0.0 ? a0 : A;
-            A = __dadd_rn(A, st[i]);
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, act && A > sslo[i]);
-            if (lane == 0 && bal) atomicAdd(&cnt[stok[i]], (unsigned)__popc(bal));
-            A = __dadd_rn(A, cur[k]);
+            for (int k = 0; k < PF; ++k) {               // loads first: independent of A
+                const int i = b + k < i1 ? b + k : i1 - 1;
+                y[k] = act ? __ldg(&Y[(int64_t)yrow[i] * nt + tl]) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < PF; ++k) {
+                const int i = b + k;
+                if (i >= i1) break;
+                const double a0 = sa0[i];
+                A = a0 >= 0.0 ? a0 : A;
+                A = __dadd_rn(A, st[i]);
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, act && A > sslo[i]);
+                if (lane == 0 && bal) atomicAdd(&cnt[stok[i]], (unsigned)__popc(bal));
+                A = __dadd_rn(A, y[k]);
+            }
         }
-#pragma unroll
-        for (int k = 0; k < PF; ++k) cur[k] = nxt[k];
     }
 }
 
@@ -1052,11 +1062,13 @@ cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, in
 
 cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const Cand &cd, const double *X,
                             int64_t nt, uint32_t *counts, cudaStream_t st) {
-    const size_t smem = (size_t)32 * dm.G + (size_t)4 * ((dm.T + 7) & ~7);
+    const size_t smem = (size_t)32 * dm.G + (size_t)4 * ((dm.Q + 1 + 3) & ~3) +
+                        (size_t)4 * ((dm.T + 7) & ~7);
     cudaError_t e = prep(mc_count_kernel, smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((nt + 31) / 32), (unsigned)cd.count);
-    mc_count_kernel<<<grid, 32, smem, st>>>(dm, tb, cd, X, nt, counts);
+    const int warps = dm.Q < kMcWarps ? dm.Q : kMcWarps;   // warps split the queues
+    mc_count_kernel<<<grid, 32 * warps, smem, st>>>(dm, tb, cd, X, nt, counts);
     ++g_launches;
     return cudaGetLastError();
 }
