@@ -975,3 +975,27 @@ def test_tiers_large_G_lane_per_queue(G, Q, D, backlog, n, kind, monkeypatch):
     thr, _ = _tier_out(e, cand)
     for k in ("wt", "sd", "v"):
         assert torch.equal(warp[k], thr[k]), k
+
+
+def test_tiers_from_device_record_and_neighbor():
+    # the tiered scorer on a winner named by a device record (no host sync) and
+    # on NEIGHBOR candidates of an incumbent row, vs the oracle
+    from workloads.synth import make_tiers
+    p = make_config("C3")
+    t = make_tiers()
+    e = est_of(p)
+    e.set_tiers(t)
+    rec = torch.empty(2, dtype=torch.int64, device="cuda")
+    e.tiered_score_estimate(e.random(0, 5000, seed=1), rec=rec)
+    one = e.tiered_score_estimate(e.from_record(rec, seed=1))
+    torch.cuda.synchronize()
+    o = O.Oracle(p)
+    s1, s2, _ = o.score_tiered(O.random_row(1, int(rec[1]), p.T), t)
+    assert abs(float(one["s1"][0]) - s1) <= 1e-5
+    base = O.random_row(1, int(rec[1]), p.T)
+    buf = e.row_buffer(base)
+    n = 3000
+    out, r2 = _tier_out(e, e.neighbor(buf, 0, n, seed=4, moves=2))
+    ref = o.tiered_range(t, O.NEIGHBOR, 0, n, seed=4, rows=base, moves=2)
+    check_scores(out["s1"].cpu().numpy(), out["s2"].cpu().numpy(), ref, p)
+    check_estimates(out, ref)
