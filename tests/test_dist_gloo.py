@@ -195,3 +195,43 @@ def test_two_rank_gloo_sharded_local_search():
         assert b == row.tolist()
         s1, s2, _ = O.Oracle(p).score(np.array(b))
         assert O.key32(s1, s2) == key
+
+
+# ------------------------------------------------- sharded two-tier scoring (R20)
+def _tier_worker(rank, world, port, N, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from workloads.synth import make_tiers
+        p = make_config("C3")
+        t = make_tiers()
+        first, count = shard_range(N, rank, world)
+        r = O.Oracle(p).tiered_range(t, O.RANDOM, first, count, seed=1, estimates=False)
+        i = O.argmin_key(r["s1"], r["s2"])
+        rec = torch.tensor([to_i64(pack_key(r["s1"][i], r["s2"][i])), first + i], dtype=torch.int64)
+        g = global_best(rec, cpu_reduce)
+        q.put((rank, g.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_tiered_argmin():
+    """Two-tier scoring shards like plain scoring: per-rank records + one
+    16-B min-loc exchange == the single-process tiered argmin."""
+    N, world = 3000, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_tier_worker, args=(r, world, port, N, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    from workloads.synth import make_tiers
+    p = make_config("C3")
+    full = O.Oracle(p).tiered_range(make_tiers(), O.RANDOM, 0, N, seed=1, estimates=False)
+    want = O.argmin_key(full["s1"], full["s2"])
+    for _, g in res:
+        assert g[1] == want
