@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 import __graft_entry__  # noqa: E402
 from paper_2407_00047_b200 import RwtEstimator  # noqa: E402
-from workloads.synth import balanced_row, make_config  # noqa: E402
+from workloads.synth import balanced_row, make_config, make_requests, make_tiers  # noqa: E402
 
 
 def main():
@@ -34,8 +34,19 @@ def main():
         e.request_violations(e.random(0, 40, seed=5))
         if p.len_tables is not None:
             e.mc_estimate(e.from_record(rec, seed=1), mc_seed=2, trials=100)
+        # two-tier swapping (R20): warp-specialised TIER path, thread kernel, lane-per-queue kernel
+        e.set_tiers(make_tiers((0, 1, 2, 3)[: p.M], tuple(range(p.D))))
+        e.tiered_score_estimate(cand, out=bufs, rec=torch.empty(2, dtype=torch.int64, device="cuda"))
+        e.tiered_score_estimate(e.random(0, 300, seed=2))
+        e.tiered_score_estimate(e.from_record(rec, seed=1))
         torch.cuda.synchronize()
         print(cfg, "ok", flush=True)
+    # request-group formation (R21)
+    from paper_2407_00047_b200 import form_groups
+    form_groups(make_requests(20000, seed=1), 4, [5, 3, 1, 8], limit=64, max_iter=20)
+    form_groups(make_requests(3000, seed=2), 4, [2, 2, 2, 2], limit=1, max_iter=5)
+    torch.cuda.synchronize()
+    print("groups ok", flush=True)
 
 
 if __name__ == "__main__":
