@@ -999,3 +999,28 @@ def test_tiers_from_device_record_and_neighbor():
     ref = o.tiered_range(t, O.NEIGHBOR, 0, n, seed=4, rows=base, moves=2)
     check_scores(out["s1"].cpu().numpy(), out["s2"].cpu().numpy(), ref, p)
     check_estimates(out, ref)
+
+
+def test_c5_full_1e8_candidates():
+    # BASELINE.json C5 at its full size on one GPU: 1e8 RANDOM candidates scored
+    # (s1/s2 arrays, 0.8 GB) and the argmin record; the record must be the
+    # lexicographic minimum of the arrays, and the oracle re-scores the winner
+    # and a strided sample of 101 candidates.
+    p = make_config("C5")
+    e = est_of(p)
+    N = 100_000_000
+    cand = e.random(0, N, seed=1)
+    s1, s2, _ = e.score_orderings(cand, with_n_over=False)
+    rec = e.best_ordering_async(cand)
+    torch.cuda.synchronize()
+    k = int(rec[1])
+    m1 = torch.min(s1)
+    tie = torch.nonzero(s1 == m1).flatten()
+    m2 = torch.min(s2[tie])
+    first = int(tie[torch.nonzero(s2[tie] == m2).flatten()[0]])
+    assert k == first
+    o = O.Oracle(p)
+    for c in list(range(0, N, N // 100)) + [k]:
+        r1, r2, _ = o.score(O.random_row(1, c, p.T))
+        assert abs(float(s1[c]) - r1) <= 1e-5
+        assert abs(float(s2[c]) - r2) <= 1e-5 * abs(r2 + 2 * p.slo.sum()) + 1e-6
