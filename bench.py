@@ -8,11 +8,11 @@ C3 (64 groups, 4 models, 8 virtual queues) on every GPU:
             per-(group, candidate) wt / sd / v written to HBM (768 MB fp32),
             S1/S2 and the argmin record
   a8        global min-loc: NCCL all-gather of 16-B records + reduce kernel
-  a9        decode of the global winner (queue, position per group), on a
-            side stream overlapping the MC sampler (they are independent)
+  a9        decode of the global winner (queue, position per group)
   a10-a12   MC check of the winner: qlm_mc_sample (1221 Philox trials per
-            GPU, candidate-independent) then qlm_mc_count of the winner; counts
-            summed with one NCCL all-reduce.  (Running the sampler on a second
+            GPU, candidate-independent: on a side stream after the fused pass,
+            overlapping a8/a9) then qlm_mc_count of the winner; counts summed
+            with one NCCL all-reduce.  (Running the sampler on a second
             stream concurrently with the fused scan was measured: the step
             gains ~2 % while the scan slows by the same SM time, so the step
             keeps them sequential for a clean per-kernel roofline.)
@@ -234,7 +234,7 @@ def run_ours(args, rank, world, local_rank):
     counts = torch.empty((1, G), dtype=torch.int32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     side = torch.cuda.Stream(dev)
-    ev_g, ev_d = torch.cuda.Event(), torch.cuda.Event()
+    ev_f, ev_s = torch.cuda.Event(), torch.cuda.Event()
 
     def step(kt=None, groups_host=None, out_host=None):
         if groups_host is not None:
@@ -244,19 +244,18 @@ def run_ours(args, rank, world, local_rank):
         est.score_estimate(cand, out=bulk, scores=False, rec=rec)   # fused a1-a7
         if kt:
             kt[1].record(stream)
-        g = global_best(rec, est.reduce_records)
+        # a10 (candidate-independent) on a side stream once the fused pass is
+        # done, overlapping the min-loc exchange (NCCL for N > 1) and the decode
+        ev_f.record(stream)
+        side.wait_event(ev_f)
+        est.mc_sample(MC_SEED, MC_TRIALS, trial_first=rank * MC_TRIALS, stream=side)
+        ev_s.record(side)
+        g = global_best(rec, est.reduce_records)                 # a8
         win = est.from_record(g, seed=CANDIDATE_SEED)
-        ev_g.record(stream)                                      # a9 decode on a side stream,
-        side.wait_event(ev_g)                                    # overlapping the MC sampler
-        with torch.cuda.stream(side):
-            qo, po = est.decode(win, stream=side)
-        ev_d.record(side)
-        est.mc_sample(MC_SEED, MC_TRIALS, trial_first=rank * MC_TRIALS)               # a10
-        est.mc_count(win, MC_TRIALS, counts=counts)                                   # a11
-        sum_counts(counts)
-        stream.wait_event(ev_d)
-        qo.record_stream(stream)
-        po.record_stream(stream)
+        qo, po = est.decode(win)                                 # a9
+        stream.wait_event(ev_s)
+        est.mc_count(win, MC_TRIALS, counts=counts)              # a11
+        sum_counts(counts)                                       # a12
         if out_host is not None:                                 # D2H of the step's result
             out_host["rec"].copy_(g, non_blocking=True)
             out_host["qo"].copy_(qo.view(-1), non_blocking=True)
