@@ -9,7 +9,7 @@
  *
  * Citations: "P:Lx" = /root/reference/PAPER.md line x, "S:Lx" = SPEC.md.
  * Every reading of a garbled or silent passage is listed in DESIGN.md
- * ("Readings of the paper", R1..R14) and referenced here by its R-number.
+ * ("Readings of the paper", R1..R21) and referenced here by its R-number.
  *
  * Build: gcc -O2 -ffp-contract=off -fPIC -shared -o liboracle.so qlm_oracle.c -lm
  * (-ffp-contract=off: no FMA contraction, so every + and * below is one IEEE
