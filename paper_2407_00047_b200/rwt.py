@@ -326,7 +326,8 @@ def form_groups(req: dict, M: int, k_per_model, limit: int = 256, max_iter: int 
     k = np.ascontiguousarray(k_per_model, np.int32)
     label = torch.empty(n, dtype=torch.int32, device=dev)
     gof = torch.empty(n, dtype=torch.int32, device=dev)
-    cap = n
+    # groups <= clusters + 2n / ceil(limit / 2): a split leaf keeps >= ceil(limit / 2) members
+    cap = int(min(n, int(k.sum()) + (2 * n) // max(1, (limit + 1) // 2) + 1))
     groups = torch.empty(cap * L.GROUP_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     G, it = C.c_int32(), C.c_int32()
     s = torch.cuda.current_stream(dev) if stream is None else stream
