@@ -180,3 +180,23 @@ def test_form_groups_host_validation(lib):
                     (dict(lab=None), "label_of")]:
         rc, err = call(**kw)
         assert rc == L.QLM_EINVAL and msg in err, (kw, rc, err)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    # no CPU fallback: with the extension absent, the binding raises on first use
+    code = ("import paper_2407_00047_b200 as q\n"
+            "try:\n    q._lib.lib()\nexcept RuntimeError as e:\n    print('RAISED', e)\n")
+    env = dict(os.environ, QLM_LIB_PATH=str(tmp_path / "absent" / "libqlm.so"))
+    out = subprocess.check_output([os.sys.executable, "-c", code], env=env, text=True, cwd=ROOT)
+    assert out.startswith("RAISED") and "not built" in out
+
+
+def test_qlm_create_without_gpu_is_a_named_error(lib):
+    # on a host without an sm_100 device the library refuses instead of falling back
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2407_00047_b200 import RwtEstimator
+    from workloads.synth import make_config
+    with pytest.raises(L.QlmError, match="CUDA device|sm_"):
+        RwtEstimator(make_config("C1"))
