@@ -176,7 +176,19 @@ def cpu_baseline(budget_s: float = 15.0):
                       f"estimates) + MC {trials} of {MC_TRIALS} trials, plain C fp64 oracle "
                       f"(-O2 -ffp-contract=off) split over {cores} host cores (one process each), "
                       f"{tp:.2f} s wall; value = sampled candidates / s",
-            "single_core": {"value": n / t1, "cores": 1, "seconds": round(t1, 3)}}
+            "single_core": {"value": n / t1, "cores": 1, "seconds": round(t1, 3)},
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, rank, world):
