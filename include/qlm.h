@@ -46,7 +46,7 @@ typedef enum {
     QLM_ENOMEM = 2,     /* device allocation failed                             */
     QLM_ECUDA = 3,      /* CUDA runtime error / unsupported device              */
     QLM_EBADORDER = 5,  /* a row is not a permutation of 0..T-1 (Eq. 6)         */
-    QLM_ERANGE = 6      /* T > 65535, ENUM index >= T!, index overflow          */
+    QLM_ERANGE = 6      /* T > 32768, ENUM index >= T!, index overflow          */
 } qlm_status;
 
 typedef struct qlm_ctx qlm_ctx;
@@ -149,7 +149,7 @@ typedef struct {
  * the device (per-(d,g) W = n*mu/Theta and n*var/Theta^2, per-(d,m) tail),
  * and synchronise.  `tabs` may be NULL (then every dist_id must be -1);
  * `opt` may be NULL (defaults).  Errors: QLM_EINVAL (named field), QLM_ERANGE
- * (T > 65535), QLM_ECUDA (no sm_100 device), QLM_ENOMEM.                     */
+ * (T = G+Q-1 > 32768), QLM_ECUDA (no sm_100 device), QLM_ENOMEM.             */
 QLM_API int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int32_t Q,
                const qlm_profile *prof, const qlm_len_tables *tabs, const qlm_options *opt,
                qlm_ctx **out);
@@ -192,7 +192,9 @@ QLM_API int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best
  * SLO is violated in candidate first + k (mean of the per-request R8/R9
  * probabilities), device fp32 [G][count]; s1_req[k] = sum n_i f_i / sum n_i,
  * device fp32 [count].  Both nullable.  One warp per candidate, O(sum n_i)
- * work per candidate: meant for evaluating winners and short lists.        */
+ * work per candidate: meant for evaluating winners and short lists.
+ * QLM_ERANGE when one candidate's per-group state does not fit in shared
+ * memory (G above about 11000).                                            */
 QLM_API int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac,
                            float *s1_req, void *stream);
 

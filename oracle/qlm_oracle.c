@@ -153,6 +153,19 @@ void or_enum_row(uint64_t c, int32_t T, int32_t *row)
     }
 }
 
+/* Row validity (Eq. 6): a permutation of 0..T-1.  Returns 1 if valid.     */
+static int or_is_permutation(const int32_t *row, int32_t T)
+{
+    char *seen = (char *)calloc((size_t)(T > 0 ? T : 1), 1);
+    int ok = 1;
+    for (int32_t s = 0; s < T && ok; ++s) {
+        if (row[s] < 0 || row[s] >= T || seen[row[s]]) ok = 0;
+        else seen[row[s]] = 1;
+    }
+    free(seen);
+    return ok;
+}
+
 /* ---- RWT estimator over one ordering ------------------------------------ */
 
 /* C - W for a group of model m on device d: P + D with D = max_out*eps*d
@@ -180,13 +193,7 @@ int or_estimate_row(const or_problem *p, const int32_t *row,
                     double *wt, double *V, int32_t *queue_of, int32_t *pos_of)
 {
     int32_t T = p->G + p->Q - 1;
-    char seen[4096];
-    if (T > 4096) return -1;
-    memset(seen, 0, (size_t)T);
-    for (int32_t s = 0; s < T; ++s) {
-        if (row[s] < 0 || row[s] >= T || seen[row[s]]) return -1;
-        seen[row[s]] = 1;
-    }
+    if (!or_is_permutation(row, T)) return -1;
     int32_t q = 0;
     int32_t d = p->q_device[0], prev = p->q_resident[0], first = 1, pos = 0;
     double A = p->q_bmean[0], B = p->q_bvar[0];
@@ -403,16 +410,7 @@ int64_t or_mc_count(const or_problem *p, int kind, const void *rows, int32_t tok
         get_row(kind, rows, token_bytes, stride, seed, first + (uint64_t)c, c, T, row);
         uint32_t *cnt = counts + c * G;
         for (int32_t i = 0; i < G; ++i) cnt[i] = 0;
-        char seen[4096];
-        int ok = T <= 4096;
-        if (ok) {
-            memset(seen, 0, (size_t)T);
-            for (int32_t s = 0; s < T; ++s) {
-                if (row[s] < 0 || row[s] >= T || seen[row[s]]) { ok = 0; break; }
-                seen[row[s]] = 1;
-            }
-        }
-        if (!ok) { ++bad; continue; }
+        if (!or_is_permutation(row, T)) { ++bad; continue; }
         for (int64_t t = 0; t < trial_count; ++t) {
             const uint32_t *x = X + t * G;
             int32_t q = 0;
@@ -487,13 +485,8 @@ int or_estimate_row_tiered(const or_problem *p, const or_tiers *t, const int32_t
                            double *wt, double *V, int32_t *cold_of)
 {
     int32_t T = p->G + p->Q - 1;
-    char seen[4096], tier[64];            /* tier: 0 = not a target yet, 1 warm, 2 cold */
-    if (T > 4096 || p->M > 64) return -1;
-    memset(seen, 0, (size_t)T);
-    for (int32_t s = 0; s < T; ++s) {
-        if (row[s] < 0 || row[s] >= T || seen[row[s]]) return -1;
-        seen[row[s]] = 1;
-    }
+    char tier[64];                        /* tier: 0 = not a target yet, 1 warm, 2 cold */
+    if (p->M > 64 || !or_is_permutation(row, T)) return -1;
     int32_t q = 0;
     int32_t d = p->q_device[0], prev = p->q_resident[0], first = 1;
     double A = p->q_bmean[0], B = p->q_bvar[0];

@@ -250,7 +250,9 @@ int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int3
     *out = nullptr;
     if (!groups || G < 1) return fail(QLM_EINVAL, "G=%d must be >= 1 with non-NULL groups", G);
     if (!queues || Q < 1) return fail(QLM_EINVAL, "Q=%d must be >= 1 with non-NULL queues", Q);
-    if ((int64_t)G + Q - 1 > 65535) return fail(QLM_ERANGE, "T=G+Q-1=%lld > 65535", (long long)G + Q - 1);
+    // T <= 32768: every scoring path keeps a candidate's row (4T bytes with its
+    // swap targets) in one warp's shared memory (qlm_big.cu)
+    if ((int64_t)G + Q - 1 > 32768) return fail(QLM_ERANGE, "T=G+Q-1=%lld > 32768", (long long)G + Q - 1);
     if (!prof) return fail(QLM_EINVAL, "prof is NULL");
     const int D = prof->D, M = prof->M;
     if (D < 1 || M < 1 || D > 64 || M > 64)
@@ -702,6 +704,11 @@ int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac
     if (cand->count == 0 || (!frac && !s1_req)) return QLM_OK;
     ScanParams p = base_params(ctx, cand);
     cudaError_t e = launch_req(p, ctx->d_groups, frac, s1_req, static_cast<cudaStream_t>(stream));
+    if (e == cudaErrorInvalidConfiguration) {
+        cudaGetLastError();
+        return fail(QLM_ERANGE, "request violations keep 20 B per group and 4 B per token of one "
+                    "candidate in shared memory: G=%d is too large (about 11000 at most)", ctx->dm.G);
+    }
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "request-violations kernel");
 }
 

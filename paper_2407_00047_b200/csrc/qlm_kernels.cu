@@ -935,9 +935,18 @@ cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st) {
         cudaGetLastError();
     }
     if (p.cd.kind == QLM_CAND_RANDOM && p.dm.T > 256 && p.ilv && p.ilv_cap >= 32 &&
-        p.chunk_recs && !p.cd.first_from && p.cd.count >= 4096)
-        return launch_two_phase(p, st);
-    return launch_scan(p, st);
+        p.chunk_recs && !p.cd.first_from && p.cd.count >= 4096) {
+        e = launch_two_phase(p, st);
+    } else {
+        e = launch_scan(p, st);
+    }
+    if (e == cudaErrorInvalidValue || e == cudaErrorInvalidConfiguration || e == cudaErrorNotSupported) {
+        // no shared-memory plan of the scan kernels fits (very large G): the
+        // warp-per-candidate path with global tables rewrites every output
+        cudaGetLastError();
+        return launch_big(p, st);
+    }
+    return e;
 }
 
 cudaError_t launch_scan(ScanParams p, cudaStream_t st) {

@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256) req_kernel(const ScanParams p, const qlm_
     const Dims dm = p.dm;
     const int G = dm.G, Q = dm.Q, T = dm.T, M = dm.M;
     const Cand cd = p.cd;
-    const int64_t loc = (int64_t)blockIdx.x * kReqWarps + warp;
+    const int64_t loc = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (loc >= cd.count) return;                              // warp-uniform
     int64_t first = cd.first;
     if (cd.first_from) {
@@ -112,15 +112,17 @@ cudaError_t launch_req(const ScanParams &p, const qlm_group *groups, float *frac
     const Dims &dm = p.dm;
     const int warp_bytes = (int)(((size_t)16 * dm.G + 4 * (size_t)dm.G + 4 * (size_t)(dm.Q + 1) +
                                   4 * (size_t)((dm.T + 7) & ~7) + 15) & ~size_t(15));
-    const size_t smem = (size_t)warp_bytes * kReqWarps;
     int optin = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (smem > (size_t)optin) return cudaErrorInvalidConfiguration;
+    int W = (int)(((size_t)optin - 1024) / (size_t)warp_bytes);   // up to 8 warps (one per candidate)
+    if (W > kReqWarps) W = kReqWarps;
+    if (W < 1) return cudaErrorInvalidConfiguration;
+    const size_t smem = (size_t)warp_bytes * W;
     cudaError_t e = cudaFuncSetAttribute(req_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int64_t grid = (p.cd.count + kReqWarps - 1) / kReqWarps;
-    req_kernel<<<(unsigned)grid, 32 * kReqWarps, smem, st>>>(p, groups, frac, s1r, warp_bytes);
+    const int64_t grid = (p.cd.count + W - 1) / W;
+    req_kernel<<<(unsigned)grid, 32 * W, smem, st>>>(p, groups, frac, s1r, warp_bytes);
     ++g_launches;
     return cudaGetLastError();
 }

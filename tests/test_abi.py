@@ -146,9 +146,9 @@ def test_queue_and_profile_validation(lib):
     assert rc == L.QLM_EINVAL and "tabs.K=3" in msg
     rc, msg = _create(lib, g, q, opt=L.Options(-1.0, 0.01, 0, 0))
     assert rc == L.QLM_EINVAL and "z_clamp" in msg
-    big = np.zeros(70000, L.GROUP_DTYPE)
+    big = np.zeros(40000, L.GROUP_DTYPE)
     rc, msg = _create(lib, big, q)
-    assert rc == L.QLM_ERANGE and "65535" in msg
+    assert rc == L.QLM_ERANGE and "32768" in msg
 
 
 def test_null_context_calls_fail_cleanly(lib):

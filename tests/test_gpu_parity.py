@@ -1024,3 +1024,38 @@ def test_c5_full_1e8_candidates():
         r1, r2, _ = o.score(O.random_row(1, c, p.T))
         assert abs(float(s1[c]) - r1) <= 1e-5
         assert abs(float(s2[c]) - r2) <= 1e-5 * abs(r2 + 2 * p.slo.sum()) + 1e-6
+
+
+@pytest.mark.parametrize("G,Q", [(3000, 8), (12000, 40)])
+def test_very_large_G_fallback(G, Q):
+    # beyond every shared-memory plan of the scan kernels: warp per candidate,
+    # lane per queue, global tables (qlm_big.cu); scores, argmin and bulk
+    p = make_problem(G, Q, name=f"G{G}")
+    e = est_of(p)
+    o = O.Oracle(p)
+    n = 96
+    s1, s2, no = e.score_orderings(e.random(5, n, seed=1))
+    ref = o.score_range(O.RANDOM, 5, n, seed=1)
+    check_scores(s1.cpu().numpy(), s2.cpu().numpy(), ref, p)
+    assert np.array_equal(no.cpu().numpy(), ref["n_over"])
+    best = e.best_ordering(e.random(5, n, seed=1))
+    ok, _ = argmin_ok(best["index"], ref["s1"], ref["s2"], p, first=5)
+    assert ok
+    dec = o.estimate(O.random_row(1, best["index"], p.T))
+    assert np.array_equal(best["queue_of_group"], dec["queue"])
+    m = 24
+    out = e.rwt_estimate(e.random(7, m, seed=2))
+    eref = o.estimate_range(O.RANDOM, 7, m, seed=2)
+    check_estimates(out, eref)
+    # wt in the oracle's sequential order: bit-identical
+    assert np.array_equal(out["wt"].cpu().numpy().astype(np.float64).T,
+                          eref["wt"].astype(np.float32).astype(np.float64))
+
+
+def test_request_violations_large_G():
+    p = make_problem(1600, 8, name="G1600")
+    e = est_of(p)
+    frac, s1r = e.request_violations(e.random(0, 9, seed=3))
+    ref = O.Oracle(p).request_violations_range(O.RANDOM, 0, 9, seed=3)
+    assert np.max(np.abs(s1r.cpu().numpy() - ref["s1"])) <= 1e-5
+    assert np.max(np.abs(frac.cpu().numpy().T - ref["frac"])) <= 1e-5
