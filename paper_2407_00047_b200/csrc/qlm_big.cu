@@ -17,6 +17,7 @@
 
 namespace qlm {
 
+template <bool TIER>
 __global__ void __launch_bounds__(256) big_kernel(const ScanParams p, int ldr) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
@@ -64,6 +65,9 @@ __global__ void __launch_bounds__(256) big_kernel(const ScanParams p, int ldr) {
             double A = qr.bmean, B = qr.bvar;
             int prev = qr.r;
             bool firsts = true;
+            uint32_t seen = 0u, warm = 0u;                // two-tier state (R20), per queue
+            int cum = 0;
+            bool exh = false;
             const int s1 = qbeg[q + 1] - 1;
             for (int s = qbeg[q]; s < s1; ++s) {
                 const int g = srow[s];
@@ -71,6 +75,16 @@ __global__ void __launch_bounds__(256) big_kernel(const ScanParams p, int ldr) {
                 const int m = gr.model;
                 if (m != prev) {                          // one transition term (R1/R2/R4/R12)
                     double trans = __ldg(&p.tb.swap[(d * M + prev) * M + m]);
+                    if constexpr (TIER) {                 // R20: cold targets pay the registry load
+                        const uint32_t bit = 1u << m;
+                        if (!(seen & bit)) {
+                            seen |= bit;
+                            const int need = cum + __ldg(&p.t_mem[m]);
+                            if (!exh && need <= __ldg(&p.t_cap[d])) { warm |= bit; cum = need; }
+                            else exh = true;
+                        }
+                        if (!(warm & bit)) trans = __dadd_rn(trans, __ldg(&p.t_load[d * M + m]));
+                    }
                     if (!firsts || qr.backlog) trans = __dadd_rn(__ldg(&p.tb.tail[d * M + prev]), trans);
                     A = __dadd_rn(A, trans);
                 }
@@ -118,7 +132,9 @@ __global__ void __launch_bounds__(256) big_kernel(const ScanParams p, int ldr) {
     }
 }
 
-cudaError_t launch_big(const ScanParams &p, cudaStream_t st) {
+template <bool TIER>
+static cudaError_t launch_big_t(const ScanParams &p, cudaStream_t st) {
+    auto kern = big_kernel<TIER>;
     const Dims &dm = p.dm;
     const int ldr = (dm.T + 7) & ~7;
     const size_t per_warp = ((size_t)4 * ldr + 4 * (size_t)(dm.Q + 1) + 15) & ~size_t(15);
@@ -126,25 +142,28 @@ cudaError_t launch_big(const ScanParams &p, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, big_kernel);
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
     const size_t avail = (size_t)optin > fa.sharedSizeBytes + 1024 ? (size_t)optin - fa.sharedSizeBytes - 1024 : 0;
     int W = (int)(avail / per_warp);
     if (W > 8) W = 8;
     if (W < 1) return cudaErrorNotSupported;
     const size_t smem = per_warp * W;
-    if ((e = cudaFuncSetAttribute(big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
         return e;
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, big_kernel, 32 * W, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * W, smem);
     if (nb < 1) nb = 1;
     int64_t grid = (p.cd.count + W - 1) / W;
     if (grid > (int64_t)sm_count() * nb) grid = (int64_t)sm_count() * nb;
     if (grid > p.max_blocks) grid = p.max_blocks;
     if (grid < 1) grid = 1;
-    big_kernel<<<(unsigned)grid, 32 * W, smem, st>>>(p, ldr);
+    kern<<<(unsigned)grid, 32 * W, smem, st>>>(p, ldr);
     ++g_launches;
     return cudaGetLastError();
 }
+
+cudaError_t launch_big(const ScanParams &p, cudaStream_t st) { return launch_big_t<false>(p, st); }
+cudaError_t launch_big_tier(const ScanParams &p, cudaStream_t st) { return launch_big_t<true>(p, st); }
 
 }  // namespace qlm

@@ -52,6 +52,7 @@ cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st); // same, two-tier swa
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st);   // ws, else scan
 cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per candidate (large G)
 cudaError_t launch_big(const ScanParams &p, cudaStream_t st);       // very large G: global tables
+cudaError_t launch_big_tier(const ScanParams &p, cudaStream_t st);  // same, two-tier swapping (R20)
 cudaError_t launch_req(const ScanParams &p, const qlm_group *groups, float *frac, float *s1r,
                        cudaStream_t st);                            // request-level (R19)
 cudaError_t launch_tier(const ScanParams &p, cudaStream_t st);     // two-tier swapping (R20)

@@ -448,6 +448,8 @@ cudaError_t launch_tier(const ScanParams &p, cudaStream_t st) {
     if (p.dm.G > 256 && !(nw && *nw && *nw != '0')) {        // large G: lane per queue
         const cudaError_t w = launch_tier_warp(p, st);
         if (w != cudaErrorNotSupported) return w;
+        cudaGetLastError();
+        return launch_big_tier(p, st);                        // tables too large for shared memory
     }
     const bool u8 = p.dm.T <= 256;
     switch (p.cd.kind) {

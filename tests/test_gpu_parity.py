@@ -1059,3 +1059,23 @@ def test_request_violations_large_G():
     ref = O.Oracle(p).request_violations_range(O.RANDOM, 0, 9, seed=3)
     assert np.max(np.abs(s1r.cpu().numpy() - ref["s1"])) <= 1e-5
     assert np.max(np.abs(frac.cpu().numpy().T - ref["frac"])) <= 1e-5
+
+
+def test_tiers_very_large_G():
+    # two-tier scoring past the lane-per-queue kernel's shared-memory tile:
+    # the global-table fallback with the tier state (R20)
+    from workloads.synth import make_random_tiers
+    rng = np.random.default_rng(77)
+    p = make_random_problem(rng, 3000, 12, 4, 2, backlog=True)
+    tiers = make_random_tiers(rng, 4, 2)
+    e = est_of(p)
+    e.set_tiers(tiers)
+    n = 64
+    out, rec = _tier_out(e, e.random(3, n, seed=9))
+    ref = O.Oracle(p).tiered_range(tiers, O.RANDOM, 3, n, seed=9)
+    check_estimates(out, ref)
+    check_scores(out["s1"].cpu().numpy(), out["s2"].cpu().numpy(), ref, p)
+    ok, _ = argmin_ok(int(rec[1]), ref["s1"], ref["s2"], p, first=3)
+    assert ok
+    assert np.array_equal(out["wt"].cpu().numpy().astype(np.float64).T,
+                          ref["wt"].astype(np.float32).astype(np.float64))
