@@ -1,5 +1,10 @@
-import sys, traceback
-sys.path.insert(0, '/root/repo')
+"""Size envelope of the C ABI: which entry points run for G up to T = 32768.
+
+    python tools/probe_sizes.py
+"""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import __graft_entry__
 __graft_entry__.build()
