@@ -355,10 +355,12 @@ def run_ours(args, rank, world, local_rank):
         bulk_bytes = N_PER_GPU * G * 3 * 4                     # algorithmic: outputs only (RANDOM)
         kname = ("ws_kernel<RANDOM,u8,SCORE,RS=3>" if G <= 256 else "scan_kernel<RANDOM,u16,DIRECT,SCORE>")
         bulk_gbs = bulk_bytes / (fused_ms / 1e3) / 1e9
-        traffic = None
+        traffic, winstr = None, None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get(CFG, {}).get("scan_kernel_dram_bytes_per_launch")
+                nt_ = json.load(f).get(CFG, {})
+                traffic = nt_.get("scan_kernel_dram_bytes_per_launch")
+                winstr = nt_.get("smsp_inst_executed_per_launch")
         except Exception:
             pass
         roofline = {"kernel": kname + " (qlm_score_estimate, fused a1-a7)", "bound": "hbm",
@@ -367,6 +369,16 @@ def run_ours(args, rank, world, local_rank):
                     "algorithmic_bytes_per_launch": bulk_bytes,
                     "bytes_per_unit": G * 12, "units_per_launch": N_PER_GPU,
                     "kernel_ms": fused_ms, "peak_source": peak_src}
+        if winstr:
+            # context for the HBM fraction: the same kernel against the SM issue
+            # roof (4 schedulers x 1 warp instruction / cycle x 148 SMs at the
+            # sampled clock), with the ncu-measured warp instructions per launch
+            clk_mhz = clk.summary().get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
+            ipeak = 148 * 4 * clk_mhz * 1e6
+            roofline["issue"] = {"achieved": winstr / (fused_ms / 1e3), "peak": ipeak,
+                                 "unit": "warp instructions/s", "frac": winstr / (fused_ms / 1e3) / ipeak,
+                                 "inst_per_launch": winstr,
+                                 "source": "profiles/ncu_traffic.json (smsp__inst_executed.sum)"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
