@@ -232,12 +232,20 @@ def run_ours(args, rank, world, local_rank):
     from workloads.synth import make_config, CANDIDATE_SEED, MC_SEED
 
     __graft_entry__.build()
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # QLM_BENCH_SHARE_GPU=1 (plumbing check only): several ranks on one GPU
+    # over gloo, exercising the N > 1 code path where only one GPU exists;
+    # the driver's multi-GPU runs use NCCL with one GPU per rank
+    share = os.environ.get("QLM_BENCH_SHARE_GPU", "0") == "1"
+    gpu = local_rank % torch.cuda.device_count() if share else local_rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     p = make_config(CFG)
-    est = RwtEstimator(p, device=local_rank)
+    est = RwtEstimator(p, device=gpu)
     G = p.G
     stream = torch.cuda.current_stream(dev)
     cand = est.random(first=rank * N_PER_GPU, count=N_PER_GPU, seed=CANDIDATE_SEED)
@@ -290,8 +298,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize()
     l0 = kernel_launches()
-    with ClockSampler(torch.cuda.get_device_properties(dev).index if hasattr(
-            torch.cuda.get_device_properties(dev), "index") else local_rank) as clk:
+    with ClockSampler(gpu) as clk:
         e0.record(stream)
         for k in range(K):
             step(kts[k])
