@@ -37,6 +37,7 @@ struct alignas(64) WsParams {
     CUtensorMap tmap[3];   // wt, sd, v: fp32 [G][count], box {32, G}
     ScanParams p;
     int pairs;             // W
+    int spread;            // 1: producers only on schedulers 2/3 (16-warp block), see launch
     int tw;                // 32-bit words per row slot column
     int off_rows, off_stage, off_bar, off_pend, off_tmem;
     int stage_floats;      // per consumer warp: 3 * G * 32
@@ -376,13 +377,27 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
     const Cand cd = p.cd;
     const int64_t count = cd.count, first = cd.first;
     const int64_t nbatch = (count + 31) >> 5;
-    const int pair = warp % W;
-    const bool producer = warp >= W;
+    // Role of this warp.  Default: warps [0, W) consume, [W, 2W) produce.
+    // spread (W = 6, 16 warps): consumers 0-5 (two per scheduler on 0/1, one
+    // on 2/3), producers 6, 7, 10, 11, 14, 15 (schedulers 2/3 only), warps
+    // 8, 9, 12, 13 idle -- every scheduler then issues one consumer's worth
+    // plus at most three producers' instead of 2 + 1 / 1 + 2.
+    int pair = warp % W;
+    bool producer = warp >= W;
+    bool idle = false;
+    if (w.spread) {
+        producer = warp >= 6;
+        const int pmap[16] = {0, 1, 2, 3, 4, 5, 0, 1, -1, -1, 2, 3, -1, -1, 4, 5};
+        pair = pmap[warp];
+        idle = pair < 0;
+    }
     const int64_t grid = gridDim.x;
     uint64_t bkey = ~0ull;
     int64_t bidx = -1;
 
-    if (producer) {
+    if (idle) {
+        // no role: only the block-wide argmin below
+    } else if (producer) {
         for (int j = 0;; ++j) {
             const int64_t b = blockIdx.x + (int64_t)(pair + j * W) * grid;
             if (b >= nbatch) break;
@@ -567,7 +582,7 @@ static cudaError_t launch_ws_rs(WsParams &w, size_t smem, int W, cudaStream_t st
     if (grid > need) grid = need;
     if (grid > w.p.max_blocks) grid = w.p.max_blocks;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, 64 * W, smem, st>>>(w);
+    kern<<<(unsigned)grid, w.spread ? 512 : 64 * W, smem, st>>>(w);
     ++g_launches;
     return cudaGetLastError();
 }
@@ -598,6 +613,9 @@ static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
     }
     if (bestW < (STAGE ? 2 : 4)) return cudaErrorNotSupported;
     plan_ws(w, bestW, bestRs, sizeof(TOK), STAGE, TIER);
+    // W = 6: spread the roles over the four schedulers (measured C3 fused pass
+    // 0.370 -> 0.350 ms); QLM_WS_SPREAD=0 restores the plain warp order
+    w.spread = (bestW == 6 && env_int_ws("QLM_WS_SPREAD", 1)) ? 1 : 0;
     if (STAGE) {
         const bool aligned = (p0.cd.count % 4 == 0) && (!p0.wt || ((uintptr_t)p0.wt & 15) == 0) &&
                              (!p0.sd || ((uintptr_t)p0.sd & 15) == 0) &&
