@@ -94,19 +94,33 @@ void or_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32
  * A candidate is a row of T = G+Q-1 tokens: a permutation of 0..T-1 where
  * token < G is a request group and token >= G separates virtual queues.    */
 
-/* RANDOM(seed, c): forward Fisher-Yates driven by Philox words (R10).     */
+/* RANDOM(seed, c): forward Fisher-Yates driven by Philox words (R10).
+ * T > 256: step i draws the 32-bit word i mod 4 of block i/4,
+ *          j = i + floor(u * (T - i) / 2^32);
+ * T <= 256: step i draws the 16-bit half (low for even i, high for odd i)
+ *          of word (i/2) mod 4 of block i/8, j = i + floor(u * (T - i) / 2^16)
+ *          (8 draws per Philox block; per-index bias <= (T - i) / 2^16).      */
 void or_random_row(uint64_t seed, uint64_t c, int32_t T, int32_t *row)
 {
     uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
     uint32_t words[4];
+    int d16 = T <= 256;
+    int per_block = d16 ? 8 : 4;
     for (int32_t k = 0; k < T; ++k) row[k] = k;
     for (int32_t i = 0; i + 1 < T; ++i) {
-        if (i % 4 == 0) {            /* one Philox block yields words 4b..4b+3 */
-            uint32_t ctr[4] = { (uint32_t)(i / 4), (uint32_t)c, (uint32_t)(c >> 32), 0x514C4D00u };
+        if (i % per_block == 0) {    /* one Philox block per 4 (or 8 half-word) draws */
+            uint32_t ctr[4] = { (uint32_t)(i / per_block), (uint32_t)c, (uint32_t)(c >> 32), 0x514C4D00u };
             or_philox4x32_10(ctr, key, words);
         }
-        uint32_t u = words[i % 4];
-        int32_t j = i + (int32_t)(((uint64_t)u * (uint64_t)(T - i)) >> 32);
+        int32_t j;
+        if (d16) {
+            uint32_t w = words[(i / 2) % 4];
+            uint32_t u = (i % 2 == 0) ? (w & 0xFFFFu) : (w >> 16);
+            j = i + (int32_t)((u * (uint32_t)(T - i)) >> 16);
+        } else {
+            uint32_t u = words[i % 4];
+            j = i + (int32_t)(((uint64_t)u * (uint64_t)(T - i)) >> 32);
+        }
         int32_t t = row[i]; row[i] = row[j]; row[j] = t;
     }
 }

@@ -70,6 +70,18 @@ def test_random_rows_uniform_over_permutations():
            [tuple(O.random_row(2, c, 20)) for c in range(5)]
 
 
+@pytest.mark.parametrize("T", [200, 300])
+def test_random_rows_first_position_uniform(T):
+    # row[0] after the whole Fisher-Yates is the first step's target j_0, which
+    # must be uniform on [0, T): chi-square over 60k rows, both draw widths
+    # (16-bit halves for T <= 256, 32-bit words above; R10)
+    N = 60000
+    first = np.array([O.random_row(3, c, T)[0] for c in range(N)])
+    counts = np.bincount(first, minlength=T)
+    chi2 = float(((counts - N / T) ** 2 / (N / T)).sum())
+    assert stats.chi2.sf(chi2, T - 1) > 1e-3
+
+
 # ---------------------------------------------------------------- SPEC worked examples
 def test_wait_mean_and_std_S279():
     g = gold("spec_examples.json")["wait_S279"]
