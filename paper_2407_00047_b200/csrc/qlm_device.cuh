@@ -88,45 +88,8 @@ __device__ __forceinline__ TOK *fy_elem(uint8_t *base, int i, int blk, int tid) 
                                    (u * (unsigned)sizeof(TOK) + (u / EPW) * (4u * (unsigned)blk - 4u)));
 }
 
-// Forward Fisher-Yates over T tokens (R10); calls f(token) for positions
-// 0..T-1 in order, each as soon as it is final (fused generation + scan).
-template <typename TOK, typename F>
-__device__ __forceinline__ void tokens_random(uint8_t *scratch, int blk, int tid, int T,
-                                              uint64_t seed, uint64_t c, F &&f) {
-    constexpr int EPW = 4 / (int)sizeof(TOK);
-    uint32_t *w32 = reinterpret_cast<uint32_t *>(scratch);
-    const int nw = (T + EPW - 1) / EPW;
-    for (int w = 0; w < nw; ++w)
-        w32[w * blk + tid] = EPW == 4 ? 0x03020100u + 0x04040404u * (uint32_t)w
-                                      : 0x00010000u + 0x00020002u * (uint32_t)w;
-    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    const uint32_t clo = (uint32_t)c, chi = (uint32_t)(c >> 32);
-    for (int i0 = 0; i0 < T; i0 += 4) {
-        uint4 wd = make_uint4(0u, 0u, 0u, 0u);
-        if (i0 < T - 1) wd = philox10(make_uint4((uint32_t)(i0 >> 2), clo, chi, kRowTag), key);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = i0 + k;
-            if (i >= T) break;
-            TOK *pi = fy_elem<TOK>(scratch, i, blk, tid);
-            int tok;
-            if (i < T - 1) {
-                const int j = i + (int)__umulhi(pick4(wd, k), (uint32_t)(T - i));
-                TOK *pj = fy_elem<TOK>(scratch, j, blk, tid);
-                const TOK ti = *pi, tj = *pj;
-                *pj = ti;
-                tok = tj;
-            } else {
-                tok = *pi;
-            }
-            f(tok);
-        }
-    }
-}
-
 // Forward Fisher-Yates materialised in place: after the call, element s of
-// the thread's scratch row holds token s (the same permutation tokens_random
-// streams).  Used by the two-phase scan (generate, then walk 4 tokens/load).
+// the thread's scratch row holds token s.  Used by the two-phase scan (generate, then walk 4 tokens/load).
 template <typename TOK>
 __device__ __forceinline__ void fy_materialise(uint8_t *scratch, int blk, int tid, int T,
                                                uint64_t seed, uint64_t c) {
@@ -142,22 +105,38 @@ __device__ __forceinline__ void fy_materialise(uint8_t *scratch, int blk, int ti
     // positions > i only), so finals are packed in a register and written one
     // 32-bit word at a time instead of one sub-word store per step.
     uint32_t fin = 0;
-    for (int i0 = 0; i0 < T - 1; i0 += 4) {
-        const uint4 wd = philox10(make_uint4((uint32_t)(i0 >> 2), clo, chi, kRowTag), key);
+    auto step = [&](int i, int j) {
+        TOK *pi = fy_elem<TOK>(scratch, i, blk, tid);
+        TOK *pj = fy_elem<TOK>(scratch, j, blk, tid);
+        const TOK ti = *pi, tj = *pj;
+        *pj = ti;
+        const int lanepos = i % EPW;
+        fin |= (uint32_t)tj << (lanepos * 8 * sizeof(TOK));
+        if (lanepos == EPW - 1) {
+            w32[(i / EPW) * blk + tid] = fin;
+            fin = 0;
+        }
+    };
+    if (T <= 256) {                 // R10: two 16-bit draws per word, 8 per Philox block
+        for (int i0 = 0; i0 < T - 1; i0 += 8) {
+            const uint4 wd = philox10(make_uint4((uint32_t)(i0 >> 3), clo, chi, kRowTag), key);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = i0 + k;
-            if (i >= T - 1) break;
-            const int j = i + (int)__umulhi(pick4(wd, k), (uint32_t)(T - i));
-            TOK *pi = fy_elem<TOK>(scratch, i, blk, tid);
-            TOK *pj = fy_elem<TOK>(scratch, j, blk, tid);
-            const TOK ti = *pi, tj = *pj;
-            *pj = ti;
-            const int lanepos = i % EPW;
-            fin |= (uint32_t)tj << (lanepos * 8 * sizeof(TOK));
-            if (lanepos == EPW - 1) {
-                w32[(i / EPW) * blk + tid] = fin;
-                fin = 0;
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + k;
+                if (i >= T - 1) break;
+                const uint32_t w = pick4(wd, k >> 1);
+                const uint32_t u = (k & 1) ? (w >> 16) : (w & 0xFFFFu);
+                step(i, i + (int)((u * (uint32_t)(T - i)) >> 16));
+            }
+        }
+    } else {                        // 32-bit draws, 4 per Philox block
+        for (int i0 = 0; i0 < T - 1; i0 += 4) {
+            const uint4 wd = philox10(make_uint4((uint32_t)(i0 >> 2), clo, chi, kRowTag), key);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = i0 + k;
+                if (i >= T - 1) break;
+                step(i, i + (int)__umulhi(pick4(wd, k), (uint32_t)(T - i)));
             }
         }
     }
@@ -433,14 +412,26 @@ __device__ __forceinline__ void warp_gen_row(const Cand &cd, int T, uint64_t c, 
                                              uint16_t *srow, uint16_t *sJ) {
     const int lane = threadIdx.x & 31;
     if (cd.kind == QLM_CAND_RANDOM) {
-        const int nb = (T - 1 + 3) / 4;
+        const bool d16 = T <= 256;                           // R10 draw width
+        const int per = d16 ? 8 : 4;
+        const int nb = (T - 1 + per - 1) / per;
         const uint2 key = make_uint2((uint32_t)cd.seed, (uint32_t)(cd.seed >> 32));
         for (int b = lane; b < nb; b += 32) {
             const uint4 wd = philox10(make_uint4((uint32_t)b, (uint32_t)c, (uint32_t)(c >> 32), kRowTag), key);
+            if (d16) {
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int i = 4 * b + h;
-                if (i + 1 < T) sJ[i] = (uint16_t)(i + (int)__umulhi(pick4(wd, h), (uint32_t)(T - i)));
+                for (int h = 0; h < 8; ++h) {
+                    const int i = 8 * b + h;
+                    const uint32_t w = pick4(wd, h >> 1);
+                    const uint32_t u = (h & 1) ? (w >> 16) : (w & 0xFFFFu);
+                    if (i + 1 < T) sJ[i] = (uint16_t)(i + (int)((u * (uint32_t)(T - i)) >> 16));
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int i = 4 * b + h;
+                    if (i + 1 < T) sJ[i] = (uint16_t)(i + (int)__umulhi(pick4(wd, h), (uint32_t)(T - i)));
+                }
             }
         }
         for (int s = lane; s < T; s += 32) srow[s] = (uint16_t)s;

@@ -351,6 +351,7 @@ __global__ void reduce_records_kernel(const qlm_record *recs, int n, qlm_record 
 // values of the (at most two) stores issued after a load that may alias it.
 // So the store chain waits on a load issued two steps earlier.  Finals are
 // packed two per word and leave as coalesced 128-B warp stores.
+// Large T only (the two-phase path runs for T > 256): 32-bit draws (R10).
 __global__ void __launch_bounds__(32) fy_rows_kernel(Cand cd, int T, uint32_t *out, int64_t ld) {
     extern __shared__ __align__(16) uint16_t srow16[];
     const int lane = threadIdx.x;
