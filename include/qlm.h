@@ -114,7 +114,9 @@ typedef struct {
 
 /* Candidate kinds (R10, R18):
  *   EXPLICIT  rows given by the caller;
- *   RANDOM    candidate c = Fisher-Yates permutation from Philox(seed, c);
+ *   RANDOM    candidate c = forward Fisher-Yates permutation from Philox(seed, c)
+ *             (R10: 16-bit swap draws, 8 per Philox block, for T <= 256;
+ *             32-bit draws, 4 per block, above);
  *   ENUM      candidate c = the c-th permutation in lexicographic order (T <= 20);
  *   NEIGHBOR  candidate c = the base row `rows` (one row of T tokens) with
  *             `moves` Philox(seed, c)-drawn transpositions (R18; SURVEY 8(f) N1,
