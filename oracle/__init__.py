@@ -83,6 +83,8 @@ def lib():
         _lib.or_score_row_tiered.restype = C.c_int
         _lib.or_tiered_range.argtypes = [P, T, C.c_int, vp, i32, i64, u64, u64, i64, dp, dp, vp, dp, dp]
         _lib.or_tiered_range.restype = i64
+        _lib.or_mc_count_tiered.argtypes = [P, T, C.c_int, vp, i32, i64, u64, u64, i64, vp, i64, vp]
+        _lib.or_mc_count_tiered.restype = i64
         _lib.or_form_groups.argtypes = [i32, i32, vp, vp, vp, vp, i32, vp, i32, i32,
                                         vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]
         _lib.or_form_groups.restype = i32
@@ -232,6 +234,18 @@ class Oracle:
                        v=np.array([[violation(wt[k, i], V[k, i], self.prob.slo[i]) for i in range(G)]
                                    for k in range(count)]) if count * G <= 2000000 else None)
         return out
+
+    def mc_count_tiered(self, tiers, kind, first, count, X, seed=0, rows=None, moves=0):
+        """MC counts under two-tier swapping (R13 + R20)."""
+        rows, tb, stride = self._rows_args(kind, rows, moves)
+        keep, t = self._tiers(tiers)
+        X = np.ascontiguousarray(X, np.uint32)
+        counts = np.zeros((count, self.G), np.uint32)
+        bad = lib().or_mc_count_tiered(C.byref(self.p), C.byref(t), kind, _ptr(rows), tb, stride, seed,
+                                       first, count, _ptr(X), X.shape[0], _ptr(counts))
+        if bad:
+            raise ValueError(f"{bad} invalid rows")
+        return counts
 
     def mc_sample(self, mc_seed, trial_first, trial_count):
         X = np.zeros((trial_count, self.G), np.uint32)

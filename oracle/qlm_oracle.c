@@ -760,3 +760,61 @@ int32_t or_form_groups(int32_t n, int32_t dims, const int32_t *model, const doub
     free(members); free(sum); free(C); free(mind); free(off); free(k_eff); free(ctr_req);
     return gid;
 }
+
+/* MC counts under two-tier swapping (R13 + R20): or_mc_count's walk with the
+ * transition term of or_estimate_row_tiered (cold targets add load[d][m] to
+ * the swap before the tail).  Returns #invalid rows.                        */
+int64_t or_mc_count_tiered(const or_problem *p, const or_tiers *tt, int kind, const void *rows,
+                           int32_t token_bytes, int64_t stride, uint64_t seed, uint64_t first,
+                           int64_t count, const uint32_t *X, int64_t trial_count,
+                           uint32_t *counts /* [count][G] */)
+{
+    int32_t G = p->G, T = p->G + p->Q - 1;
+    int32_t *row = (int32_t *)malloc(sizeof(int32_t) * (size_t)T);
+    int64_t bad = 0;
+    if (p->M > 64) { free(row); return count; }
+    for (int64_t c = 0; c < count; ++c) {
+        get_row(kind, rows, token_bytes, stride, seed, first + (uint64_t)c, c, T, row);
+        uint32_t *cnt = counts + c * G;
+        for (int32_t i = 0; i < G; ++i) cnt[i] = 0;
+        if (!or_is_permutation(row, T)) { ++bad; continue; }
+        for (int64_t t = 0; t < trial_count; ++t) {
+            const uint32_t *x = X + t * G;
+            int32_t q = 0;
+            int32_t d = p->q_device[0], prev = p->q_resident[0], first_slot = 1;
+            double A = p->q_bmean[0];
+            char tier[64];
+            int64_t cum = 0;
+            int exhausted = 0;
+            memset(tier, 0, sizeof tier);
+            for (int32_t s = 0; s < T; ++s) {
+                int32_t tok = row[s];
+                if (tok >= G) {
+                    ++q;
+                    d = p->q_device[q]; prev = p->q_resident[q]; first_slot = 1;
+                    A = p->q_bmean[q];
+                    cum = 0; exhausted = 0;
+                    memset(tier, 0, sizeof tier);
+                    continue;
+                }
+                int32_t i = tok, m = p->model[i];
+                if (m != prev) {
+                    if (tier[m] == 0) {
+                        if (!exhausted && cum + tt->mem[m] <= tt->cap[d]) { tier[m] = 1; cum += tt->mem[m]; }
+                        else { tier[m] = 2; exhausted = 1; }
+                    }
+                    int backlog = p->q_bmean[q] > 0.0;
+                    double trans = p->swap[(d * p->M + prev) * p->M + m];
+                    if (tier[m] == 2) trans = trans + tt->load[d * p->M + m];
+                    if (!first_slot || backlog) trans = tail_of(p, d, prev) + trans;
+                    A = A + trans;
+                }
+                if (A > p->slo[i]) cnt[i] += 1;
+                A = A + (double)x[i] / p->theta[d * p->M + m];
+                prev = m; first_slot = 0;
+            }
+        }
+    }
+    free(row);
+    return bad;
+}

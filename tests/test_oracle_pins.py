@@ -737,3 +737,27 @@ def test_groups_fixed_point_split_and_stats(seed):
         assert g["slo"][k] == r["slo"][mem].min()
         assert g["mu"][k] == pytest.approx(o.mean(), rel=1e-14)
         assert g["var"][k] == pytest.approx(o.var(), rel=1e-12, abs=1e-9)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_mc_tiered_reduces_to_untiered_and_folded_table(seed):
+    # tiered MC counts: cap >= sum(mem) (all warm) equals or_mc_count; cap = 0
+    # (all cold) equals or_mc_count with swap + load folded into the table
+    import dataclasses
+    from workloads.synth import make_random_tiers
+    rng = np.random.default_rng(4400 + seed)
+    G, Q, M, D = int(rng.integers(4, 16)), int(rng.integers(1, 4)), int(rng.integers(2, 5)), int(rng.integers(1, 3))
+    p = make_random_problem(rng, G, Q, M, D, backlog=bool(seed % 2), with_tables=True)
+    tiers = make_random_tiers(rng, M, D)
+    o = O.Oracle(p)
+    X = o.mc_sample(3, 0, 40)
+    allwarm = dict(tiers, cap=np.full(D, int(tiers["mem"].sum()), np.int32))
+    cold = dict(tiers, cap=np.zeros(D, np.int32))
+    base = o.mc_count(O.RANDOM, 0, 30, X, seed=2)
+    assert np.array_equal(o.mc_count_tiered(allwarm, O.RANDOM, 0, 30, X, seed=2), base)
+    sw = p.swap + tiers["load"][:, None, :]
+    for d in range(D):
+        np.fill_diagonal(sw[d], 0.0)
+    of = O.Oracle(dataclasses.replace(p, swap=sw))
+    assert np.array_equal(o.mc_count_tiered(cold, O.RANDOM, 0, 30, X, seed=2),
+                          of.mc_count(O.RANDOM, 0, 30, X, seed=2))
