@@ -266,6 +266,12 @@ QLM_API int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k
                             qlm_group *groups, int32_t group_cap, int32_t *n_groups, int32_t *iters,
                             int32_t device, void *stream);
 
+/* qlm_mc_count under two-tier swapping (R13 + R20): counts[k][g] with the
+ * warm/cold transition costs of qlm_set_tiers.  Same contract as
+ * qlm_mc_count; QLM_EINVAL if no tier tables are set.                      */
+QLM_API int qlm_tiered_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count,
+                                uint32_t *counts, void *stream);
+
 /* Local-search step (R18), asynchronous on `stream`:
  * if *rec (e.g. from qlm_best_ordering_async over NEIGHBOR candidates of
  * base row cand->rows) has index >= 0 and a key strictly below

@@ -92,6 +92,7 @@ SIGNATURES = {
     "qlm_local_search": (C.c_int, [_vp, _vp, _i32, _i32, _i64, _i32, _u64, _vp, _vp]),
     "qlm_abi_version": (C.c_int, []),
     "qlm_set_tiers": (C.c_int, [_vp, C.POINTER(Tiers)]),
+    "qlm_tiered_mc_count": (C.c_int, [_vp, C.POINTER(Candidates), _i64, _vp, _vp]),
     "qlm_form_groups": (C.c_int, [C.POINTER(Requests), _i32, _vp, _i32, _i32, _vp, _vp, _vp, _i32,
                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32), _i32, _vp]),
     "qlm_tiered_score_estimate": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp, _vp, _vp, _vp,

@@ -821,4 +821,29 @@ int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k_per_mod
     return QLM_OK;
 }
 
+int qlm_tiered_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count,
+                        uint32_t *counts, void *stream) {
+    if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
+    if (!ctx->has_tiers) return fail(QLM_EINVAL, "no tier tables: call qlm_set_tiers first");
+    int rc = check_cand(ctx, cand);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    if (trial_count != ctx->mc_trials)
+        return fail(QLM_EINVAL, "trial_count=%lld differs from the last qlm_mc_sample (%lld)",
+                    (long long)trial_count, (long long)ctx->mc_trials);
+    if (cand->count > 65535) return fail(QLM_ERANGE, "MC: cand.count=%lld > 65535", (long long)cand->count);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cand->count == 0) return QLM_OK;
+    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)cand->count * ctx->dm.G * 4, st);
+    if (e != cudaSuccess) return cuda_fail(e, "counts memset");
+    if (trial_count == 0) return QLM_OK;
+    const int M = ctx->dm.M, D = ctx->dm.D;
+    const size_t o_cap = a16((size_t)M * 4), o_load = a16(o_cap + (size_t)D * 4);
+    uint8_t *t = static_cast<uint8_t *>(ctx->d_tier);
+    if ((e = launch_mc_count(ctx->dm, ctx->tb, to_cand(cand), ctx->d_X, trial_count, counts, st,
+                             reinterpret_cast<const int32_t *>(t), reinterpret_cast<const int32_t *>(t + o_cap),
+                             reinterpret_cast<const double *>(t + o_load))) != cudaSuccess)
+        return cuda_fail(e, "MC count kernel");
+    return QLM_OK;
+}
+
 }  // extern "C"

@@ -639,7 +639,8 @@ __global__ void __launch_bounds__(256) mc_sample_kernel(Dims dm, Tables tb, uint
 constexpr int kMcWarps = 8;
 __global__ void __launch_bounds__(32 * kMcWarps) mc_count_kernel(Dims dm, Tables tb, Cand cd,
                                                                  const double *Y, int64_t nt,
-                                                                 uint32_t *counts) {
+                                                                 uint32_t *counts, const int32_t *t_mem,
+                                                                 const int32_t *t_cap, const double *t_load) {
     extern __shared__ __align__(16) uint8_t smem[];
     int64_t first = cd.first;
     if (cd.first_from) {
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(32 * kMcWarps) mc_count_kernel(Dims dm, Tables
     uint16_t *sq = stok + G;                            // [G]
     uint16_t *srow = sq + G;                            // [T]
     uint16_t *sJ = srow + ((T + 7) & ~7);               // [T]
+    uint8_t *scold = reinterpret_cast<uint8_t *>(sJ + ((T + 7) & ~7));   // [G] two-tier: cold target (R20)
     const int64_t loc = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (warp == 0) {
@@ -665,6 +667,30 @@ __global__ void __launch_bounds__(32 * kMcWarps) mc_count_kernel(Dims dm, Tables
             sq[i] = (uint16_t)q;
         });
         __syncwarp();
+        if (t_mem && lane == 0) {                        // R20 tier state: sequential per queue
+            uint32_t seen = 0u, warm = 0u;
+            int cum = 0;
+            bool exh = false;
+            for (int i = 0; i < G; ++i) {
+                const int q = sq[i];
+                const bool firsts = i == 0 || sq[i - 1] != q;
+                if (firsts) { seen = 0u; warm = 0u; cum = 0; exh = false; }
+                const int prev = firsts ? tb.qrec[q].r : tb.grec[stok[i - 1]].model;
+                const int m = tb.grec[stok[i]].model, d = tb.qrec[q].d;
+                bool cold = false;
+                if (m != prev) {
+                    const uint32_t bit = 1u << m;
+                    if (!(seen & bit)) {
+                        seen |= bit;
+                        if (!exh && cum + t_mem[m] <= t_cap[d]) { warm |= bit; cum += t_mem[m]; }
+                        else exh = true;
+                    }
+                    cold = !(warm & bit);
+                }
+                scold[i] = cold ? 1 : 0;
+            }
+        }
+        __syncwarp();
         for (int i = lane; i < G; i += 32) {
             const int tok = stok[i], q = sq[i];
             const QRec qr = tb.qrec[q];
@@ -672,10 +698,12 @@ __global__ void __launch_bounds__(32 * kMcWarps) mc_count_kernel(Dims dm, Tables
             const bool firsts = i == 0 || sq[i - 1] != q;
             const int prev = firsts ? qr.r : tb.grec[stok[i - 1]].model;
             const int d = qr.d, m = g.model;
-            double c = 0.0;                              // transition term (R2/R3)
+            double c = 0.0;                              // transition term (R2/R3; R20 cold load)
             if (m != prev) {
                 const double t = (firsts && !qr.backlog) ? 0.0 : tb.tail[d * M + prev];
-                c = __dadd_rn(t, tb.swap[(d * M + prev) * M + m]);
+                double sw = tb.swap[(d * M + prev) * M + m];
+                if (t_mem && scold[i]) sw = __dadd_rn(sw, t_load[d * M + m]);
+                c = __dadd_rn(t, sw);
             }
             st[i] = c;
             sslo[i] = g.slo;
@@ -1071,14 +1099,15 @@ cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, in
 }
 
 cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const Cand &cd, const double *X,
-                            int64_t nt, uint32_t *counts, cudaStream_t st) {
+                            int64_t nt, uint32_t *counts, cudaStream_t st, const int32_t *t_mem,
+                            const int32_t *t_cap, const double *t_load) {
     const size_t smem = (size_t)32 * dm.G + (size_t)4 * ((dm.Q + 1 + 3) & ~3) +
-                        (size_t)4 * ((dm.T + 7) & ~7);
+                        (size_t)4 * ((dm.T + 7) & ~7) + (size_t)((dm.G + 15) & ~15);
     cudaError_t e = prep(mc_count_kernel, smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((nt + 31) / 32), (unsigned)cd.count);
     const int warps = dm.Q < kMcWarps ? dm.Q : kMcWarps;   // warps split the queues
-    mc_count_kernel<<<grid, 32 * warps, smem, st>>>(dm, tb, cd, X, nt, counts);
+    mc_count_kernel<<<grid, 32 * warps, smem, st>>>(dm, tb, cd, X, nt, counts, t_mem, t_cap, t_load);
     ++g_launches;
     return cudaGetLastError();
 }

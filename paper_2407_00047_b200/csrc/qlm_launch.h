@@ -71,6 +71,8 @@ cudaError_t launch_check_rows(const Cand &cd, int T, unsigned long long *n_bad, 
 cudaError_t launch_mc_sample(const Dims &dm, const Tables &tb, uint64_t seed, int64_t t0,
                              int64_t nt, double *Y, cudaStream_t st);
 cudaError_t launch_mc_count(const Dims &dm, const Tables &tb, const Cand &cd, const double *Y,
-                            int64_t nt, uint32_t *counts, cudaStream_t st);
+                            int64_t nt, uint32_t *counts, cudaStream_t st,
+                            const int32_t *t_mem = nullptr, const int32_t *t_cap = nullptr,
+                            const double *t_load = nullptr);   // tier tables (R20) or none
 
 }  // namespace qlm

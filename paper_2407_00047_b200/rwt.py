@@ -177,6 +177,13 @@ class RwtEstimator:
                                                   self._stream(stream)), "qlm_tiered_score_estimate")
         return out
 
+    def tiered_mc_count(self, cand: Cand, trials: int, counts: torch.Tensor | None = None, stream=None):
+        """qlm_tiered_mc_count: MC counts with the warm/cold swap costs (R13 + R20)."""
+        counts = self._empty((cand.count, self.G), torch.int32) if counts is None else counts
+        L.check(L.lib().qlm_tiered_mc_count(self._h, C.byref(cand.c()), trials, counts.data_ptr(),
+                                            self._stream(stream)), "qlm_tiered_mc_count")
+        return counts
+
     def adopt_best(self, cand: Cand, rec: torch.Tensor, incumbent: torch.Tensor, stream=None):
         """Device-side local-search step: cand.rows <- winner row if rec beats incumbent."""
         L.check(L.lib().qlm_adopt_best(self._h, C.byref(cand.c()), rec.data_ptr(), incumbent.data_ptr(),

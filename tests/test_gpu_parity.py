@@ -1079,3 +1079,35 @@ def test_tiers_very_large_G():
     assert ok
     assert np.array_equal(out["wt"].cpu().numpy().astype(np.float64).T,
                           ref["wt"].astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("cfg", ["C4", "rand"])
+def test_tiered_mc_counts_bit_exact(cfg):
+    # MC counts under two-tier swapping (R13 + R20), bit-exact against the oracle
+    from workloads.synth import make_tiers, make_random_tiers
+    if cfg == "C4":
+        p = make_config("C4")
+        t = make_tiers()
+        t["cap"] = np.array([150], np.int32)
+        rows = np.stack([balanced_row(p.G, p.Q)] + [O.random_row(5, c, p.T) for c in range(3)])
+    else:
+        rng = np.random.default_rng(91)
+        p = make_random_problem(rng, 40, 5, 4, 2, backlog=True, with_tables=True)
+        t = make_random_tiers(rng, 4, 2)
+        rows = np.stack([O.random_row(6, c, p.T) for c in range(6)])
+    e = est_of(p)
+    e.set_tiers(t)
+    tb = 1 if p.T <= 256 else 2
+    cand = e.explicit(rows_tensor(rows, token_bytes=tb))
+    trials = 200
+    e.mc_sample(mc_seed=4, trials=trials)
+    got = e.tiered_mc_count(cand, trials).cpu().numpy().astype(np.uint32)
+    o = O.Oracle(p)
+    X = o.mc_sample(4, 0, trials)
+    ref = o.mc_count_tiered(t, O.EXPLICIT, 0, len(rows), X, rows=rows.astype(np.uint8 if tb == 1 else np.uint16))
+    assert np.array_equal(got, ref)
+    plain = e.mc_count(cand, trials).cpu().numpy().astype(np.uint32)
+    assert np.array_equal(plain, o.mc_count(O.EXPLICIT, 0, len(rows), X,
+                                            rows=rows.astype(np.uint8 if tb == 1 else np.uint16)))
+    if cfg == "C4":
+        assert not np.array_equal(got, plain)           # the cold loads matter here
