@@ -39,6 +39,9 @@ def main():
         e.tiered_score_estimate(cand, out=bufs, rec=torch.empty(2, dtype=torch.int64, device="cuda"))
         e.tiered_score_estimate(e.random(0, 300, seed=2))
         e.tiered_score_estimate(e.from_record(rec, seed=1))
+        if p.len_tables is not None:
+            e.mc_sample(mc_seed=2, trials=64)
+            e.tiered_mc_count(e.from_record(rec, seed=1), 64)
         torch.cuda.synchronize()
         print(cfg, "ok", flush=True)
     # request-group formation (R21)
