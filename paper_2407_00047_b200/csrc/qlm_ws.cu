@@ -368,10 +368,17 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
     }
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + w.off_bar);
     uint64_t *empty = full + 2 * W;
+    // dynamic batches: each producer takes the block's next batch from a
+    // shared counter and leaves its index with the row slot, so pairs on
+    // lightly loaded schedulers take more tiles (static striding made every
+    // pair wait for the slowest one at the end)
+    int64_t *slot_b = reinterpret_cast<int64_t *>(empty + 2 * W);        // [2W]
+    unsigned long long *next_b = reinterpret_cast<unsigned long long *>(slot_b + 2 * W);
     if (tid < 2 * W) {
         mbar_init(&full[tid], 32);
         mbar_init(&empty[tid], 32);
     }
+    if (tid == 0) *next_b = 0ull;
     __syncthreads();
 
     const Cand cd = p.cd;
@@ -399,10 +406,18 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         // no role: only the block-wide argmin below
     } else if (producer) {
         for (int j = 0;; ++j) {
-            const int64_t b = blockIdx.x + (int64_t)(pair + j * W) * grid;
-            if (b >= nbatch) break;
             const int s = 2 * pair + (j & 1);
             mbar_wait(&empty[s], ((j >> 1) & 1) ^ 1);
+            int64_t b = 0;
+            if (lane == 0) {
+                b = blockIdx.x + (int64_t)atomicAdd(next_b, 1ull) * grid;
+                slot_b[s] = b;                             // published by the arrive below
+            }
+            b = __shfl_sync(0xFFFFFFFFu, b, 0);
+            if (b >= nbatch) {                             // end of stream for the paired consumer
+                mbar_arrive(&full[s]);
+                break;
+            }
             const int64_t loc = (b << 5) + lane;
             uint8_t *slot = smem + w.off_rows + (size_t)s * w.tw * 128;
             if (loc < count) produce_row<KIND, TOK>(cd, T, slot, lane, loc, first + loc);
@@ -424,10 +439,10 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         const int full_words = T / EPW;
         const int tw = w.tw;
         for (int j = 0;; ++j) {
-            const int64_t b = blockIdx.x + (int64_t)(pair + j * W) * grid;
-            if (b >= nbatch) break;
             const int s = 2 * pair + (j & 1);
             mbar_wait(&full[s], (j >> 1) & 1);
+            const int64_t b = slot_b[s];
+            if (b >= nbatch) break;
             if (j > 0 && w.use_tma) {
                 if (lane == 0) bulk_wait_read0();              // previous tile read out
                 __syncwarp();
@@ -545,7 +560,7 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage, boo
     const int epw = 4 / tok_bytes;
     w.tw = (dm.T + epw - 1) / epw;
     w.off_rows = (int)off; off = a16(off + (size_t)2 * W * w.tw * 128);
-    w.off_bar = (int)off;  off = a16(off + (size_t)4 * W * 8);
+    w.off_bar = (int)off;  off = a16(off + (size_t)6 * W * 8 + 8);   // full, empty, slot batch, counter
     w.off_pend = (int)off; off = a16(off + (size_t)W * kPend * 32 * sizeof(Pend));
     w.stage_floats = stage ? 3 * (dm.G + 1) * 32 : 0;
     off = a1k(off);
