@@ -66,6 +66,7 @@ struct qlm_ctx {
     void *d_tier = nullptr;            // two-tier swapping (R20): mem [M] | cap [D] | load [D][M]
     bool has_tiers = false;
     std::vector<qlm_group> groups;
+    int slo_hi_only = 0;                   // every groups[i].slo_s has a zero low word
     std::vector<qlm_queue> queues;
     std::vector<double> prof;              // theta|prefill|eps|dec|maxo [D*M] each, swap [D*M*M]
 };
@@ -94,6 +95,17 @@ int validate_groups(const qlm_group *g, int G, int M, int n_tables) {
         if (x.reserved != 0) return fail(QLM_EINVAL, "groups[%d].reserved must be 0", i);
     }
     return QLM_OK;
+}
+
+// The warp-specialised D = 1 kernel keeps only the high word of each slo_s
+// (qlm_ws2.cu); exact when every low word is zero (20 s, 60 s, 3600 s, 0.5 s ...).
+int slo_hi_only(const std::vector<qlm_group> &g) {
+    for (const qlm_group &x : g) {
+        uint64_t u;
+        memcpy(&u, &x.slo_s, 8);
+        if ((uint32_t)u != 0u) return 0;
+    }
+    return 1;
 }
 
 int check_dev(qlm_ctx *ctx) {
@@ -178,7 +190,9 @@ ScanParams base_params(const qlm_ctx *ctx, const qlm_candidates *c) {
     p.counter = ctx->d_counter;
     p.max_blocks = ctx->max_blocks;
     p.zc2 = ctx->zc2;
+    p.zc = (float)ctx->z_clamp;
     p.alpha = ctx->alpha;
+    p.slo_hi_only = ctx->slo_hi_only;
     return p;
 }
 
@@ -341,6 +355,7 @@ int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int3
     ctx->alpha = (float)alpha;
     ctx->has_tables = tabs != nullptr;
     ctx->groups.assign(groups, groups + G);
+    ctx->slo_hi_only = slo_hi_only(ctx->groups);
     ctx->queues.assign(queues, queues + Q);
     const size_t DM = (size_t)D * M;
     ctx->prof.resize(5 * DM + DM * M);
@@ -428,6 +443,7 @@ int qlm_update_groups(qlm_ctx *ctx, const qlm_group *groups, void *stream) {
                                     cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "update_groups copy");
     ctx->groups.assign(groups, groups + ctx->dm.G);
+    ctx->slo_hi_only = slo_hi_only(ctx->groups);
     return rebuild(ctx, st);
 }
 

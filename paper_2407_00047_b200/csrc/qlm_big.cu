@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) big_kernel(const ScanParams p, int ldr) {
     }
     const int64_t count = none ? 0 : cd.count;
     const int64_t ldo = p.ld_out ? p.ld_out : count;
-    const double zc2 = p.zc2;
+    const float zc = p.zc;
     const float alpha = p.alpha;
     const double den = *p.tb.den;
     uint64_t bkey = ~0ull;
@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(256) big_kernel(const ScanParams p, int ldr) {
         for (int q = lane; q < Q; q += 32) {
             const QRec qr = p.tb.qrec[q];
             const int d = qr.d;
-            double A = qr.bmean, B = qr.bvar;
+            double A = qr.bmean;
+            float B = (float)qr.bvar;                     // fp32 (R22)
             int prev = qr.r;
             bool firsts = true;
             uint32_t seen = 0u, warm = 0u;                // two-tier state (R20), per queue
@@ -88,22 +89,23 @@ __global__ void __launch_bounds__(256) big_kernel(const ScanParams p, int ldr) {
                     if (!firsts || qr.backlog) trans = __dadd_rn(__ldg(&p.tb.tail[d * M + prev]), trans);
                     A = __dadd_rn(A, trans);
                 }
-                const double wt = A, V = B;               // exclusive (R5)
+                const double wt = A;                      // exclusive (R5)
+                const float V = B;
                 const double2 ab = p.tb.ab[d * G + g];
                 A = __dadd_rn(A, ab.x);
-                B = __dadd_rn(B, ab.y);
+                B = __fadd_rn(B, (float)ab.y);
                 prev = m;
                 firsts = false;
                 const double slack = __dsub_rn(gr.slo, wt);
+                const float sd = slot_sd(V);
                 bool clamped;
-                const float v = violation(slack, V, zc2, clamped);
+                const float v = slot_v(slack, sd, zc, clamped);
                 S2 = __dsub_rn(S2, slack);
                 num = __dadd_rn(num, (double)gr.n * (double)v);
                 over += v > alpha;
                 const int64_t o = (int64_t)g * ldo + loc;
-                const float Vf = (float)V;
                 if (p.wt) p.wt[o] = (float)wt;
-                if (p.sd) p.sd[o] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
+                if (p.sd) p.sd[o] = sd;
                 if (p.vo) p.vo[o] = v;
             }
         }

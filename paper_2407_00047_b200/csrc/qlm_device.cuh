@@ -284,20 +284,21 @@ struct SlotTables {
 };
 
 struct ScanState {
-    double A, B;           // exclusive mean / variance accumulators of the queue
+    double A;              // exclusive mean accumulator of the queue (fp64)
+    float B;               // exclusive variance accumulator (fp32, R22)
     int q, d, prev;        // prev: transition-table row p'
 };
 
 __device__ __forceinline__ void start_queue(const SlotTables &t, ScanState &s, int q) {
     const QRec r = t.sq[q];
-    s.A = r.bmean; s.B = r.bvar; s.d = r.d;
+    s.A = r.bmean; s.B = (float)r.bvar; s.d = r.d;
     s.prev = r.backlog ? r.r : t.M + r.r;   // R4/R12: a tail only behind a pinned backlog
     s.q = q;
 }
 
 // One group slot: returns its (wt, V) and record.
 __device__ __forceinline__ void group_slot(const SlotTables &t, ScanState &s, int tok,
-                                           double &wt, double &V, GRec &g) {
+                                           double &wt, float &V, GRec &g) {
     {   // one 128-bit load of the 16-B record (two 64-bit loads conflict across replicas)
         const double2 raw = *reinterpret_cast<const double2 *>(t.sg + (tok << t.rs) + t.rl);
         const unsigned long long hi = (unsigned long long)__double_as_longlong(raw.y);
@@ -311,7 +312,7 @@ __device__ __forceinline__ void group_slot(const SlotTables &t, ScanState &s, in
     wt = s.A;
     V = s.B;                                         // exclusive (R5)
     s.A = __dadd_rn(s.A, ab.x);
-    s.B = __dadd_rn(s.B, ab.y);
+    s.B = __fadd_rn(s.B, (float)ab.y);
     s.prev = m;
 }
 
@@ -361,6 +362,23 @@ __device__ __forceinline__ float violation(double slack, double V, double zc2, b
     float v = sf < 0.0f ? 1.0f : 0.0f;
     if (!clamped) v = phibar(sf * rsqrt_approx(fmaxf(Vf, 1e-30f)));
     return v;
+}
+
+// The slot arithmetic every Gaussian scan kernel shares (R8/R9/R22), so their
+// outputs are bit-identical to each other:
+//   V accumulates in fp32 (b rounded once to fp32 when the tables are built);
+//   sd = sqrt.approx(V);  clamped <=> |slack| >= z_clamp * sd (exact for V = 0,
+//   where it reduces to the step [wt > slo]; near |z| = z_clamp it can differ
+//   from the exact test only where Phi-bar < 1e-15);  v = [slack < 0] when
+//   clamped, else Phi-bar(slack / sd).
+__device__ __forceinline__ float slot_sd(float V) { return sqrt_approx(V); }
+__device__ __forceinline__ bool slot_clamped(float sf, float sd, float zc) { return fabsf(sf) >= zc * sd; }
+__device__ __forceinline__ float slot_v_clamped(float sf) { return sf < 0.0f ? 1.0f : 0.0f; }
+__device__ __forceinline__ float slot_v_open(float sf, float sd) { return phibar(sf * rcp_approx(sd)); }
+__device__ __forceinline__ float slot_v(double slack, float sd, float zc, bool &clamped) {
+    const float sf = (float)slack;
+    clamped = slot_clamped(sf, sd, zc);
+    return clamped ? slot_v_clamped(sf) : slot_v_open(sf, sd);
 }
 
 __device__ __forceinline__ uint64_t make_key(float s1, float s2) {

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
         }
     }
     const int G = p.dm.G, Q = p.dm.Q, T = p.dm.T;
-    const double zc2 = p.zc2;
+    const float zc = p.zc;
     const float alpha = p.alpha;
     const int64_t count = cd.count;
     const int64_t ldo = p.ld_out ? p.ld_out : count;     // bulk leading dimension
@@ -200,42 +200,42 @@ __global__ void __launch_bounds__(256) scan_kernel(const ScanParams p) {
         if (tid < nvalid) {
             ScanState s;
             start_queue(tab, s, 0);
-            double S2 = 0.0;
-            float acc1 = 0.0f, acc2 = 0.0f;       // sum n_i v_i: clamped / unclamped slots, row order
+            double S2 = 0.0, acc2 = 0.0;          // sum n_i v_i: clamped (fp32, exact integers) /
+            float acc1 = 0.0f;                    // unclamped (fp64) slots, row order (R11)
             int over = 0;
             for_tokens<KIND, TOK>(cd, T, scratch, blk, loc, first + loc, [&](int tok) {
                 if (tok >= G) {                          // queue separator
                     start_queue(tab, s, s.q + 1 < Q ? s.q + 1 : Q - 1);
                     return;
                 }
-                double wt, V;
+                double wt;
+                float V;
                 GRec g;
                 group_slot(tab, s, tok, wt, V, g);
                 const double slack = __dsub_rn(g.slo, wt);        // -p_i (Eq. 11)
+                const float sd = slot_sd(V);
                 bool clamped;
-                const float v = violation(slack, V, zc2, clamped);
+                const float v = slot_v(slack, sd, zc, clamped);
                 if constexpr (SCORE) {
                     S2 = __dsub_rn(S2, slack);                    // sum_i p_i
                     if (clamped) acc1 = fmaf((float)g.n, v, acc1);
-                    else acc2 = fmaf((float)g.n, v, acc2);
+                    else acc2 = __fma_rn((double)g.n, (double)v, acc2);
                     over += v > alpha;
                 }
                 if constexpr (OUT == OUT_STAGED) {
                     const int o = tok * blk + tid;
-                    const float Vf = (float)V;
                     st0[o] = (float)wt;
-                    st1[o] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
+                    st1[o] = sd;
                     st2[o] = v;
                 } else if constexpr (OUT == OUT_DIRECT) {
                     const int64_t o = (int64_t)tok * ldo + loc;
-                    const float Vf = (float)V;
                     if (gout[0]) gout[0][o] = (float)wt;
-                    if (gout[1]) gout[1][o] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
+                    if (gout[1]) gout[1][o] = sd;
                     if (gout[2]) gout[2][o] = v;
                 }
             });
             if constexpr (SCORE) {
-                const float s1 = (float)(((double)acc1 + (double)acc2) / den);   // R11
+                const float s1 = (float)(((double)acc1 + acc2) / den);   // R11
                 const float s2 = (float)S2;
                 if (p.s1) p.s1[loc] = s1;
                 if (p.s2) p.s2[loc] = s2;

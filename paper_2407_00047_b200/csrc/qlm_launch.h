@@ -19,6 +19,7 @@ struct ScanParams {
     qlm_record *out_rec;       // argmin result (nullable = no argmin)
     int max_blocks;
     double zc2;                // z_clamp^2
+    float zc;                  // z_clamp (fp32: the clamp test of R9/R22)
     float alpha;
     int blk;
     int use_tma;               // staged outputs leave through bulk async copies
@@ -33,6 +34,7 @@ struct ScanParams {
     const int32_t *t_mem;      // two-tier swapping (R20): model sizes [M]
     const int32_t *t_cap;      // CPU memory per device row [D]
     const double *t_load;      // storage -> CPU load time [D][M]
+    int slo_hi_only;           // every slo_s has a zero low 32-bit word (qlm_ws2.cu records)
 };
 
 // Internal candidate kind: rows materialised word-interleaved by fy_rows_kernel
@@ -48,6 +50,7 @@ cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
                          const Tables &tb, cudaStream_t st);
 cudaError_t launch_scan(ScanParams p, cudaStream_t st);
 cudaError_t launch_ws(ScanParams p, cudaStream_t st);      // warp-specialised fast path
+cudaError_t launch_ws2(const ScanParams &p, cudaStream_t st);  // same, D = 1 / byte rows (qlm_ws2.cu)
 cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st); // same, two-tier swapping (R20)
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st);   // ws, else scan
 cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per candidate (large G)

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(128) tier_kernel(const ScanParams p, const Tie
         first = cd.first_from->index;
         none = first < 0;
     }
-    const double zc2 = p.zc2;
+    const float zc = p.zc;
     const float alpha = p.alpha;
     const int64_t count = none ? 0 : cd.count;
     float *const gout[3] = {p.wt, p.sd, p.vo};
@@ -109,18 +109,19 @@ __global__ void __launch_bounds__(128) tier_kernel(const ScanParams p, const Tie
         if (tid < nvalid) {
             // queue state (R4/R12) and tier state (R20)
             int q = 0, d = sq[0].d, prow = sq[0].backlog ? sq[0].r : M + sq[0].r;
-            double A = sq[0].bmean, B = sq[0].bvar, S2 = 0.0;
+            double A = sq[0].bmean, S2 = 0.0, acc2 = 0.0;
+            float B = (float)sq[0].bvar;                      // fp32 (R22)
             uint32_t seen = 0u, warm = 0u;
             int cum = 0;
             bool exh = false;
-            float acc1 = 0.0f, acc2 = 0.0f;
+            float acc1 = 0.0f;
             int over = 0;
             tier_tokens<KIND, TOK>(cd, T, scratch, blk, loc, first + loc, [&](int tok) {
                 if (tok >= G) {                              // separator: next queue, fresh CPU memory
                     q = q + 1 < Q ? q + 1 : Q - 1;
                     const QRec r = sq[q];
                     d = r.d; prow = r.backlog ? r.r : M + r.r;
-                    A = r.bmean; B = r.bvar;
+                    A = r.bmean; B = (float)r.bvar;
                     seen = 0u; warm = 0u; cum = 0; exh = false;
                     return;
                 }
@@ -139,21 +140,22 @@ __global__ void __launch_bounds__(128) tier_kernel(const ScanParams p, const Tie
                 }
                 const int ti = (d * 2 * M + prow) * M + m;
                 A = __dadd_rn(A, cold ? trc[ti] : trw[ti]);
-                const double wt = A, V = B;                  // exclusive (R5)
+                const double wt = A;                         // exclusive (R5)
+                const float V = B;
                 const double2 ab = sab[d * G + tok];
                 A = __dadd_rn(A, ab.x);
-                B = __dadd_rn(B, ab.y);
+                B = __fadd_rn(B, (float)ab.y);
                 prow = m;
                 const double slack = __dsub_rn(g.slo, wt);
+                const float sd = slot_sd(V);
                 bool clamped;
-                const float v = violation(slack, V, zc2, clamped);
+                const float v = slot_v(slack, sd, zc, clamped);
                 S2 = __dsub_rn(S2, slack);
                 if (clamped) acc1 = fmaf((float)g.n, v, acc1);
-                else acc2 = fmaf((float)g.n, v, acc2);
+                else acc2 = __fma_rn((double)g.n, (double)v, acc2);
                 over += v > alpha;
                 if (bulk) {
-                    const float Vf = (float)V;
-                    const float o3[3] = {(float)wt, Vf * rsqrt_approx(fmaxf(Vf, 1e-30f)), v};
+                    const float o3[3] = {(float)wt, sd, v};
                     if (L.stage) {
 #pragma unroll
                         for (int a = 0; a < 3; ++a) st[a][tok * blk + tid] = o3[a];
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(128) tier_kernel(const ScanParams p, const Tie
                     }
                 }
             });
-            const float s1 = (float)(((double)acc1 + (double)acc2) / den);   // R11
+            const float s1 = (float)(((double)acc1 + acc2) / den);   // R11
             const float s2 = (float)S2;
             if (p.s1) p.s1[loc] = s1;
             if (p.s2) p.s2[loc] = s2;
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, cons
         none = first < 0;
     }
     const int64_t count = none ? 0 : cd.count;
-    const double zc2 = p.zc2;
+    const float zc = p.zc;
     const float alpha = p.alpha;
     const double den = *p.tb.den;
     float *const gout[3] = {p.wt, p.sd, p.vo};
@@ -325,7 +327,8 @@ __global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, cons
                 const QRec r = sq[q];
                 const int d = r.d;
                 int prow = r.backlog ? r.r : M + r.r;         // R4 / R12
-                double A = r.bmean, B = r.bvar;
+                double A = r.bmean;
+                float B = (float)r.bvar;                      // fp32 (R22)
                 uint32_t seen = 0u, warm = 0u;
                 int cum = 0;
                 bool exh = false;
@@ -347,22 +350,23 @@ __global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, cons
                     }
                     const int ti = (d * 2 * M + prow) * M + m;
                     A = __dadd_rn(A, cold ? trc[ti] : trw[ti]);
-                    const double wt = A, V = B;
+                    const double wt = A;
+                    const float V = B;
                     const double2 ab = sab[d * G + tok];
                     A = __dadd_rn(A, ab.x);
-                    B = __dadd_rn(B, ab.y);
+                    B = __fadd_rn(B, (float)ab.y);
                     prow = m;
                     const double slack = __dsub_rn(g.slo, wt);
+                    const float sd = slot_sd(V);
                     bool clamped;
-                    const float v = violation(slack, V, zc2, clamped);
+                    const float v = slot_v(slack, sd, zc, clamped);
                     S2 = __dsub_rn(S2, slack);
                     num = __dadd_rn(num, (double)g.n * (double)v);
                     over += v > alpha;
                     if (bulk) {
-                        const float Vf = (float)V;
                         float *o = tile + (size_t)tok * kTwPad + warp;
                         o[0] = (float)wt;
-                        o[(size_t)G * kTwPad] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
+                        o[(size_t)G * kTwPad] = sd;
                         o[(size_t)2 * G * kTwPad] = v;
                     }
                 }

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
     const int64_t count = cd.count;
     const int64_t ldo = p.ld_out ? p.ld_out : count;
     const bool any_out = p.wt || p.sd || p.vo;
-    const float zc2f = (float)p.zc2;
+    const float zc = p.zc;
     const float alpha = p.alpha;
     const double den = SCORE ? *p.tb.den : 1.0;
     const int S = (T + 31) >> 5;                          // chunk length
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
             // ---- pass 1: chunk aggregate from a zero (or reset) state
             ScanState s;
             enter(s);
-            if (!fresh) { s.A = 0.0; s.B = 0.0; }
+            if (!fresh) { s.A = 0.0; s.B = 0.0f; }
             bool reset = fresh;
             for (int pos = p0; pos < p1; ++pos) {
                 const int tok = row[pos];
@@ -176,23 +176,25 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
                     reset = true;
                     continue;
                 }
-                double wt, V;
+                double wt;
+                float V;
                 GRec g;
                 group_slot(tab, s, tok, wt, V, g);
             }
             // ---- segmented inclusive scan of (reset, A, B) over the lanes
             bool f = reset || p0 >= T;
-            double a = p0 >= T ? 0.0 : s.A, b = p0 >= T ? 0.0 : s.B;
+            double a = p0 >= T ? 0.0 : s.A;
+            float b = p0 >= T ? 0.0f : s.B;
             if (p0 >= T) f = false;                            // empty chunk: identity
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int f2 = __shfl_up_sync(0xFFFFFFFFu, (int)f, o);
                 const double a2 = __shfl_up_sync(0xFFFFFFFFu, a, o);
-                const double b2 = __shfl_up_sync(0xFFFFFFFFu, b, o);
-                if (lane >= o && !f) { a = __dadd_rn(a2, a); b = __dadd_rn(b2, b); f = f2 != 0; }
+                const float b2 = __shfl_up_sync(0xFFFFFFFFu, b, o);
+                if (lane >= o && !f) { a = __dadd_rn(a2, a); b = __fadd_rn(b2, b); f = f2 != 0; }
             }
             const double ain = __shfl_up_sync(0xFFFFFFFFu, a, 1);   // exclusive: state at chunk start
-            const double bin = __shfl_up_sync(0xFFFFFFFFu, b, 1);
+            const float bin = __shfl_up_sync(0xFFFFFFFFu, b, 1);
             // ---- pass 2: emit the chunk's slots from the true start state
             enter(s);
             if (!fresh) { s.A = ain; s.B = bin; }
@@ -204,26 +206,26 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
                     start_queue(tab, s, s.q + 1 < Q ? s.q + 1 : Q - 1);
                     continue;
                 }
-                double wt, V;
+                double wt;
+                float V;
                 GRec g;
                 group_slot(tab, s, tok, wt, V, g);
                 const double slack = __dsub_rn(g.slo, wt);
+                const float sd = slot_sd(V);
                 bool clamped;
-                const float v = violation(slack, V, p.zc2, clamped);
+                const float v = slot_v(slack, sd, zc, clamped);
                 if constexpr (SCORE) {
                     S2 = __dsub_rn(S2, slack);
                     num = fma((double)g.n, (double)v, num);
                     over += v > alpha;
                 }
                 if (any_out) {
-                    const float Vf = (float)V;
                     float *o = tile + (size_t)tok * kWidePad + warp;
                     o[0] = (float)wt;
-                    o[(size_t)G * kWidePad] = Vf * rsqrt_approx(fmaxf(Vf, 1e-30f));
+                    o[(size_t)G * kWidePad] = sd;
                     o[(size_t)2 * G * kWidePad] = v;
                 }
             }
-            (void)zc2f;
             if constexpr (SCORE) {
 #pragma unroll
                 for (int o = 16; o; o >>= 1) {

@@ -146,9 +146,10 @@ struct alignas(16) WsQ {      // 32 B (two LDS.128)
 };
 
 struct Acc {
-    double A, B, S2;
+    double A, S2;
+    float B;                 // fp32 variance accumulator (R22)
     float acc1;              // sum n_i v_i over clamped slots (v in {0, 1}: exact)
-    float acc2;              // sum n_i v_i over unclamped slots, row order
+    double acc2;             // sum n_i v_i over unclamped slots, row order
     int prow, dG, dbase, q, over, npend;
     // two-tier swapping (R20): previous model, seen / warm target masks,
     // CPU memory taken, exhausted flag, the queue's CPU memory
@@ -177,7 +178,7 @@ __device__ __forceinline__ void flush_pending(Pend *pq, const WsG *__restrict__ 
             const float v = phibar(e.z);
             st2[e.tg * 32 + lane] = v;
             if constexpr (SCORE) {
-                a.acc2 = fmaf(sgl[e.tg * RSCALE].nf, v, a.acc2);
+                a.acc2 = __fma_rn((double)sgl[e.tg * RSCALE].nf, (double)v, a.acc2);
                 a.over += v > alpha ? 1 : 0;
             }
         }
@@ -189,7 +190,7 @@ template <typename TOK, int RS, bool SCORE, bool PAD, bool TIER>
 __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const double2 *__restrict__ sabl,
                                              const double *__restrict__ str, const WsQ *__restrict__ sq,
                                              uint32_t word, int nvalid_tok, int G, int M, int lane,
-                                             float zc2f, float alpha, float *st, int arr_stride,
+                                             float zc, float alpha, float *st, int arr_stride,
                                              Pend *pq, Acc &a, const int *__restrict__ smemsz,
                                              int cold_off) {
     constexpr int K = 4 / (int)sizeof(TOK);
@@ -262,17 +263,20 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
         tr[k] = str[TIER && cold[k] ? ti + cold_off : ti];   // R20: cold table follows the warm one
     }
     // (iv) the Eq. 10 chain (operation order identical to the sequential definition)
-    double wt[K], V[K];
-    double A = a.A, B = a.B;
+    double wt[K];
+    float V[K];
+    double A = a.A;
+    float B = a.B;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const double A1 = __dadd_rn(A, tr[k]);
         wt[k] = A1;
         V[k] = B;
-        const double A2 = __dadd_rn(A1, ab[k].x), B2 = __dadd_rn(B, ab[k].y);
+        const double A2 = __dadd_rn(A1, ab[k].x);
+        const float B2 = __fadd_rn(B, (float)ab[k].y);
         if (PAD && k >= nvalid_tok) continue;
         A = isbar[k] ? r[k].bmean : A2;
-        B = isbar[k] ? r[k].bvar : B2;
+        B = isbar[k] ? (float)r[k].bvar : B2;
     }
     a.A = A; a.B = B; a.prow = prow; a.dG = dG; a.dbase = dbase; a.q = q;
     // (v) violation probabilities, scores, staging
@@ -280,16 +284,14 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
     for (int k = 0; k < K; ++k) {
         const double slack = __dsub_rn(g[k].slo, wt[k]);
         const float sf = (float)slack;
-        const float Vf = (float)V[k];
-        const float rr = rsqrt_approx(fmaxf(Vf, 1e-30f));
-        // |z| >= z_clamp  <=>  slack^2 >= z_clamp^2 V   (R9; exact for V = 0)
-        const bool clamped = sf * sf >= zc2f * Vf;
-        const float v = sf < 0.0f ? 1.0f : 0.0f;              // clamped value (R9)
+        const float sd = slot_sd(V[k]);
+        const bool clamped = slot_clamped(sf, sd, zc);        // R9 / R22
+        const float v = slot_v_clamped(sf);
         const bool grp = !isbar[k] && tg[k] < G;
         const bool defer = grp && !clamped;
         if (defer) {                                           // exact value later, FIFO
             Pend e;
-            e.z = sf * rr;
+            e.z = sf * rcp_approx(sd);                       // phibar(e.z) = slot_v_open(sf, sd)
             e.tg = tg[k];
             pq[a.npend * 32 + lane] = e;
             ++a.npend;
@@ -304,7 +306,7 @@ __device__ __forceinline__ void consume_word(const WsG *__restrict__ sgl, const 
         {
             float *o = st + tg[k] * 32 + lane;               // separators -> trash row G
             o[0] = (float)wt[k];
-            o[arr_stride] = Vf * rr;
+            o[arr_stride] = sd;
             o[2 * arr_stride] = v;                           // deferred slots overwritten at flush
         }
     }
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
         const WsG *sgl = sg + (lane & ((1 << RS) - 1));
         const double2 *sabl = sab + (lane & ((1 << RS) - 1));
         const double *strl = str + (lane & ((1 << kTrRs) - 1));
-        const float zc2f = (float)p.zc2;
+        const float zc = p.zc;
         const float alpha = p.alpha;
         const double den = *p.tb.den;
         const int arr = (G + 1) * 32;
@@ -452,14 +454,14 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
             if (loc < count) {
                 Acc a;
                 const WsQ r0 = sq[0];
-                a.A = r0.bmean; a.B = r0.bvar; a.prow = r0.prow0; a.dG = r0.dG; a.dbase = r0.dbase;
-                a.q = 0; a.S2 = 0.0; a.acc1 = 0.0f; a.acc2 = 0.0f; a.over = 0; a.npend = 0;
+                a.A = r0.bmean; a.B = (float)r0.bvar; a.prow = r0.prow0; a.dG = r0.dG; a.dbase = r0.dbase;
+                a.q = 0; a.S2 = 0.0; a.acc1 = 0.0f; a.acc2 = 0.0; a.over = 0; a.npend = 0;
                 a.pmod = r0.tier & 63; a.capd = r0.tier >> 6; a.cum = 0; a.exh = 0; a.seen = 0u; a.warm = 0u;
                 uint32_t cur = w32[lane];
                 for (int wi = 0; wi < full_words; ++wi) {
                     const uint32_t nxt = w32[(wi + 1 < tw ? wi + 1 : wi) * 32 + lane];   // prefetch
                     consume_word<TOK, RS, SCORE, false, TIER>(sgl, sabl, strl, sq, cur, EPW, G,
-                                                              M, lane, zc2f, alpha, st, arr, pq, a,
+                                                              M, lane, zc, alpha, st, arr, pq, a,
                                                               smemsz, ntr);
                     cur = nxt;
                     if (__any_sync(__activemask(), a.npend > kPend - EPW))
@@ -467,11 +469,11 @@ __global__ void __launch_bounds__(512, 1) ws_kernel(const __grid_constant__ WsPa
                 }
                 if (full_words * EPW < T)
                     consume_word<TOK, RS, SCORE, true, TIER>(sgl, sabl, strl, sq, cur,
-                                                             T - full_words * EPW, G, M, lane, zc2f,
+                                                             T - full_words * EPW, G, M, lane, zc,
                                                              alpha, st, arr, pq, a, smemsz, ntr);
                 flush_pending<SCORE, (1 << RS)>(pq, sgl_rs, lane, alpha, st2, a);
                 if constexpr (SCORE) {
-                    const float s1 = (float)(((double)a.acc1 + (double)a.acc2) / den);     // R11
+                    const float s1 = (float)(((double)a.acc1 + a.acc2) / den);     // R11
                     const float s2 = (float)a.S2;
                     if (p.s1) p.s1[loc] = s1;
                     if (p.s2) p.s2[loc] = s2;
@@ -675,6 +677,11 @@ cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st) {
 // Fast path for large candidate sets; cudaErrorNotSupported -> caller falls back.
 cudaError_t launch_ws(ScanParams p, cudaStream_t st) {
     if (p.cd.first_from || p.cd.count < 4096 || env_int_ws("QLM_NO_WS", 0)) return cudaErrorNotSupported;
+    if (!env_int_ws("QLM_NO_WS2", 0)) {
+        const cudaError_t e = launch_ws2(p, st);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
     switch (p.cd.kind) {
     case QLM_CAND_RANDOM:
         return p.dm.T <= 256 ? launch_ws_k<QLM_CAND_RANDOM, uint8_t>(p, st)
