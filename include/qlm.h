@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define QLM_ABI_VERSION 3
+#define QLM_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define QLM_API __attribute__((visibility("default")))
@@ -45,6 +45,7 @@ typedef enum {
     QLM_EINVAL = 1,     /* invalid argument; qlm_last_error names it           */
     QLM_ENOMEM = 2,     /* device allocation failed                             */
     QLM_ECUDA = 3,      /* CUDA runtime error / unsupported device              */
+    QLM_ENCCL = 4,      /* NCCL missing or a communicator call failed           */
     QLM_EBADORDER = 5,  /* a row is not a permutation of 0..T-1 (Eq. 6)         */
     QLM_ERANGE = 6      /* T > 32768, ENUM index >= T!, index overflow          */
 } qlm_status;
@@ -344,6 +345,50 @@ QLM_API int qlm_rows(qlm_ctx *ctx, const qlm_candidates *cand, uint16_t *rows_ou
 /* Validate EXPLICIT rows (Eq. 6 bijection); synchronous.  *n_bad = number
  * of rows that are not permutations of 0..T-1.                              */
 QLM_API int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, void *stream);
+
+/* ---- multi-GPU: one NCCL communicator per context ----------
+ * The scheduler makes ONE global choice of plan (objective
+ * P:L761-767) while candidates (and MC trials) are sharded over the GPUs of a
+ * box, one process and one context per GPU, each rank passing its own
+ * candidate range (and trial range).  Once a communicator is attached, every
+ * call that produces an argmin record returns the GLOBAL record -- the
+ * lexicographic (S1, S2, index) min over all ranks (R11/R14), the same on
+ * every rank -- and every MC count is the sum over ranks:
+ *   qlm_best_ordering_async, qlm_score_estimate (rec), qlm_tiered_score_estimate
+ *   (rec): one 16-B NCCL all-gather + qlm_reduce_records on `stream`, no host
+ *   synchronisation;
+ *   qlm_best_ordering: the global record, scored and decoded by the rank
+ *   whose range holds it and shared with one NCCL max all-reduce (so EXPLICIT
+ *   rows never leave their rank);
+ *   qlm_mc_count, qlm_mc_estimate, qlm_tiered_mc_count: counts summed with one
+ *   NCCL all-reduce on `stream`;
+ *   qlm_local_search: iteration it's candidates [it*per_iter, (it+1)*per_iter)
+ *   are split into contiguous rank shards; the global winner is adopted on
+ *   every rank, so the incumbent stays identical everywhere.
+ * These calls are then collective: every rank must make the same sequence of
+ * them.  NCCL is loaded at run time (the copy torch already loaded, else
+ * libnccl.so.2 or $QLM_NCCL_PATH); without it the comm calls return
+ * QLM_ENCCL and everything else works as before.                            */
+#define QLM_COMM_ID_BYTES 128
+
+/* A fresh NCCL unique id (rank 0 calls it and broadcasts the 128 bytes to
+ * the other ranks, e.g. with torch.distributed).  Host memory, caller-owned. */
+QLM_API int qlm_comm_unique_id(uint8_t id[QLM_COMM_ID_BYTES]);
+
+/* Collective over `world` ranks: create this context's communicator (rank
+ * `rank`, on the context's device) from the broadcast id and attach it.
+ * Each rank's context must be on a different GPU.  Errors: QLM_EINVAL (rank
+ * not in [0, world), world < 1, already attached), QLM_ENCCL, QLM_ENOMEM.  */
+QLM_API int qlm_comm_attach(qlm_ctx *ctx, const uint8_t id[QLM_COMM_ID_BYTES], int32_t rank,
+                            int32_t world);
+
+/* Destroy and detach the communicator (qlm_destroy also does it).  Calls
+ * return to per-device results.  Synchronises the context's device.          */
+QLM_API int qlm_comm_detach(qlm_ctx *ctx);
+
+/* *rank, *world of the attached communicator (0, 1 when none is attached);
+ * *nccl_version = NCCL's version code (0 when NCCL is not loaded).          */
+QLM_API int qlm_comm_info(const qlm_ctx *ctx, int32_t *rank, int32_t *world, int32_t *nccl_version);
 
 /* ---- introspection --------------------------------------------------------- */
 QLM_API int qlm_dims(const qlm_ctx *ctx, int32_t *G, int32_t *Q, int32_t *T, int32_t *D, int32_t *M);

@@ -13,7 +13,8 @@ import numpy as np
 LIB_PATH = os.environ.get("QLM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                           "libqlm.so")
 
-QLM_OK, QLM_EINVAL, QLM_ENOMEM, QLM_ECUDA, QLM_EBADORDER, QLM_ERANGE = 0, 1, 2, 3, 5, 6
+QLM_OK, QLM_EINVAL, QLM_ENOMEM, QLM_ECUDA, QLM_ENCCL, QLM_EBADORDER, QLM_ERANGE = 0, 1, 2, 3, 4, 5, 6
+COMM_ID_BYTES = 128
 CAND_EXPLICIT, CAND_RANDOM, CAND_ENUM, CAND_NEIGHBOR = 0, 1, 2, 3
 MAX_MOVES = 8
 
@@ -97,6 +98,10 @@ SIGNATURES = {
                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32), _i32, _vp]),
     "qlm_tiered_score_estimate": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp, _vp, _vp, _vp,
                                             _vp, _vp]),
+    "qlm_comm_unique_id": (C.c_int, [_vp]),
+    "qlm_comm_attach": (C.c_int, [_vp, _vp, _i32, _i32]),
+    "qlm_comm_detach": (C.c_int, [_vp]),
+    "qlm_comm_info": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
 }
 
 _lib = None

@@ -8,12 +8,12 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libqlm.so")
-SOURCES = [os.path.join(PKG, "csrc", n) for n in ("qlm_api.cu", "qlm_kernels.cu", "qlm_ws.cu", "qlm_ws2.cu", "qlm_wide.cu", "qlm_req.cu", "qlm_tier.cu", "qlm_group.cu", "qlm_big.cu")]
+SOURCES = [os.path.join(PKG, "csrc", n) for n in ("qlm_api.cu", "qlm_kernels.cu", "qlm_ws.cu", "qlm_ws2.cu", "qlm_wide.cu", "qlm_req.cu", "qlm_tier.cu", "qlm_group.cu", "qlm_big.cu", "qlm_comm.cu")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-    "-shared",
+    "-shared", "-ldl",
 ]
 
 

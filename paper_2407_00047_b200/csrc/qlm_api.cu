@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "qlm_comm.h"
 #include "qlm_launch.h"
 
 using namespace qlm;
@@ -65,6 +66,10 @@ struct qlm_ctx {
     size_t X_cap = 0;
     void *d_tier = nullptr;            // two-tier swapping (R20): mem [M] | cap [D] | load [D][M]
     bool has_tiers = false;
+    // multi-GPU (qlm_comm_attach): the communicator and its scratch
+    Comm *comm = nullptr;
+    qlm_record *d_comm_recs = nullptr;     // [world] gathered records
+    int32_t *d_comm_buf = nullptr;         // [2G + 5] winner decode / scores (max all-reduce)
     std::vector<qlm_group> groups;
     int slo_hi_only = 0;                   // every groups[i].slo_s has a zero low word
     std::vector<qlm_queue> queues;
@@ -111,6 +116,32 @@ int slo_hi_only(const std::vector<qlm_group> &g) {
 int check_dev(qlm_ctx *ctx) {
     cudaError_t e = cudaSetDevice(ctx->device);
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "cudaSetDevice");
+}
+
+// a8 when a communicator is attached: the global min-loc of every rank's
+// record -- one 16-B all-gather and the (key, index) reduction, both on `st`.
+int global_record(qlm_ctx *ctx, qlm_record *rec, cudaStream_t st) {
+    if (!ctx->comm) return QLM_OK;
+    std::string err;
+    if (!comm_allgather_bytes(ctx->comm, rec, ctx->d_comm_recs, sizeof(qlm_record), st, err))
+        return fail(QLM_ENCCL, "%s", err.c_str());
+    cudaError_t e = launch_reduce_records(ctx->d_comm_recs, comm_world(ctx->comm), rec, st);
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "reduce_records (global)");
+}
+
+// a12 when a communicator is attached: counts summed over the ranks on `st`.
+int global_counts(qlm_ctx *ctx, uint32_t *counts, size_t n, cudaStream_t st) {
+    if (!ctx->comm || n == 0) return QLM_OK;
+    std::string err;
+    if (!comm_allreduce_sum_u32(ctx->comm, counts, n, st, err)) return fail(QLM_ENCCL, "%s", err.c_str());
+    return QLM_OK;
+}
+
+// Rank r's contiguous shard [first, first + count) of n items.
+void shard(int64_t n, int r, int w, int64_t &first, int64_t &count) {
+    const int64_t base = n / w, extra = n % w;
+    first = r * base + (r < extra ? r : extra);
+    count = base + (r < extra ? 1 : 0);
 }
 
 int check_cand(const qlm_ctx *ctx, const qlm_candidates *c) {
@@ -426,6 +457,7 @@ int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int3
 void qlm_destroy(qlm_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    if (ctx->comm) qlm_comm_detach(ctx);
     void *ptrs[] = {ctx->d_raw, ctx->d_tab, ctx->d_block_recs, ctx->d_counter, ctx->d_rec,
                     ctx->d_dec_out, ctx->d_bad, ctx->d_X, ctx->d_ilv, ctx->d_chunk_recs,
                     ctx->d_ls_rec, ctx->d_tier};
@@ -467,17 +499,17 @@ int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (cand->count == 0) {
-        const qlm_record none = {~0ull, -1};
-        cudaError_t e = cudaMemcpyAsync(rec, &none, sizeof none, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        return e == cudaSuccess ? QLM_OK : cuda_fail(e, "empty record");
+    if (cand->count == 0) {                                  // the "none" record
+        cudaError_t e = cudaMemsetAsync(rec, 0xFF, sizeof(qlm_record), st);
+        if (e != cudaSuccess) return cuda_fail(e, "empty record");
+        return global_record(ctx, rec, st);
     }
     ScanParams p = base_params(ctx, cand);
     p.out_rec = rec;
     attach_ilv(ctx, p);
     cudaError_t e = launch_any_scan(p, st);
-    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "score/argmin kernel");
+    if (e != cudaSuccess) return cuda_fail(e, "score/argmin kernel");
+    return global_record(ctx, rec, st);
 }
 
 int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, qlm_record *out,
@@ -519,38 +551,66 @@ int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     memset(out, 0, sizeof *out);
     out->index = -1;
-    if (cand->count == 0) return QLM_OK;
-    if ((rc = qlm_best_ordering_async(ctx, cand, ctx->d_rec, stream))) return rc;
+    if (cand->count == 0 && !ctx->comm) return QLM_OK;
+    if ((rc = qlm_best_ordering_async(ctx, cand, ctx->d_rec, stream))) return rc;   // global when attached
     qlm_record h;
     cudaError_t e = cudaMemcpyAsync(&h, ctx->d_rec, sizeof h, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "best_ordering");
     out->index = h.index;
     if (h.index < 0) return QLM_OK;
-    // re-score and decode the winner on the device
-    qlm_candidates one = *cand;
-    one.first = h.index;
-    one.count = 1;
-    one.first_from = nullptr;
-    if (cand->kind == QLM_CAND_EXPLICIT)
-        one.rows = static_cast<const uint8_t *>(cand->rows) + (h.index - cand->first) * cand->stride;
-    float *d_s = reinterpret_cast<float *>(ctx->d_rec + 1);
-    int32_t *d_no = reinterpret_cast<int32_t *>(ctx->d_rec + 2);
-    if ((rc = qlm_score_orderings(ctx, &one, d_s, d_s + 1, d_no, stream))) return rc;
-    if ((rc = qlm_decode(ctx, &one, ctx->d_dec_out, ctx->d_dec_out + ctx->dm.G, stream))) return rc;
-    float s[2];
-    int32_t no = 0;
-    if ((e = cudaMemcpyAsync(s, d_s, sizeof s, cudaMemcpyDeviceToHost, st)) ||
-        (e = cudaMemcpyAsync(&no, d_no, sizeof no, cudaMemcpyDeviceToHost, st)) ||
-        (queue_of_group && (e = cudaMemcpyAsync(queue_of_group, ctx->d_dec_out,
-                                                ctx->dm.G * sizeof(int32_t), cudaMemcpyDeviceToHost, st))) ||
-        (pos_of_group && (e = cudaMemcpyAsync(pos_of_group, ctx->d_dec_out + ctx->dm.G,
-                                              ctx->dm.G * sizeof(int32_t), cudaMemcpyDeviceToHost, st))) ||
+    // re-score and decode the winner on the device -- on the rank whose range
+    // holds it (EXPLICIT rows live there), shared by a max all-reduce
+    const int G = ctx->dm.G;
+    const bool owner = h.index >= cand->first && h.index < cand->first + cand->count;
+    int32_t sc[5] = {-1, -1, -1, -1, -1};                   // s1 hi/lo, s2 hi/lo (16-bit halves), n_over
+    if (owner) {
+        qlm_candidates one = *cand;
+        one.first = h.index;
+        one.count = 1;
+        one.first_from = nullptr;
+        if (cand->kind == QLM_CAND_EXPLICIT)
+            one.rows = static_cast<const uint8_t *>(cand->rows) + (h.index - cand->first) * cand->stride;
+        float *d_s = reinterpret_cast<float *>(ctx->d_rec + 1);
+        int32_t *d_no = reinterpret_cast<int32_t *>(ctx->d_rec + 2);
+        if ((rc = qlm_score_orderings(ctx, &one, d_s, d_s + 1, d_no, stream))) return rc;
+        if ((rc = qlm_decode(ctx, &one, ctx->d_dec_out, ctx->d_dec_out + G, stream))) return rc;
+        float sv[2];
+        int32_t no = 0;
+        if ((e = cudaMemcpyAsync(sv, d_s, sizeof sv, cudaMemcpyDeviceToHost, st)) ||
+            (e = cudaMemcpyAsync(&no, d_no, sizeof no, cudaMemcpyDeviceToHost, st)) ||
+            (e = cudaStreamSynchronize(st)))
+            return cuda_fail(e, "best_ordering scores");
+        uint32_t b1, b2;
+        memcpy(&b1, &sv[0], 4);
+        memcpy(&b2, &sv[1], 4);
+        sc[0] = (int32_t)(b1 >> 16); sc[1] = (int32_t)(b1 & 0xFFFFu);
+        sc[2] = (int32_t)(b2 >> 16); sc[3] = (int32_t)(b2 & 0xFFFFu);
+        sc[4] = no;
+    }
+    const int32_t *dec = ctx->d_dec_out;
+    if (ctx->comm) {
+        int32_t *buf = ctx->d_comm_buf;                     // non-owners contribute -1 everywhere
+        std::string err;
+        if ((e = owner ? cudaMemcpyAsync(buf, ctx->d_dec_out, 2 * (size_t)G * 4, cudaMemcpyDeviceToDevice, st)
+                       : cudaMemsetAsync(buf, 0xFF, 2 * (size_t)G * 4, st)) ||
+            (e = cudaMemcpyAsync(buf + 2 * G, sc, sizeof sc, cudaMemcpyHostToDevice, st)))
+            return cuda_fail(e, "best_ordering share");
+        if (!comm_allreduce_max_i32(ctx->comm, buf, 2 * (size_t)G + 5, st, err))
+            return fail(QLM_ENCCL, "%s", err.c_str());
+        if ((e = cudaMemcpyAsync(sc, buf + 2 * G, sizeof sc, cudaMemcpyDeviceToHost, st))) return cuda_fail(e, "share");
+        dec = buf;
+    }
+    if ((queue_of_group && (e = cudaMemcpyAsync(queue_of_group, dec, G * sizeof(int32_t),
+                                                cudaMemcpyDeviceToHost, st))) ||
+        (pos_of_group && (e = cudaMemcpyAsync(pos_of_group, dec + G, G * sizeof(int32_t),
+                                              cudaMemcpyDeviceToHost, st))) ||
         (e = cudaStreamSynchronize(st)))
         return cuda_fail(e, "best_ordering readback");
-    out->s1 = s[0];
-    out->s2 = s[1];
-    out->n_over = no;
+    const uint32_t b1 = ((uint32_t)sc[0] << 16) | (uint32_t)sc[1], b2 = ((uint32_t)sc[2] << 16) | (uint32_t)sc[3];
+    memcpy(&out->s1, &b1, 4);
+    memcpy(&out->s2, &b2, 4);
+    out->n_over = sc[4];
     return QLM_OK;
 }
 
@@ -569,10 +629,9 @@ int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cand->count == 0) {
         if (!rec) return QLM_OK;
-        const qlm_record none = {~0ull, -1};
-        cudaError_t e = cudaMemcpyAsync(rec, &none, sizeof none, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        return e == cudaSuccess ? QLM_OK : cuda_fail(e, "empty record");
+        cudaError_t e = cudaMemsetAsync(rec, 0xFF, sizeof(qlm_record), st);   // the "none" record
+        if (e != cudaSuccess) return cuda_fail(e, "empty record");
+        return global_record(ctx, rec, st);
     }
     if (!wt_mean && !wt_std && !viol && !s1 && !s2 && !n_over && !rec) return QLM_OK;
     ScanParams p = base_params(ctx, cand);
@@ -580,7 +639,8 @@ int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
     p.s1 = s1; p.s2 = s2; p.n_over = n_over; p.out_rec = rec;
     attach_ilv(ctx, p);
     cudaError_t e = launch_any_scan(p, st);
-    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "scan kernel");
+    if (e != cudaSuccess) return cuda_fail(e, "scan kernel");
+    return rec ? global_record(ctx, rec, st) : QLM_OK;
 }
 
 int qlm_mc_sample(qlm_ctx *ctx, uint64_t mc_seed, int64_t trial_first, int64_t trial_count,
@@ -625,11 +685,11 @@ int qlm_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count, 
     if (cand->count == 0) return QLM_OK;
     cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)cand->count * ctx->dm.G * 4, st);
     if (e != cudaSuccess) return cuda_fail(e, "counts memset");
-    if (trial_count == 0) return QLM_OK;
+    if (trial_count == 0) return global_counts(ctx, counts, (size_t)cand->count * ctx->dm.G, st);
     if ((e = launch_mc_count(ctx->dm, ctx->tb, to_cand(cand), ctx->d_X, trial_count, counts, st)) !=
         cudaSuccess)
         return cuda_fail(e, "MC count kernel");
-    return QLM_OK;
+    return global_counts(ctx, counts, (size_t)cand->count * ctx->dm.G, st);
 }
 
 int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
@@ -700,12 +760,22 @@ int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves
     nb.seed = seed;
     nb.moves = moves;
     nb.count = per_iter;
+    // with a communicator, rank r scores its contiguous shard of every
+    // iteration and the global winner is adopted everywhere
+    int64_t sh_first = 0, sh_count = per_iter;
+    if (ctx->comm) shard(per_iter, comm_rank(ctx->comm), comm_world(ctx->comm), sh_first, sh_count);
     for (int32_t it = 0; it < iters; ++it) {
-        nb.first = (int64_t)it * per_iter;
+        nb.first = (int64_t)it * per_iter + sh_first;
+        nb.count = sh_count;
         if ((rc = check_cand(ctx, &nb))) return rc;
-        ScanParams p = base_params(ctx, &nb);
-        p.out_rec = ctx->d_ls_rec;
-        if ((e = launch_any_scan(p, st)) != cudaSuccess) return cuda_fail(e, "local search: scores");
+        if (sh_count > 0) {
+            ScanParams p = base_params(ctx, &nb);
+            p.out_rec = ctx->d_ls_rec;
+            if ((e = launch_any_scan(p, st)) != cudaSuccess) return cuda_fail(e, "local search: scores");
+        } else if ((e = cudaMemsetAsync(ctx->d_ls_rec, 0xFF, sizeof(qlm_record), st)) != cudaSuccess) {
+            return cuda_fail(e, "local search: empty shard");
+        }
+        if ((rc = global_record(ctx, ctx->d_ls_rec, st))) return rc;
         if ((e = launch_adopt(ctx->dm, to_cand(&nb), ctx->d_ls_rec, incumbent, st)) != cudaSuccess)
             return cuda_fail(e, "local search: adopt");
     }
@@ -783,10 +853,9 @@ int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *w
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cand->count == 0) {
         if (!rec) return QLM_OK;
-        const qlm_record none = {~0ull, -1};
-        cudaError_t e = cudaMemcpyAsync(rec, &none, sizeof none, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        return e == cudaSuccess ? QLM_OK : cuda_fail(e, "empty record");
+        cudaError_t e = cudaMemsetAsync(rec, 0xFF, sizeof(qlm_record), st);   // the "none" record
+        if (e != cudaSuccess) return cuda_fail(e, "empty record");
+        return global_record(ctx, rec, st);
     }
     if (!wt_mean && !wt_std && !viol && !s1 && !s2 && !n_over && !rec) return QLM_OK;
     ScanParams p = base_params(ctx, cand);
@@ -799,7 +868,8 @@ int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *w
     p.t_cap = reinterpret_cast<const int32_t *>(t + o_cap);
     p.t_load = reinterpret_cast<const double *>(t + o_load);
     cudaError_t e = launch_tier(p, st);
-    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "tier kernel");
+    if (e != cudaSuccess) return cuda_fail(e, "tier kernel");
+    return rec ? global_record(ctx, rec, st) : QLM_OK;
 }
 
 int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k_per_model, int32_t limit,
@@ -851,7 +921,7 @@ int qlm_tiered_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_
     if (cand->count == 0) return QLM_OK;
     cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)cand->count * ctx->dm.G * 4, st);
     if (e != cudaSuccess) return cuda_fail(e, "counts memset");
-    if (trial_count == 0) return QLM_OK;
+    if (trial_count == 0) return global_counts(ctx, counts, (size_t)cand->count * ctx->dm.G, st);
     const int M = ctx->dm.M, D = ctx->dm.D;
     const size_t o_cap = a16((size_t)M * 4), o_load = a16(o_cap + (size_t)D * 4);
     uint8_t *t = static_cast<uint8_t *>(ctx->d_tier);
@@ -859,6 +929,61 @@ int qlm_tiered_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_
                              reinterpret_cast<const int32_t *>(t), reinterpret_cast<const int32_t *>(t + o_cap),
                              reinterpret_cast<const double *>(t + o_load))) != cudaSuccess)
         return cuda_fail(e, "MC count kernel");
+    return global_counts(ctx, counts, (size_t)cand->count * ctx->dm.G, st);
+}
+
+int qlm_comm_unique_id(uint8_t id[QLM_COMM_ID_BYTES]) {
+    if (!id) return fail(QLM_EINVAL, "id is NULL");
+    std::string err;
+    if (!comm_unique_id(id, err)) return fail(QLM_ENCCL, "%s", err.c_str());
+    return QLM_OK;
+}
+
+int qlm_comm_attach(qlm_ctx *ctx, const uint8_t id[QLM_COMM_ID_BYTES], int32_t rank, int32_t world) {
+    if (!ctx || !id) return fail(QLM_EINVAL, "ctx or id is NULL");
+    if (world < 1 || rank < 0 || rank >= world)
+        return fail(QLM_EINVAL, "rank=%d, world=%d: need 0 <= rank < world", rank, world);
+    if (ctx->comm) return fail(QLM_EINVAL, "a communicator is already attached");
+    int rc = check_dev(ctx);
+    if (rc) return rc;
+    if (cudaMalloc(&ctx->d_comm_recs, (size_t)world * sizeof(qlm_record)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_comm_buf, (2 * (size_t)ctx->dm.G + 5) * sizeof(int32_t)) != cudaSuccess) {
+        cudaFree(ctx->d_comm_recs);
+        ctx->d_comm_recs = nullptr;
+        return fail(QLM_ENOMEM, "communicator scratch");
+    }
+    std::string err;
+    ctx->comm = comm_init(id, rank, world, err);
+    if (!ctx->comm) {
+        cudaFree(ctx->d_comm_recs);
+        cudaFree(ctx->d_comm_buf);
+        ctx->d_comm_recs = nullptr;
+        ctx->d_comm_buf = nullptr;
+        return fail(QLM_ENCCL, "%s", err.c_str());
+    }
+    return QLM_OK;
+}
+
+int qlm_comm_detach(qlm_ctx *ctx) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    if (!ctx->comm) return QLM_OK;
+    int rc = check_dev(ctx);
+    if (rc) return rc;
+    cudaDeviceSynchronize();
+    comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+    cudaFree(ctx->d_comm_recs);
+    cudaFree(ctx->d_comm_buf);
+    ctx->d_comm_recs = nullptr;
+    ctx->d_comm_buf = nullptr;
+    return QLM_OK;
+}
+
+int qlm_comm_info(const qlm_ctx *ctx, int32_t *rank, int32_t *world, int32_t *nccl_version) {
+    if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
+    if (rank) *rank = ctx->comm ? comm_rank(ctx->comm) : 0;
+    if (world) *world = ctx->comm ? comm_world(ctx->comm) : 1;
+    if (nccl_version) *nccl_version = comm_nccl_version();
     return QLM_OK;
 }
 

@@ -13,6 +13,25 @@ import torch
 import torch.distributed as dist
 
 
+def attach_comm(est, group=None, unique_id=None):
+    """Attach the library's own NCCL communicator to `est` (include/qlm.h
+    qlm_comm_*): rank 0 creates the 128-byte unique id, torch.distributed
+    broadcasts it (the only thing it carries), and every rank attaches.  From
+    then on the library's argmin records are global and its MC counts are
+    summed over ranks inside the C ABI; global_best / sum_counts pass through.
+    """
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    make = unique_id if unique_id is not None else type(est).comm_unique_id
+    on_gpu = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+    buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(make()), dtype=torch.uint8))
+    dist.broadcast(buf, src=0, group=group)
+    est.comm_attach(bytes(buf.cpu().numpy().tobytes()), rank, world)
+    return est
+
+
 def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous [first, first+count) of `total` candidates for `rank`."""
     base, extra = divmod(total, world)
@@ -37,17 +56,23 @@ def gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
     return torch.cat(parts)
 
 
-def global_best(rec: torch.Tensor, reduce, group=None) -> torch.Tensor:
+def global_best(rec: torch.Tensor, reduce, group=None, est=None) -> torch.Tensor:
     """Global min-loc: gather all ranks' records, then `reduce(records)`.
 
-    `reduce` is RwtEstimator.reduce_records on the GPU path.
+    `reduce` is RwtEstimator.reduce_records on the GPU path.  When `est` has
+    the library's communicator attached (attach_comm) its records are already
+    global and this is the identity.
     """
+    if est is not None and getattr(est, "comm_attached", False):
+        return rec
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return rec
     return reduce(gather_records(rec, group))
 
 
-def sum_counts(counts: torch.Tensor, group=None) -> torch.Tensor:
+def sum_counts(counts: torch.Tensor, group=None, est=None) -> torch.Tensor:
+    if est is not None and getattr(est, "comm_attached", False):
+        return counts                                   # summed inside the C ABI
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     return counts
@@ -64,6 +89,8 @@ def local_search(est, row, moves: int = 2, per_iter: int = 1 << 16, iters: int =
     incumbent row stays identical on all ranks.  Equal to est.local_search on
     one rank.  Returns (row buffer, incumbent record).
     """
+    if getattr(est, "comm_attached", False):          # the library shards and exchanges itself
+        return est.local_search(row, moves, per_iter, iters, seed)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     lo, n = shard_range(per_iter, rank, world)

@@ -109,6 +109,37 @@ class RwtEstimator:
         except Exception:
             pass
 
+    # -- multi-GPU: the library's own NCCL communicator (include/qlm.h) -----------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """A fresh 128-byte NCCL unique id (rank 0; broadcast it to the others)."""
+        buf = (C.c_uint8 * L.COMM_ID_BYTES)()
+        L.check(L.lib().qlm_comm_unique_id(buf), "qlm_comm_unique_id")
+        return bytes(buf)
+
+    def comm_attach(self, uid: bytes, rank: int, world: int):
+        """Collective: attach this context to the communicator `uid` as `rank` of
+        `world`; argmin records become global and MC counts sums over ranks."""
+        if len(uid) != L.COMM_ID_BYTES:
+            raise ValueError(f"unique id must be {L.COMM_ID_BYTES} bytes, got {len(uid)}")
+        buf = (C.c_uint8 * L.COMM_ID_BYTES).from_buffer_copy(uid)
+        torch.cuda.synchronize(self.device)
+        L.check(L.lib().qlm_comm_attach(self._h, buf, rank, world), "qlm_comm_attach")
+        self._comm = (rank, world)
+
+    def comm_detach(self):
+        L.check(L.lib().qlm_comm_detach(self._h), "qlm_comm_detach")
+        self._comm = None
+
+    def comm_info(self) -> dict:
+        r, w, v = C.c_int32(), C.c_int32(), C.c_int32()
+        L.check(L.lib().qlm_comm_info(self._h, C.byref(r), C.byref(w), C.byref(v)), "qlm_comm_info")
+        return dict(rank=r.value, world=w.value, nccl_version=v.value)
+
+    @property
+    def comm_attached(self) -> bool:
+        return getattr(self, "_comm", None) is not None
+
     # -- helpers --------------------------------------------------------------
     def _stream(self, stream):
         s = torch.cuda.current_stream(self.device) if stream is None else stream

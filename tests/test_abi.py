@@ -159,7 +159,29 @@ def test_null_context_calls_fail_cleanly(lib):
     assert lib.qlm_adopt_best(None, C.byref(cand), None, None, None) == L.QLM_EINVAL
     assert lib.qlm_local_search(None, None, 1, 2, 64, 1, 1, None, None) == L.QLM_EINVAL
     lib.qlm_destroy(None)
-    assert lib.qlm_abi_version() == 3
+    assert lib.qlm_abi_version() == 4
+
+
+def test_comm_calls_validate_on_the_host(lib):
+    # the communicator entry points reject bad arguments before
+    # touching CUDA or NCCL
+    buf = (C.c_uint8 * L.COMM_ID_BYTES)()
+    assert lib.qlm_comm_unique_id(None) == L.QLM_EINVAL
+    assert lib.qlm_comm_attach(None, buf, 0, 1) == L.QLM_EINVAL
+    assert lib.qlm_comm_detach(None) == L.QLM_EINVAL
+    assert lib.qlm_comm_info(None, None, None, None) == L.QLM_EINVAL
+    assert "NULL" in lib.qlm_last_error().decode()
+
+
+def test_comm_unique_id_needs_no_gpu(lib):
+    # NCCL is resolved at run time (dlopen); the unique id is host-side bootstrap
+    # state, so it can be made on the CPU host; without NCCL the call names it
+    buf = (C.c_uint8 * L.COMM_ID_BYTES)()
+    rc = lib.qlm_comm_unique_id(buf)
+    if rc == L.QLM_OK:
+        assert any(bytes(buf))
+    else:
+        assert rc == L.QLM_ENCCL and "nccl" in lib.qlm_last_error().decode().lower()
 
 
 def test_form_groups_host_validation(lib):

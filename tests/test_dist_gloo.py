@@ -235,3 +235,52 @@ def test_two_rank_gloo_tiered_argmin():
     want = O.argmin_key(full["s1"], full["s2"])
     for _, g in res:
         assert g[1] == want
+
+
+# ------------------------------------- the library's communicator: id plumbing
+class _FakeCommEstimator:
+    """Stands in for RwtEstimator: records what comm_attach receives."""
+
+    def __init__(self):
+        self.got = None
+        self.comm_attached = False
+
+    def comm_attach(self, uid, rank, world):
+        self.got = (uid, rank, world)
+        self.comm_attached = True
+
+
+def _attach_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2407_00047_b200.dist import attach_comm
+        est = _FakeCommEstimator()
+        attach_comm(est, unique_id=lambda: bytes(range(7, 135)))
+        rec = torch.tensor([1, 2], dtype=torch.int64)
+        same = global_best(rec, cpu_reduce, est=est)        # records already global: identity
+        cnt = torch.ones(3, dtype=torch.int64)
+        sum_counts(cnt, est=est)                             # summed inside the C ABI: identity
+        q.put((rank, est.got, same.tolist(), cnt.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_comm_id_broadcast():
+    """attach_comm: rank 0's 128-byte NCCL unique id reaches every rank intact
+    (torch.distributed carries only that), each rank attaches with its own
+    (rank, world), and the Python exchange helpers become pass-throughs."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_attach_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    for rank, (uid, r, w), same, cnt in res:
+        assert uid == bytes(range(7, 135)) and r == rank and w == world
+        assert same == [1, 2] and cnt == [1, 1, 1]
