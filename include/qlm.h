@@ -160,10 +160,11 @@ QLM_API void qlm_destroy(qlm_ctx *ctx);
 QLM_API const char *qlm_last_error(void);
 
 /* Replace all G group records (same G) from host memory: validated on the
- * host, copied H2D on `stream` and the derived tables rebuilt there
- * (asynchronous).  The host array must stay valid until the stream reaches
- * the copy (pinned memory recommended).  A new request arriving in a group
- * is this call.                                                */
+ * host, deep-copied into a context-owned pinned buffer (the caller may reuse
+ * or free the array on return; the device reads the validated snapshot),
+ * copied H2D on `stream` and the derived tables rebuilt there (asynchronous).
+ * Back-to-back calls wait for the previous call's copy to leave the staging
+ * buffer.  A new request arriving in a group is this call.     */
 QLM_API int qlm_update_groups(qlm_ctx *ctx, const qlm_group *groups, void *stream);
 
 /* ---- the hot path -------------------------------------------------------- */
@@ -216,8 +217,9 @@ typedef struct {
     const double *load_s;     /* host [D][M] >= 0: storage -> CPU load time (s)      */
 } qlm_tiers;
 
-/* Set (deep copy, synchronous) or clear (tiers = NULL) the context's tier
- * tables.  Errors: QLM_EINVAL (M > 32, a NULL array, a size < 1, a negative
+/* Set (deep copy, synchronous: drains the context's device first, so no
+ * tiered kernel on any stream reads half-updated tables) or clear (tiers =
+ * NULL) the context's tier tables.  Errors: QLM_EINVAL (M > 32, a NULL array, a size < 1, a negative
  * cap, a negative or non-finite load; the message names it), QLM_ERANGE
  * (sum of model_mem > 2^24).                                               */
 QLM_API int qlm_set_tiers(qlm_ctx *ctx, const qlm_tiers *tiers);
@@ -393,6 +395,19 @@ QLM_API int qlm_comm_info(const qlm_ctx *ctx, int32_t *rank, int32_t *world, int
 /* ---- introspection --------------------------------------------------------- */
 QLM_API int qlm_dims(const qlm_ctx *ctx, int32_t *G, int32_t *Q, int32_t *T, int32_t *D, int32_t *M);
 QLM_API int64_t qlm_kernel_launches(void);   /* kernels launched by this process so far */
+
+/* Testing: restrict the kernel selection process-wide so tests can compare
+ * the kernels that implement one call (they must agree bit for bit, R22).
+ * flags: QLM_OVERRIDE_* bits (0 = the measured default choice); ilv_cap > 0
+ * limits the candidates per chunk of the large-T two-phase path (0 = the
+ * default).  Errors: QLM_EINVAL on unknown bits or ilv_cap < 0.             */
+#define QLM_OVERRIDE_NO_WS 1u          /* no warp-specialised kernels (qlm_ws.cu, qlm_ws2.cu) */
+#define QLM_OVERRIDE_NO_WS2 2u         /* no D = 1 warp-specialised kernel (qlm_ws2.cu)       */
+#define QLM_OVERRIDE_NO_TWO_PHASE 4u   /* no two-phase large-T RANDOM path                    */
+#define QLM_OVERRIDE_NO_WIDE 8u        /* no warp-per-candidate large-G bulk kernel           */
+#define QLM_OVERRIDE_NO_TIER_WARP 16u  /* no lane-per-queue tiered kernel                     */
+#define QLM_OVERRIDE_ALL 31u
+QLM_API int qlm_set_kernel_overrides(uint32_t flags, int64_t ilv_cap);
 QLM_API int qlm_abi_version(void);
 
 #ifdef __cplusplus

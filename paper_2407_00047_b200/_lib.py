@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("QLM_LIB_PATH") or os.path.join(os.path.dirname(os.pat
 
 QLM_OK, QLM_EINVAL, QLM_ENOMEM, QLM_ECUDA, QLM_ENCCL, QLM_EBADORDER, QLM_ERANGE = 0, 1, 2, 3, 4, 5, 6
 COMM_ID_BYTES = 128
+OVERRIDE = {"no_ws": 1, "no_ws2": 2, "no_two_phase": 4, "no_wide": 8, "no_tier_warp": 16}
 CAND_EXPLICIT, CAND_RANDOM, CAND_ENUM, CAND_NEIGHBOR = 0, 1, 2, 3
 MAX_MOVES = 8
 
@@ -102,6 +103,7 @@ SIGNATURES = {
     "qlm_comm_attach": (C.c_int, [_vp, _vp, _i32, _i32]),
     "qlm_comm_detach": (C.c_int, [_vp]),
     "qlm_comm_info": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "qlm_set_kernel_overrides": (C.c_int, [C.c_uint32, _i64]),
 }
 
 _lib = None

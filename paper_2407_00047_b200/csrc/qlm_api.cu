@@ -72,6 +72,8 @@ struct qlm_ctx {
     int32_t *d_comm_buf = nullptr;         // [2G + 5] winner decode / scores (max all-reduce)
     std::vector<qlm_group> groups;
     int slo_hi_only = 0;                   // every groups[i].slo_s has a zero low word
+    qlm_group *h_stage = nullptr;          // pinned staging of qlm_update_groups (deep copy)
+    cudaEvent_t ev_stage = nullptr;        // the staging's last H2D copy
     std::vector<qlm_queue> queues;
     std::vector<double> prof;              // theta|prefill|eps|dec|maxo [D*M] each, swap [D*M*M]
 };
@@ -99,6 +101,13 @@ int validate_groups(const qlm_group *g, int G, int M, int n_tables) {
             return fail(QLM_EINVAL, "groups[%d].n_req=%d > 65536 with a length table", i, x.n_req);
         if (x.reserved != 0) return fail(QLM_EINVAL, "groups[%d].reserved must be 0", i);
     }
+    // S1's numerator over clamped slots is a sum of n_i kept in fp32 by every
+    // kernel: exact while the total request count is below 2^24 (R11)
+    int64_t total = 0;
+    for (int i = 0; i < G; ++i) total += g[i].n_req;
+    if (total >= ((int64_t)1 << 24))
+        return fail(QLM_ERANGE, "sum of groups[].n_req = %lld >= 2^24 (S1 is exact below 2^24 requests)",
+                    (long long)total);
     return QLM_OK;
 }
 
@@ -112,6 +121,21 @@ int slo_hi_only(const std::vector<qlm_group> &g) {
     }
     return 1;
 }
+
+// Every entry point leaves the caller's current device as it found it: the
+// context's device is made current for the call and restored on return.
+struct DevGuard {
+    int prev = -1;
+    DevGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); prev = -1; }
+    }
+    ~DevGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DevGuard(const DevGuard &) = delete;
+    DevGuard &operator=(const DevGuard &) = delete;
+};
 
 int check_dev(qlm_ctx *ctx) {
     cudaError_t e = cudaSetDevice(ctx->device);
@@ -233,14 +257,13 @@ ScanParams base_params(const qlm_ctx *ctx, const qlm_candidates *c) {
 void attach_ilv(qlm_ctx *ctx, ScanParams &p) {
     if (p.cd.kind != QLM_CAND_RANDOM || ctx->dm.T <= 256 || p.cd.first_from || p.cd.count < 4096)
         return;
-    const char *off = getenv("QLM_NO_TWO_PHASE");       // tests: force the fused fallback
-    if (off && *off && *off != '0') return;
+    if (override_on(QLM_OVERRIDE_NO_TWO_PHASE)) return;   // tests: force the fused fallback
     if (!ctx->d_ilv) {
         const size_t row_bytes = (size_t)((ctx->dm.T + 1) / 2) * 4;
         int64_t cap = (int64_t)(((size_t)1 << 30) / row_bytes);
         cap = cap > 262144 ? 262144 : cap;
-        const char *ec = getenv("QLM_ILV_CAP");           // tests: small chunks
-        if (ec && *ec && atoll(ec) > 0 && atoll(ec) < cap) cap = atoll(ec);
+        const int64_t ec = g_override_ilv_cap.load();      // tests: small chunks
+        if (ec > 0 && ec < cap) cap = ec;
         cap &= ~int64_t(31);
         if (cap < 32) return;
         if (cudaMalloc(&ctx->d_ilv, (size_t)cap * row_bytes) != cudaSuccess) {
@@ -278,6 +301,14 @@ const char *qlm_last_error(void) { return g_err.c_str(); }
 
 int64_t qlm_kernel_launches(void) { return g_launches.load(); }
 
+int qlm_set_kernel_overrides(uint32_t flags, int64_t ilv_cap) {
+    if (flags & ~(uint32_t)QLM_OVERRIDE_ALL) return fail(QLM_EINVAL, "flags=0x%x has unknown bits", flags);
+    if (ilv_cap < 0) return fail(QLM_EINVAL, "ilv_cap=%lld < 0", (long long)ilv_cap);
+    g_override_flags.store(flags);
+    g_override_ilv_cap.store(ilv_cap);
+    return QLM_OK;
+}
+
 int qlm_dims(const qlm_ctx *ctx, int32_t *G, int32_t *Q, int32_t *T, int32_t *D, int32_t *M) {
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     if (G) *G = ctx->dm.G;
@@ -291,6 +322,7 @@ int qlm_dims(const qlm_ctx *ctx, int32_t *G, int32_t *Q, int32_t *T, int32_t *D,
 int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int32_t Q,
                const qlm_profile *prof, const qlm_len_tables *tabs, const qlm_options *opt,
                qlm_ctx **out) {
+    DevGuard dg_;
     if (!out) return fail(QLM_EINVAL, "out is NULL");
     *out = nullptr;
     if (!groups || G < 1) return fail(QLM_EINVAL, "G=%d must be >= 1 with non-NULL groups", G);
@@ -455,6 +487,7 @@ int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int3
 }
 
 void qlm_destroy(qlm_ctx *ctx) {
+    DevGuard dg_;
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->comm) qlm_comm_detach(ctx);
@@ -463,17 +496,33 @@ void qlm_destroy(qlm_ctx *ctx) {
                     ctx->d_ls_rec, ctx->d_tier};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    if (ctx->ev_stage) cudaEventDestroy(ctx->ev_stage);
     delete ctx;
 }
 
 int qlm_update_groups(qlm_ctx *ctx, const qlm_group *groups, void *stream) {
+    DevGuard dg_;
     if (!ctx || !groups) return fail(QLM_EINVAL, "ctx or groups is NULL");
     int rc = validate_groups(groups, ctx->dm.G, ctx->dm.M, ctx->dm.n_tables);
     if (rc || (rc = check_dev(ctx))) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaMemcpyAsync(ctx->d_groups, groups, ctx->dm.G * sizeof(qlm_group),
-                                    cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "update_groups copy");
+    const size_t bytes = ctx->dm.G * sizeof(qlm_group);
+    cudaError_t e;
+    if (!ctx->h_stage) {
+        if ((e = cudaMallocHost(&ctx->h_stage, bytes)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ctx->ev_stage, cudaEventDisableTiming)) != cudaSuccess) {
+            ctx->h_stage = nullptr;
+            return cuda_fail(e, "update_groups staging");
+        }
+    } else if ((e = cudaEventSynchronize(ctx->ev_stage)) != cudaSuccess) {   // previous copy has read it
+        return cuda_fail(e, "update_groups staging");
+    }
+    // deep copy: the device reads the validated snapshot, never the caller's buffer
+    memcpy(ctx->h_stage, groups, bytes);
+    if ((e = cudaMemcpyAsync(ctx->d_groups, ctx->h_stage, bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (e = cudaEventRecord(ctx->ev_stage, st)) != cudaSuccess)
+        return cuda_fail(e, "update_groups copy");
     ctx->groups.assign(groups, groups + ctx->dm.G);
     ctx->slo_hi_only = slo_hi_only(ctx->groups);
     return rebuild(ctx, st);
@@ -481,6 +530,7 @@ int qlm_update_groups(qlm_ctx *ctx, const qlm_group *groups, void *stream) {
 
 int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, float *s2,
                         int32_t *n_over, void *stream) {
+    DevGuard dg_;
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -495,6 +545,7 @@ int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, flo
 
 int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record *rec,
                             void *stream) {
+    DevGuard dg_;
     if (!ctx || !rec) return fail(QLM_EINVAL, "ctx or rec is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -514,6 +565,7 @@ int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record
 
 int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, qlm_record *out,
                        void *stream) {
+    DevGuard dg_;
     if (!ctx || !recs || !out || n < 1) return fail(QLM_EINVAL, "reduce_records: bad arguments");
     int rc = check_dev(ctx);
     if (rc) return rc;
@@ -523,6 +575,7 @@ int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, qlm_reco
 
 int qlm_decode(qlm_ctx *ctx, const qlm_candidates *cand, int32_t *queue_of_group,
                int32_t *pos_of_group, void *stream) {
+    DevGuard dg_;
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -534,6 +587,7 @@ int qlm_decode(qlm_ctx *ctx, const qlm_candidates *cand, int32_t *queue_of_group
 }
 
 int qlm_rows(qlm_ctx *ctx, const qlm_candidates *cand, uint16_t *rows_out, void *stream) {
+    DevGuard dg_;
     if (!ctx || !rows_out) return fail(QLM_EINVAL, "ctx or rows_out is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -545,6 +599,7 @@ int qlm_rows(qlm_ctx *ctx, const qlm_candidates *cand, uint16_t *rows_out, void 
 
 int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
                       int32_t *queue_of_group, int32_t *pos_of_group, void *stream) {
+    DevGuard dg_;
     if (!ctx || !out) return fail(QLM_EINVAL, "ctx or out is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -623,6 +678,7 @@ int qlm_rwt_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean, f
 int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean, float *wt_std,
                        float *viol, float *s1, float *s2, int32_t *n_over, qlm_record *rec,
                        void *stream) {
+    DevGuard dg_;
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -645,6 +701,7 @@ int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
 
 int qlm_mc_sample(qlm_ctx *ctx, uint64_t mc_seed, int64_t trial_first, int64_t trial_count,
                   void *stream) {
+    DevGuard dg_;
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_dev(ctx);
     if (rc) return rc;
@@ -674,6 +731,7 @@ int qlm_mc_sample(qlm_ctx *ctx, uint64_t mc_seed, int64_t trial_first, int64_t t
 
 int qlm_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count, uint32_t *counts,
                  void *stream) {
+    DevGuard dg_;
     if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -702,6 +760,7 @@ int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
 }
 
 int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, void *stream) {
+    DevGuard dg_;
     if (!ctx || !n_bad) return fail(QLM_EINVAL, "ctx or n_bad is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -719,6 +778,7 @@ int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, voi
 
 int qlm_adopt_best(qlm_ctx *ctx, const qlm_candidates *cand, const qlm_record *rec,
                    qlm_record *incumbent, void *stream) {
+    DevGuard dg_;
     if (!ctx || !rec || !incumbent) return fail(QLM_EINVAL, "ctx, rec or incumbent is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -729,6 +789,7 @@ int qlm_adopt_best(qlm_ctx *ctx, const qlm_candidates *cand, const qlm_record *r
 
 int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves, int64_t per_iter,
                      int32_t iters, uint64_t seed, qlm_record *incumbent, void *stream) {
+    DevGuard dg_;
     if (!ctx || !row || !incumbent) return fail(QLM_EINVAL, "ctx, row or incumbent is NULL");
     if (moves < 1 || moves > QLM_MAX_MOVES)
         return fail(QLM_EINVAL, "moves=%d must lie in [1, %d]", moves, QLM_MAX_MOVES);
@@ -784,6 +845,7 @@ int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves
 
 int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac, float *s1_req,
                            void *stream) {
+    DevGuard dg_;
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -799,6 +861,7 @@ int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac
 }
 
 int qlm_set_tiers(qlm_ctx *ctx, const qlm_tiers *tiers) {
+    DevGuard dg_;
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_dev(ctx);
     if (rc) return rc;
@@ -837,7 +900,11 @@ int qlm_set_tiers(qlm_ctx *ctx, const qlm_tiers *tiers) {
     memcpy(h.data(), tiers->model_mem, (size_t)M * 4);
     memcpy(h.data() + o_cap, tiers->cpu_cap, (size_t)D * 4);
     memcpy(h.data() + o_load, tiers->load_s, (size_t)D * M * 8);
-    cudaError_t e = cudaMemcpy(ctx->d_tier, h.data(), bytes, cudaMemcpyHostToDevice);
+    // tiered kernels may still read the old tables on any stream: drain the
+    // device before overwriting them (this call is synchronous by contract)
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "set_tiers: device sync");
+    e = cudaMemcpy(ctx->d_tier, h.data(), bytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "upload tier tables");
     ctx->has_tiers = true;
     return QLM_OK;
@@ -846,6 +913,7 @@ int qlm_set_tiers(qlm_ctx *ctx, const qlm_tiers *tiers) {
 int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
                               float *wt_std, float *viol, float *s1, float *s2, int32_t *n_over,
                               qlm_record *rec, void *stream) {
+    DevGuard dg_;
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     if (!ctx->has_tiers) return fail(QLM_EINVAL, "no tier tables: call qlm_set_tiers first");
     int rc = check_cand(ctx, cand);
@@ -875,6 +943,7 @@ int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *w
 int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k_per_model, int32_t limit,
                     int32_t max_iter, int32_t *label_of, int32_t *group_of, qlm_group *groups,
                     int32_t group_cap, int32_t *n_groups, int32_t *iters, int32_t device, void *stream) {
+    DevGuard dg_;
     if (!req || !k_per_model || !n_groups)
         return fail(QLM_EINVAL, "req, k_per_model and n_groups must be non-NULL");
     if (req->n < 1 || req->n >= (1 << 28)) return fail(QLM_EINVAL, "req.n=%d not in [1, 2^28)", req->n);
@@ -909,6 +978,7 @@ int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k_per_mod
 
 int qlm_tiered_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count,
                         uint32_t *counts, void *stream) {
+    DevGuard dg_;
     if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
     if (!ctx->has_tiers) return fail(QLM_EINVAL, "no tier tables: call qlm_set_tiers first");
     int rc = check_cand(ctx, cand);
@@ -940,6 +1010,7 @@ int qlm_comm_unique_id(uint8_t id[QLM_COMM_ID_BYTES]) {
 }
 
 int qlm_comm_attach(qlm_ctx *ctx, const uint8_t id[QLM_COMM_ID_BYTES], int32_t rank, int32_t world) {
+    DevGuard dg_;
     if (!ctx || !id) return fail(QLM_EINVAL, "ctx or id is NULL");
     if (world < 1 || rank < 0 || rank >= world)
         return fail(QLM_EINVAL, "rank=%d, world=%d: need 0 <= rank < world", rank, world);
@@ -965,6 +1036,7 @@ int qlm_comm_attach(qlm_ctx *ctx, const uint8_t id[QLM_COMM_ID_BYTES], int32_t r
 }
 
 int qlm_comm_detach(qlm_ctx *ctx) {
+    DevGuard dg_;
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     if (!ctx->comm) return QLM_OK;
     int rc = check_dev(ctx);

@@ -13,7 +13,9 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 
 #include "qlm_device.cuh"
@@ -22,6 +24,8 @@
 namespace qlm {
 
 std::atomic<int64_t> g_launches{0};
+std::atomic<uint32_t> g_override_flags{0};
+std::atomic<int64_t> g_override_ilv_cap{0};
 
 // =============================================================================
 // a0: table build (one block; runs once per qlm_create / qlm_update_groups)
@@ -752,23 +756,39 @@ __global__ void __launch_bounds__(32 * kMcWarps) mc_count_kernel(Dims dm, Tables
 // =============================================================================
 // launchers
 // =============================================================================
-static int g_sm_count = 0;
-
+// Per-device caches: a process may hold contexts on several ordinals, and the
+// SM count and the dynamic shared-memory opt-in are properties of a device.
 int sm_count() {
-    if (!g_sm_count) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return g_sm_count;
+    static std::mutex mu;
+    static std::unordered_map<int, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n;
+    return n;
+}
+
+// Environment overrides (tests and tuning only) are read once per process.
+int env_cached(const char *name, int dflt) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const std::string key = std::string(name) + "#" + std::to_string(dflt);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    const char *v = getenv(name);
+    const int r = v && *v ? atoi(v) : dflt;
+    cache[key] = r;
+    return r;
 }
 
 static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-static int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
+static int env_int(const char *name, int dflt) { return env_cached(name, dflt); }
 
 static const size_t kMaxSmem = 227 * 1024;
 
@@ -777,12 +797,13 @@ static const size_t kMaxSmem = 227 * 1024;
 template <typename K>
 static size_t max_dyn(K kern) {
     static std::mutex mu;
-    static std::unordered_map<const void *, size_t> cache;
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find(reinterpret_cast<const void *>(kern));
-    if (it != cache.end()) return it->second;
+    static std::map<std::pair<const void *, int>, size_t> cache;   // (kernel, device)
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(reinterpret_cast<const void *>(kern), dev);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) { cudaGetLastError(); return 0; }
@@ -792,7 +813,7 @@ static size_t max_dyn(K kern) {
         cudaGetLastError();
         return 0;
     }
-    cache[reinterpret_cast<const void *>(kern)] = m;
+    cache[key] = m;
     return m;
 }
 
@@ -1064,6 +1085,7 @@ cudaError_t launch_reduce_records(const qlm_record *recs, int n, qlm_record *out
 
 cudaError_t launch_check_rows(const Cand &cd, int T, unsigned long long *n_bad, cudaStream_t st) {
     if (cd.count <= 0) return cudaSuccess;
+    if (cd.count > INT32_MAX) return cudaErrorInvalidValue;        // one block per row
     const size_t smem = (size_t)((T + 31) / 32) * 4;
     check_rows_kernel<<<(unsigned)cd.count, 128, smem, st>>>(cd, T, n_bad);
     ++g_launches;

@@ -42,7 +42,12 @@ struct ScanParams {
 constexpr int KIND_ILV = 7;
 
 extern std::atomic<int64_t> g_launches;
-int sm_count();
+// qlm_set_kernel_overrides (tests: compare kernel paths on one process)
+extern std::atomic<uint32_t> g_override_flags;
+extern std::atomic<int64_t> g_override_ilv_cap;
+inline bool override_on(uint32_t bit) { return (g_override_flags.load(std::memory_order_relaxed) & bit) != 0; }
+int sm_count();                                 // of the current device (cached per device)
+int env_cached(const char *name, int dflt);     // tuning/test overrides, read once per process
 
 cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
                          const double *theta, const double *prefill, const double *eps,

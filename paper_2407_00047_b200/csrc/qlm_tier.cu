@@ -448,8 +448,7 @@ static cudaError_t launch_tier_warp(const ScanParams &p, cudaStream_t st) {
 cudaError_t launch_tier(const ScanParams &p, cudaStream_t st) {
     const cudaError_t ws = launch_ws_tier(p, st);            // warp-specialised fast path
     if (ws != cudaErrorNotSupported) return ws;
-    const char *nw = getenv("QLM_NO_TIER_WARP");
-    if (p.dm.G > 256 && !(nw && *nw && *nw != '0')) {        // large G: lane per queue
+    if (p.dm.G > 256 && !override_on(QLM_OVERRIDE_NO_TIER_WARP)) {   // large G: lane per queue
         const cudaError_t w = launch_tier_warp(p, st);
         if (w != cudaErrorNotSupported) return w;
         cudaGetLastError();

@@ -314,8 +314,7 @@ static cudaError_t launch_wide_t(ScanParams p, cudaStream_t st) {
 // Warp-per-candidate path: rows word-interleaved (two-phase chunks) or
 // EXPLICIT u16.  cudaErrorNotSupported when it does not apply.
 cudaError_t launch_wide(const ScanParams &p, cudaStream_t st) {
-    const char *off = getenv("QLM_NO_WIDE");
-    if (off && *off && *off != '0') return cudaErrorNotSupported;
+    if (override_on(QLM_OVERRIDE_NO_WIDE)) return cudaErrorNotSupported;
     if (p.cd.first_from || p.cd.count < 1) return cudaErrorNotSupported;
     const bool ilv = p.cd.kind == KIND_ILV;
     const bool ex16 = p.cd.kind == QLM_CAND_EXPLICIT && p.cd.tb == 2;

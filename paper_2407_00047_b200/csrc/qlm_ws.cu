@@ -26,6 +26,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "qlm_device.cuh"
 #include "qlm_launch.h"
@@ -543,10 +545,7 @@ static bool make_map(CUtensorMap *tm, float *ptr, int64_t count, int G) {
 static size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 static size_t a1k(size_t x) { return (x + 1023) & ~size_t(1023); }
 
-static int env_int_ws(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
+static int env_int_ws(const char *name, int dflt) { return env_cached(name, dflt); }
 
 // Shared-memory plan for W pairs; returns total bytes.
 static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage, bool tier) {
@@ -572,26 +571,34 @@ static size_t plan_ws(WsParams &w, int W, int rs, int tok_bytes, bool stage, boo
     return off;
 }
 
+// Dynamic shared-memory opt-in of a kernel on the current device (the
+// attribute is per device), cached per (kernel, device).
 template <typename K>
 static size_t ws_max_dyn(K kern) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, size_t> cache;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(reinterpret_cast<const void *>(kern), dev);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) { cudaGetLastError(); return 0; }
-    const size_t m = optin > (int)fa.sharedSizeBytes + 1024 ? (size_t)optin - fa.sharedSizeBytes - 1024 : 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
+    size_t m = 0;
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && optin > (int)fa.sharedSizeBytes + 1024) {
+        m = (size_t)optin - fa.sharedSizeBytes - 1024;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m) != cudaSuccess) m = 0;
     }
+    cudaGetLastError();
+    cache[key] = m;
     return m;
 }
 
 template <int KIND, typename TOK, bool SCORE, int RS, bool TIER>
 static cudaError_t launch_ws_rs(WsParams &w, size_t smem, int W, cudaStream_t st) {
     auto kern = ws_kernel<KIND, TOK, SCORE, RS, TIER>;
-    static size_t lim = 0;
-    if (!lim) lim = ws_max_dyn(kern);
+    const size_t lim = ws_max_dyn(kern);
     if (!lim || smem > lim) return cudaErrorNotSupported;
     const int64_t nbatch = (w.p.cd.count + 31) / 32;
     int64_t grid = sm_count();
@@ -634,7 +641,8 @@ static cudaError_t launch_ws_t(const ScanParams &p0, cudaStream_t st) {
     // 0.370 -> 0.350 ms); QLM_WS_SPREAD=0 restores the plain warp order
     w.spread = (bestW == 6 && env_int_ws("QLM_WS_SPREAD", 1)) ? 1 : 0;
     if (STAGE) {
-        const bool aligned = (p0.cd.count % 4 == 0) && (!p0.wt || ((uintptr_t)p0.wt & 15) == 0) &&
+        const bool aligned = (p0.cd.count % 4 == 0) && p0.cd.count <= INT32_MAX - 64 &&   // int32 TMA x
+                             (!p0.wt || ((uintptr_t)p0.wt & 15) == 0) &&
                              (!p0.sd || ((uintptr_t)p0.sd & 15) == 0) &&
                              (!p0.vo || ((uintptr_t)p0.vo & 15) == 0) && p0.dm.G <= 256;
         bool ok = aligned;
@@ -659,7 +667,7 @@ static cudaError_t launch_ws_k(ScanParams &p, cudaStream_t st) {
 // Two-tier swapping (R20) through the warp-specialised kernel: RANDOM and
 // EXPLICIT candidates with bulk outputs (the tier kernel covers the rest).
 cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st) {
-    if (p.cd.first_from || p.cd.count < 4096 || env_int_ws("QLM_NO_WS", 0)) return cudaErrorNotSupported;
+    if (p.cd.first_from || p.cd.count < 4096 || override_on(QLM_OVERRIDE_NO_WS)) return cudaErrorNotSupported;
     if (!(p.wt || p.sd || p.vo) || p.dm.M > 32) return cudaErrorNotSupported;
     if ((size_t)3 * (p.dm.G + 1) * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
     switch (p.cd.kind) {
@@ -676,8 +684,8 @@ cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st) {
 
 // Fast path for large candidate sets; cudaErrorNotSupported -> caller falls back.
 cudaError_t launch_ws(ScanParams p, cudaStream_t st) {
-    if (p.cd.first_from || p.cd.count < 4096 || env_int_ws("QLM_NO_WS", 0)) return cudaErrorNotSupported;
-    if (!env_int_ws("QLM_NO_WS2", 0)) {
+    if (p.cd.first_from || p.cd.count < 4096 || override_on(QLM_OVERRIDE_NO_WS)) return cudaErrorNotSupported;
+    if (!override_on(QLM_OVERRIDE_NO_WS2)) {
         const cudaError_t e = launch_ws2(p, st);
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();

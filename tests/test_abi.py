@@ -151,6 +151,18 @@ def test_queue_and_profile_validation(lib):
     assert rc == L.QLM_ERANGE and "32768" in msg
 
 
+def test_total_requests_below_2_pow_24(lib):
+    # S1's clamped-slot numerator is an fp32 sum of n_i: exact below 2^24 (R11)
+    g = np.zeros(2, L.GROUP_DTYPE)
+    g["n_req"], g["slo_s"], g["mu_out"], g["dist_id"] = [1 << 23, (1 << 23) - 1], 10.0, 100.0, -1
+    q = np.zeros(1, L.QUEUE_DTYPE)
+    rc, msg = _create(lib, g, q)
+    assert rc != L.QLM_ERANGE                          # 2^24 - 1 requests: accepted (no GPU -> ECUDA)
+    g["n_req"][1] = 1 << 23
+    rc, msg = _create(lib, g, q)
+    assert rc == L.QLM_ERANGE and "2^24" in msg
+
+
 def test_null_context_calls_fail_cleanly(lib):
     cand = L.Candidates(L.CAND_RANDOM, 1, None, 0, 1, 0, 10, None)
     assert lib.qlm_score_orderings(None, C.byref(cand), None, None, None, None) == L.QLM_EINVAL

@@ -23,6 +23,17 @@ def _built():
     __graft_entry__.build()
 
 
+def kernel_overrides(**kw):
+    from paper_2407_00047_b200 import kernel_overrides as ko
+    ko(**kw)
+
+
+@pytest.fixture(autouse=True)
+def _default_kernels():
+    yield
+    kernel_overrides()                          # every test ends on the default kernel choice
+
+
 def est_of(p, **kw):
     from paper_2407_00047_b200 import RwtEstimator
     return RwtEstimator(p, device=0, **kw)
@@ -348,7 +359,7 @@ def test_warp_specialised_and_fallback_kernels_agree(cfg, n, kind, monkeypatch):
         cand = e.explicit(rows_tensor(rows, token_bytes=p.token_bytes))
     res = {}
     for no_ws in ("1", "0"):
-        monkeypatch.setenv("QLM_NO_WS", no_ws)
+        kernel_overrides(no_ws=no_ws == "1")
         rec = torch.empty(2, dtype=torch.int64, device="cuda")
         bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
         bufs["n_over"] = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -432,8 +443,7 @@ def test_two_phase_large_T_matches_fused(cfg, n, out, monkeypatch):
     p = make_config(cfg)
     res = {}
     for mode in ("fused", "two_phase"):
-        monkeypatch.setenv("QLM_NO_TWO_PHASE", "1" if mode == "fused" else "0")
-        monkeypatch.setenv("QLM_ILV_CAP", "4096")
+        kernel_overrides(no_two_phase=mode == "fused", ilv_cap=4096)
         e = est_of(p)
         cand = e.random(7, n, seed=1)
         rec = torch.empty(2, dtype=torch.int64, device="cuda")
@@ -494,6 +504,10 @@ def test_wide_kernel_bulk_large_G(G, Q, D, backlog, n):
     s1 = r["s1"].cpu().numpy()[:4096]
     s2 = r["s2"].cpu().numpy()[:4096]
     check_scores(s1, s2, ref, p)
+    # the in-kernel argmin over all n candidates follows the oracle rule
+    full = o.score_range(O.RANDOM, 11, n, seed=5)
+    ok, cstar = argmin_ok(int(rec[1]), full["s1"], full["s2"], p, first=11)
+    assert ok, (int(rec[1]) - 11, cstar)
 
 
 # ------------------------------------------------------- NEIGHBOR candidates / local search (R18)
@@ -526,7 +540,7 @@ def test_neighbor_scores_and_bulk(cfg, n, moves, monkeypatch):
     check_scores(s1[:m].cpu().numpy(), s2[:m].cpu().numpy(), ref, p)
     res = {}
     for no_ws in ("1", "0"):
-        monkeypatch.setenv("QLM_NO_WS", no_ws)
+        kernel_overrides(no_ws=no_ws == "1")
         rec = torch.empty(2, dtype=torch.int64, device="cuda")
         bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
         res[no_ws] = (e.score_estimate(cand, out=bufs, rec=rec), rec)
@@ -685,10 +699,10 @@ def test_neighbor_u16_paths_c4_and_local_search_c5():
     cand = e.neighbor(base, 0, 4608, seed=6, moves=5)
     res = {}
     for no_ws in ("1", "0"):
-        os.environ["QLM_NO_WS"] = no_ws
+        kernel_overrides(no_ws=no_ws == "1")
         bufs = {k: torch.empty((p.G, 4608), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
         res[no_ws] = e.score_estimate(cand, out=bufs)
-    os.environ.pop("QLM_NO_WS", None)
+    kernel_overrides()
     for k in ("wt", "sd", "v", "s1", "s2"):
         assert torch.equal(res["0"][k], res["1"][k]), k
     est = O.Oracle(p).estimate_range(O.NEIGHBOR, 0, 64, seed=6, rows=base_np, moves=5)
@@ -819,9 +833,9 @@ def test_tiers_ws_path_bit_identical_to_thread_kernel(cfg, monkeypatch):
     n = 8192 + 64
     cand = e.random(31, n, seed=1)
     ws, rws = _tier_out(e, cand)
-    monkeypatch.setenv("QLM_NO_WS", "1")
+    kernel_overrides(no_ws=True)
     th, rth = _tier_out(e, cand)
-    monkeypatch.delenv("QLM_NO_WS")
+    kernel_overrides()
     for k in ("wt", "sd", "v", "s1", "s2", "n_over"):
         assert torch.equal(ws[k], th[k]), k
     assert torch.equal(rws, rth)
@@ -971,7 +985,7 @@ def test_tiers_large_G_lane_per_queue(G, Q, D, backlog, n, kind, monkeypatch):
     assert np.array_equal(warp["n_over"].cpu().numpy(), ref["n_over"])
     ok, _ = argmin_ok(int(rw[1]), ref["s1"], ref["s2"], p, first=kw["first"])
     assert ok
-    monkeypatch.setenv("QLM_NO_TIER_WARP", "1")
+    kernel_overrides(no_tier_warp=True)
     thr, _ = _tier_out(e, cand)
     for k in ("wt", "sd", "v"):
         assert torch.equal(warp[k], thr[k]), k

@@ -82,6 +82,43 @@ def test_random_rows_first_position_uniform(T):
     assert stats.chi2.sf(chi2, T - 1) > 1e-3
 
 
+@pytest.mark.parametrize("T", [2, 3, 71, 255, 256])
+def test_random_row_16bit_draw_is_multiply_shift_of_philox_R10(T):
+    # The oracle's first Fisher-Yates step for T <= 256 is exactly
+    # j0 = floor(u * T / 2^16), u = the low 16 bits of word 0 of the KAT-pinned
+    # Philox block (ctr = (0, lo32 c, hi32 c, 'QLM\0'), key = seed): row[0] == j0
+    # after the whole shuffle (later steps never touch position 0)
+    seed = 0x1234_5678_9ABC
+    for c in range(0, 4000, 7):
+        w = O.philox4x32_10([0, c & 0xFFFFFFFF, c >> 32, 0x514C4D00], [seed & 0xFFFFFFFF, seed >> 32])
+        u = int(w[0]) & 0xFFFF
+        assert O.random_row(seed, c, T)[0] == (u * T) >> 16
+
+
+def test_random_row_16bit_draw_bias_exact_R10():
+    # Exact bias of R10's 16-bit multiply-shift draws (no rejection): for every
+    # step range m = T - i in [2, 256], enumerate all 2^16 draws u and count the
+    # preimages of each index j = floor(u m / 2^16).  Each j gets floor(2^16/m)
+    # or ceil(2^16/m) draws, so a step's index probability is within a factor
+    # (ceil or floor)(2^16/m) * m / 2^16 of 1/m: relative bias <= m / 2^16,
+    # largest at m = 255 (1/257 = 0.389 %), zero when m divides 2^16.
+    u = np.arange(1 << 16, dtype=np.int64)
+    worst = 0.0
+    for m in range(2, 257):
+        cnt = np.bincount((u * m) >> 16, minlength=m)
+        fl, ce = (1 << 16) // m, -(-(1 << 16) // m)
+        assert cnt.sum() == 1 << 16 and set(np.unique(cnt)) <= {fl, ce}
+        assert int(cnt.max()) * m - (1 << 16) < m and (1 << 16) - int(cnt.min()) * m < m
+        worst = max(worst, (int(cnt.max()) - int(cnt.min())) * m / (1 << 16))
+    assert worst == 255 / 65536
+    # whole-row consequence (DESIGN R10): a C3 row (T = 71) has probability
+    # within [0.9830, 1.0203] x 1/71!; T = 256 within [0.8056, 1.3204] x 1/256!
+    for T, lo_b, hi_b in ((71, 0.9830, 1.0203), (256, 0.8056, 1.3204)):
+        lo = math.prod(((1 << 16) // m) * m / (1 << 16) for m in range(2, T + 1))
+        hi = math.prod((-(-(1 << 16) // m)) * m / (1 << 16) for m in range(2, T + 1))
+        assert lo_b <= lo < 1.0 < hi <= hi_b and abs(lo - lo_b) < 1e-4 and abs(hi - hi_b) < 1e-4
+
+
 # ---------------------------------------------------------------- SPEC worked examples
 def test_wait_mean_and_std_S279():
     g = gold("spec_examples.json")["wait_S279"]
@@ -214,7 +251,12 @@ def test_identical_groups_closed_form_P8():
 
 
 def test_insight3_interleaving_costs_extra_transitions():
-    # PAPER.md L351-357 / SPEC.md L316: interleaved X,Y,X,Y vs grouped X,X,Y,Y.
+    # PAPER.md L351-357 (Insight 3): interleaved X,Y,X,Y vs grouped X,X,Y,Y costs
+    # the extra model transitions.  Each transition costs tail + S here: Eq. 10
+    # charges the completion C = W + tail of the group ahead at a model boundary
+    # (reading R1, P:L705 / P:L743-746).  SPEC.md charges S
+    # only; that is a recorded divergence from SPEC (R1), not a
+    # SPEC pin.
     tail, S = 1.0, 20.0
     p = hand_problem([0, 1, 0, 1], 25, 200.0, 0.0, 1e4, theta=1000.0, prefill=0.5, eps=1.0,
                      dtok=0.5, max_out=1.0, swap=S, M=2)
