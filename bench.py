@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel roofline list")
     ap.add_argument("--config", default="C3", choices=["C2", "C3", "C5", "C5h"],
                     help="workload (BASELINE.json configs); the metric is quoted on C3")
     ap.add_argument("--candidates", type=int, default=None,
@@ -416,13 +417,23 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "weak", "vs_baseline": None, "dtype": DTYPE, "data": "synthetic",
             "config": workload_config(world),
             "roofline": roofline,
-            "kernels": {"fused_scan_ms": fused_ms,
-                        "fused_scan_orderings_per_s": N_PER_GPU / (fused_ms / 1e3),
-                        "share_of_step": {"fused_scan": fused_ms / ms_per_step}},
+            "step": {"fused_scan_ms": fused_ms,
+                     "fused_scan_orderings_per_s": N_PER_GPU / (fused_ms / 1e3),
+                     "share_of_step": {"fused_scan": fused_ms / ms_per_step}},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if world == 1 and not args.no_kernels:
+            # every other kernel of the library against its binding roof
+            # (SURVEY 8(d)); instruction counts from profiles/r2_kernels_ncu.json
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import kernel_suite
+            clk_mhz = clk.summary().get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
+            main = {"name": "score_estimate RANDOM fused a1-a7 (" + kname + ")", "config": CFG,
+                    "value": N_PER_GPU / (fused_ms / 1e3), "unit": UNIT, "ms": fused_ms,
+                    "roofline": {k: roofline[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}}
+            line["kernels"] = [main] + kernel_suite.run(reps=10, hbm_peak=hbm_peak, clk_mhz=clk_mhz)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
         print(json.dumps(line), flush=True)

@@ -1,5 +1,6 @@
 """Write profiles/ncu_traffic.json from an `ncu --page raw --csv` export of one
-ws_kernel launch (DRAM bytes and warp instructions per launch).
+launch of the bench step's fused kernel (ws2_kernel since round 2): DRAM
+bytes and warp instructions per launch, read by bench.py's roofline.
 
     ncu -i gpurun_out/ev_ws.ncu-rep --page raw --csv > raw.csv
     python tools/update_traffic.py raw.csv "<source note>"
