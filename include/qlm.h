@@ -292,8 +292,12 @@ QLM_API int qlm_adopt_best(qlm_ctx *ctx, const qlm_candidates *cand, const qlm_r
  * the argmin if it improves the key (qlm_adopt_best).  On completion `row`
  * holds the best ordering found and *incumbent its key (index = the
  * candidate index it was adopted from, -1 if the start row was kept).
- * Errors: QLM_EINVAL (moves outside 1..QLM_MAX_MOVES, per_iter < 1,
- * iters < 0, NULL pointers, misaligned row).                               */
+ * Unless the stream is already capturing, the 2*iters + 2
+ * launches are captured into a CUDA graph kept in the context (updated in
+ * place by later calls) and launched as one unit (the
+ * scheduler must stay off the critical path).  Errors: QLM_EINVAL (moves
+ * outside 1..QLM_MAX_MOVES, per_iter < 1, iters < 0, NULL pointers,
+ * misaligned row).                                                         */
 QLM_API int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves,
                      int64_t per_iter, int32_t iters, uint64_t seed, qlm_record *incumbent,
                      void *stream);
@@ -406,7 +410,8 @@ QLM_API int64_t qlm_kernel_launches(void);   /* kernels launched by this process
 #define QLM_OVERRIDE_NO_TWO_PHASE 4u   /* no two-phase large-T RANDOM path                    */
 #define QLM_OVERRIDE_NO_WIDE 8u        /* no warp-per-candidate large-G bulk kernel           */
 #define QLM_OVERRIDE_NO_TIER_WARP 16u  /* no lane-per-queue tiered kernel                     */
-#define QLM_OVERRIDE_ALL 31u
+#define QLM_OVERRIDE_NO_GRAPH 32u      /* qlm_local_search launches directly (no CUDA graph)   */
+#define QLM_OVERRIDE_ALL 63u
 QLM_API int qlm_set_kernel_overrides(uint32_t flags, int64_t ilv_cap);
 QLM_API int qlm_abi_version(void);
 

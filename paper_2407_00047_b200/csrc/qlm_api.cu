@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "qlm_comm.h"
 #include "qlm_launch.h"
 
@@ -68,6 +70,9 @@ struct qlm_ctx {
     bool has_tiers = false;
     // multi-GPU (qlm_comm_attach): the communicator and its scratch
     Comm *comm = nullptr;
+    cudaGraphExec_t ls_exec = nullptr;     // qlm_local_search's captured launches
+    cudaStream_t aux = nullptr;            // blocking stream standing in for the legacy default stream
+    std::vector<int64_t> ls_sig;           // arguments the captured search was built from
     qlm_record *d_comm_recs = nullptr;     // [world] gathered records
     int32_t *d_comm_buf = nullptr;         // [2G + 5] winner decode / scores (max all-reduce)
     std::vector<qlm_group> groups;
@@ -135,6 +140,16 @@ struct DevGuard {
     }
     DevGuard(const DevGuard &) = delete;
     DevGuard &operator=(const DevGuard &) = delete;
+};
+
+// NVTX range over an entry point (free when no tool is attached): nsys / ncu
+// timelines show every library call with its kernels and collectives.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) {
+        nvtxRangePushA(name);
+        qlog(2, "%s", name);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 int check_dev(qlm_ctx *ctx) {
@@ -291,6 +306,56 @@ int rebuild(qlm_ctx *ctx, cudaStream_t st) {
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "build_tables");
 }
 
+// The local search's launches (start-row score, then per iteration: the
+// neighbourhood argmin, the global exchange when a communicator is attached,
+// the adoption), in stream order on `st`.
+int enqueue_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves, int64_t per_iter,
+                   int32_t iters, uint64_t seed, qlm_record *incumbent, cudaStream_t st) {
+    const int T = ctx->dm.T;
+    int rc;
+    // score the start row (EXPLICIT, one candidate) into the incumbent record
+    qlm_candidates ex;
+    memset(&ex, 0, sizeof ex);
+    ex.kind = QLM_CAND_EXPLICIT;
+    ex.token_bytes = token_bytes;
+    ex.rows = row;
+    ex.stride = (((int64_t)T * token_bytes) + 15) / 16 * 16;
+    ex.count = 1;
+    if ((rc = check_cand(ctx, &ex))) return rc;
+    ScanParams p0 = base_params(ctx, &ex);
+    p0.out_rec = incumbent;
+    cudaError_t e = launch_any_scan(p0, st);
+    if (e == cudaSuccess)             // index -1: the start row is the incumbent
+        e = cudaMemsetAsync(&incumbent->index, 0xFF, sizeof(int64_t), st);
+    if (e != cudaSuccess) return cuda_fail(e, "local search: start row");
+    qlm_candidates nb = ex;
+    nb.kind = QLM_CAND_NEIGHBOR;
+    nb.stride = 0;
+    nb.seed = seed;
+    nb.moves = moves;
+    nb.count = per_iter;
+    // with a communicator, rank r scores its contiguous shard of every
+    // iteration and the global winner is adopted everywhere
+    int64_t sh_first = 0, sh_count = per_iter;
+    if (ctx->comm) shard(per_iter, comm_rank(ctx->comm), comm_world(ctx->comm), sh_first, sh_count);
+    for (int32_t it = 0; it < iters; ++it) {
+        nb.first = (int64_t)it * per_iter + sh_first;
+        nb.count = sh_count;
+        if ((rc = check_cand(ctx, &nb))) return rc;
+        if (sh_count > 0) {
+            ScanParams p = base_params(ctx, &nb);
+            p.out_rec = ctx->d_ls_rec;
+            if ((e = launch_any_scan(p, st)) != cudaSuccess) return cuda_fail(e, "local search: scores");
+        } else if ((e = cudaMemsetAsync(ctx->d_ls_rec, 0xFF, sizeof(qlm_record), st)) != cudaSuccess) {
+            return cuda_fail(e, "local search: empty shard");
+        }
+        if ((rc = global_record(ctx, ctx->d_ls_rec, st))) return rc;
+        if ((e = launch_adopt(ctx->dm, to_cand(&nb), ctx->d_ls_rec, incumbent, st)) != cudaSuccess)
+            return cuda_fail(e, "local search: adopt");
+    }
+    return QLM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -323,6 +388,7 @@ int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int3
                const qlm_profile *prof, const qlm_len_tables *tabs, const qlm_options *opt,
                qlm_ctx **out) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_create");
     if (!out) return fail(QLM_EINVAL, "out is NULL");
     *out = nullptr;
     if (!groups || G < 1) return fail(QLM_EINVAL, "G=%d must be >= 1 with non-NULL groups", G);
@@ -488,6 +554,7 @@ int qlm_create(const qlm_group *groups, int32_t G, const qlm_queue *queues, int3
 
 void qlm_destroy(qlm_ctx *ctx) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_destroy");
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     if (ctx->comm) qlm_comm_detach(ctx);
@@ -497,12 +564,15 @@ void qlm_destroy(qlm_ctx *ctx) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    if (ctx->ls_exec) cudaGraphExecDestroy(ctx->ls_exec);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->ev_stage) cudaEventDestroy(ctx->ev_stage);
     delete ctx;
 }
 
 int qlm_update_groups(qlm_ctx *ctx, const qlm_group *groups, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_update_groups");
     if (!ctx || !groups) return fail(QLM_EINVAL, "ctx or groups is NULL");
     int rc = validate_groups(groups, ctx->dm.G, ctx->dm.M, ctx->dm.n_tables);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -531,6 +601,7 @@ int qlm_update_groups(qlm_ctx *ctx, const qlm_group *groups, void *stream) {
 int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, float *s2,
                         int32_t *n_over, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_score_orderings");
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -546,6 +617,7 @@ int qlm_score_orderings(qlm_ctx *ctx, const qlm_candidates *cand, float *s1, flo
 int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record *rec,
                             void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_best_ordering_async");
     if (!ctx || !rec) return fail(QLM_EINVAL, "ctx or rec is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -566,6 +638,7 @@ int qlm_best_ordering_async(qlm_ctx *ctx, const qlm_candidates *cand, qlm_record
 int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, qlm_record *out,
                        void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_reduce_records");
     if (!ctx || !recs || !out || n < 1) return fail(QLM_EINVAL, "reduce_records: bad arguments");
     int rc = check_dev(ctx);
     if (rc) return rc;
@@ -576,6 +649,7 @@ int qlm_reduce_records(qlm_ctx *ctx, const qlm_record *recs, int32_t n, qlm_reco
 int qlm_decode(qlm_ctx *ctx, const qlm_candidates *cand, int32_t *queue_of_group,
                int32_t *pos_of_group, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_decode");
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -588,6 +662,7 @@ int qlm_decode(qlm_ctx *ctx, const qlm_candidates *cand, int32_t *queue_of_group
 
 int qlm_rows(qlm_ctx *ctx, const qlm_candidates *cand, uint16_t *rows_out, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_rows");
     if (!ctx || !rows_out) return fail(QLM_EINVAL, "ctx or rows_out is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -600,6 +675,7 @@ int qlm_rows(qlm_ctx *ctx, const qlm_candidates *cand, uint16_t *rows_out, void 
 int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best *out,
                       int32_t *queue_of_group, int32_t *pos_of_group, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_best_ordering");
     if (!ctx || !out) return fail(QLM_EINVAL, "ctx or out is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -679,6 +755,7 @@ int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
                        float *viol, float *s1, float *s2, int32_t *n_over, qlm_record *rec,
                        void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_score_estimate");
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -702,6 +779,7 @@ int qlm_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *wt_mean,
 int qlm_mc_sample(qlm_ctx *ctx, uint64_t mc_seed, int64_t trial_first, int64_t trial_count,
                   void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_mc_sample");
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_dev(ctx);
     if (rc) return rc;
@@ -732,6 +810,7 @@ int qlm_mc_sample(qlm_ctx *ctx, uint64_t mc_seed, int64_t trial_first, int64_t t
 int qlm_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count, uint32_t *counts,
                  void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_mc_count");
     if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -761,6 +840,7 @@ int qlm_mc_estimate(qlm_ctx *ctx, const qlm_candidates *cand, uint64_t mc_seed,
 
 int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_check_rows");
     if (!ctx || !n_bad) return fail(QLM_EINVAL, "ctx or n_bad is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -779,6 +859,7 @@ int qlm_check_rows(qlm_ctx *ctx, const qlm_candidates *cand, int64_t *n_bad, voi
 int qlm_adopt_best(qlm_ctx *ctx, const qlm_candidates *cand, const qlm_record *rec,
                    qlm_record *incumbent, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_adopt_best");
     if (!ctx || !rec || !incumbent) return fail(QLM_EINVAL, "ctx, rec or incumbent is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -790,6 +871,7 @@ int qlm_adopt_best(qlm_ctx *ctx, const qlm_candidates *cand, const qlm_record *r
 int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves, int64_t per_iter,
                      int32_t iters, uint64_t seed, qlm_record *incumbent, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_local_search");
     if (!ctx || !row || !incumbent) return fail(QLM_EINVAL, "ctx, row or incumbent is NULL");
     if (moves < 1 || moves > QLM_MAX_MOVES)
         return fail(QLM_EINVAL, "moves=%d must lie in [1, %d]", moves, QLM_MAX_MOVES);
@@ -799,53 +881,69 @@ int qlm_local_search(qlm_ctx *ctx, void *row, int32_t token_bytes, int32_t moves
     int rc = check_dev(ctx);
     if (rc) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int T = ctx->dm.T;
-    // score the start row (EXPLICIT, one candidate) into the incumbent record
-    qlm_candidates ex;
-    memset(&ex, 0, sizeof ex);
-    ex.kind = QLM_CAND_EXPLICIT;
-    ex.token_bytes = token_bytes;
-    ex.rows = row;
-    ex.stride = (((int64_t)T * token_bytes) + 15) / 16 * 16;
-    ex.count = 1;
-    if ((rc = check_cand(ctx, &ex))) return rc;
-    ScanParams p0 = base_params(ctx, &ex);
-    p0.out_rec = incumbent;
-    cudaError_t e = launch_any_scan(p0, st);
-    if (e == cudaSuccess)             // index -1: the start row is the incumbent
-        e = cudaMemsetAsync(&incumbent->index, 0xFF, sizeof(int64_t), st);
-    if (e != cudaSuccess) return cuda_fail(e, "local search: start row");
-    qlm_candidates nb = ex;
-    nb.kind = QLM_CAND_NEIGHBOR;
-    nb.stride = 0;
-    nb.seed = seed;
-    nb.moves = moves;
-    nb.count = per_iter;
-    // with a communicator, rank r scores its contiguous shard of every
-    // iteration and the global winner is adopted everywhere
-    int64_t sh_first = 0, sh_count = per_iter;
-    if (ctx->comm) shard(per_iter, comm_rank(ctx->comm), comm_world(ctx->comm), sh_first, sh_count);
-    for (int32_t it = 0; it < iters; ++it) {
-        nb.first = (int64_t)it * per_iter + sh_first;
-        nb.count = sh_count;
-        if ((rc = check_cand(ctx, &nb))) return rc;
-        if (sh_count > 0) {
-            ScanParams p = base_params(ctx, &nb);
-            p.out_rec = ctx->d_ls_rec;
-            if ((e = launch_any_scan(p, st)) != cudaSuccess) return cuda_fail(e, "local search: scores");
-        } else if ((e = cudaMemsetAsync(ctx->d_ls_rec, 0xFF, sizeof(qlm_record), st)) != cudaSuccess) {
-            return cuda_fail(e, "local search: empty shard");
-        }
-        if ((rc = global_record(ctx, ctx->d_ls_rec, st))) return rc;
-        if ((e = launch_adopt(ctx->dm, to_cand(&nb), ctx->d_ls_rec, incumbent, st)) != cudaSuccess)
-            return cuda_fail(e, "local search: adopt");
+    // the search is 2 * iters + 2 short launches: they are captured once into
+    // a CUDA graph (updated in place on later calls of the same shape) and
+    // launched as one unit, so the launches do not pace it.  The legacy
+    // default stream cannot capture: a blocking context stream stands in for
+    // it (ordered with the legacy stream both ways)
+    if (!st && iters >= 2 && !override_on(QLM_OVERRIDE_NO_GRAPH) && !ctx->aux &&
+        cudaStreamCreateWithFlags(&ctx->aux, cudaStreamDefault) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->aux = nullptr;
     }
-    return QLM_OK;
+    cudaStream_t cst = st ? st : ctx->aux;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cst && cudaStreamIsCapturing(cst, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        cs = cudaStreamCaptureStatusActive;                   // unknown: do not nest
+    }
+    const bool graph = cst && iters >= 2 && cs == cudaStreamCaptureStatusNone &&
+                       !override_on(QLM_OVERRIDE_NO_GRAPH);
+    if (!graph) return enqueue_search(ctx, row, token_bytes, moves, per_iter, iters, seed, incumbent, st);
+    // the same call again (same row buffer, record, shape, seed and stream):
+    // replay the instantiated graph without capturing
+    const std::vector<int64_t> sig = {(int64_t)(uintptr_t)row, token_bytes, moves, per_iter, iters,
+                                      (int64_t)seed, (int64_t)(uintptr_t)incumbent, (int64_t)(uintptr_t)cst,
+                                      (int64_t)ctx->dm.G, (int64_t)(uintptr_t)ctx->comm};
+    cudaError_t e;
+    if (ctx->ls_exec && sig == ctx->ls_sig) {
+        e = cudaGraphLaunch(ctx->ls_exec, cst);
+        return e == cudaSuccess ? QLM_OK : cuda_fail(e, "local search: graph launch");
+    }
+    e = cudaStreamBeginCapture(cst, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(e, "local search: begin capture");
+    rc = enqueue_search(ctx, row, token_bytes, moves, per_iter, iters, seed, incumbent, cst);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(cst, &g);
+    if (rc || e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        return rc ? rc : cuda_fail(e, "local search: end capture");
+    }
+    if (ctx->ls_exec) {
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(ctx->ls_exec, g, &info) != cudaSuccess) {   // another shape: rebuild
+            cudaGetLastError();
+            cudaGraphExecDestroy(ctx->ls_exec);
+            ctx->ls_exec = nullptr;
+        }
+    }
+    if (!ctx->ls_exec && (e = cudaGraphInstantiate(&ctx->ls_exec, g, 0)) != cudaSuccess) {
+        ctx->ls_exec = nullptr;
+        cudaGraphDestroy(g);
+        return cuda_fail(e, "local search: instantiate");
+    }
+    cudaGraphDestroy(g);
+    ctx->ls_sig = sig;
+    qlog(1, "local search: CUDA graph of %d iterations x %lld candidates", iters, (long long)per_iter);
+    e = cudaGraphLaunch(ctx->ls_exec, cst);
+    return e == cudaSuccess ? QLM_OK : cuda_fail(e, "local search: graph launch");
 }
 
 int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac, float *s1_req,
                            void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_request_violations");
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_cand(ctx, cand);
     if (rc || (rc = check_dev(ctx))) return rc;
@@ -862,6 +960,7 @@ int qlm_request_violations(qlm_ctx *ctx, const qlm_candidates *cand, float *frac
 
 int qlm_set_tiers(qlm_ctx *ctx, const qlm_tiers *tiers) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_set_tiers");
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     int rc = check_dev(ctx);
     if (rc) return rc;
@@ -914,6 +1013,7 @@ int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *w
                               float *wt_std, float *viol, float *s1, float *s2, int32_t *n_over,
                               qlm_record *rec, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_tiered_score_estimate");
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     if (!ctx->has_tiers) return fail(QLM_EINVAL, "no tier tables: call qlm_set_tiers first");
     int rc = check_cand(ctx, cand);
@@ -944,6 +1044,7 @@ int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k_per_mod
                     int32_t max_iter, int32_t *label_of, int32_t *group_of, qlm_group *groups,
                     int32_t group_cap, int32_t *n_groups, int32_t *iters, int32_t device, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_form_groups");
     if (!req || !k_per_model || !n_groups)
         return fail(QLM_EINVAL, "req, k_per_model and n_groups must be non-NULL");
     if (req->n < 1 || req->n >= (1 << 28)) return fail(QLM_EINVAL, "req.n=%d not in [1, 2^28)", req->n);
@@ -979,6 +1080,7 @@ int qlm_form_groups(const qlm_requests *req, int32_t M, const int32_t *k_per_mod
 int qlm_tiered_mc_count(qlm_ctx *ctx, const qlm_candidates *cand, int64_t trial_count,
                         uint32_t *counts, void *stream) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_tiered_mc_count");
     if (!ctx || !counts) return fail(QLM_EINVAL, "ctx or counts is NULL");
     if (!ctx->has_tiers) return fail(QLM_EINVAL, "no tier tables: call qlm_set_tiers first");
     int rc = check_cand(ctx, cand);
@@ -1011,6 +1113,7 @@ int qlm_comm_unique_id(uint8_t id[QLM_COMM_ID_BYTES]) {
 
 int qlm_comm_attach(qlm_ctx *ctx, const uint8_t id[QLM_COMM_ID_BYTES], int32_t rank, int32_t world) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_comm_attach");
     if (!ctx || !id) return fail(QLM_EINVAL, "ctx or id is NULL");
     if (world < 1 || rank < 0 || rank >= world)
         return fail(QLM_EINVAL, "rank=%d, world=%d: need 0 <= rank < world", rank, world);
@@ -1037,11 +1140,17 @@ int qlm_comm_attach(qlm_ctx *ctx, const uint8_t id[QLM_COMM_ID_BYTES], int32_t r
 
 int qlm_comm_detach(qlm_ctx *ctx) {
     DevGuard dg_;
+    NvtxRange nv_("qlm_comm_detach");
     if (!ctx) return fail(QLM_EINVAL, "ctx is NULL");
     if (!ctx->comm) return QLM_OK;
     int rc = check_dev(ctx);
     if (rc) return rc;
     cudaDeviceSynchronize();
+    if (ctx->ls_exec) {                       // a captured search may hold the communicator's calls
+        cudaGraphExecDestroy(ctx->ls_exec);
+        ctx->ls_exec = nullptr;
+        ctx->ls_sig.clear();
+    }
     comm_destroy(ctx->comm);
     ctx->comm = nullptr;
     cudaFree(ctx->d_comm_recs);

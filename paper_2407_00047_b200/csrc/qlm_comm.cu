@@ -14,7 +14,10 @@
 #include <mutex>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "qlm_comm.h"
+#include "qlm_launch.h"
 
 namespace qlm {
 
@@ -114,15 +117,27 @@ int comm_world(const Comm *c) { return c ? c->world : 1; }
 
 bool comm_allgather_bytes(Comm *c, const void *send, void *recv, size_t bytes, cudaStream_t st,
                           std::string &err) {
-    return nccl_ok(api().AllGather(send, recv, bytes, ncclUint8, c->c, st), "ncclAllGather", err);
+    nvtxRangePushA("qlm_nccl_allgather");
+    qlog(1, "ncclAllGather %zu B x %d ranks", bytes, c->world);
+    const bool ok = nccl_ok(api().AllGather(send, recv, bytes, ncclUint8, c->c, st), "ncclAllGather", err);
+    nvtxRangePop();
+    return ok;
 }
 
 bool comm_allreduce_sum_u32(Comm *c, uint32_t *buf, size_t n, cudaStream_t st, std::string &err) {
-    return nccl_ok(api().AllReduce(buf, buf, n, ncclUint32, ncclSum, c->c, st), "ncclAllReduce(sum)", err);
+    nvtxRangePushA("qlm_nccl_allreduce_sum");
+    qlog(1, "ncclAllReduce(sum, u32) n=%zu", n);
+    const bool ok = nccl_ok(api().AllReduce(buf, buf, n, ncclUint32, ncclSum, c->c, st), "ncclAllReduce(sum)", err);
+    nvtxRangePop();
+    return ok;
 }
 
 bool comm_allreduce_max_i32(Comm *c, int32_t *buf, size_t n, cudaStream_t st, std::string &err) {
-    return nccl_ok(api().AllReduce(buf, buf, n, ncclInt32, ncclMax, c->c, st), "ncclAllReduce(max)", err);
+    nvtxRangePushA("qlm_nccl_allreduce_max");
+    qlog(1, "ncclAllReduce(max, i32) n=%zu", n);
+    const bool ok = nccl_ok(api().AllReduce(buf, buf, n, ncclInt32, ncclMax, c->c, st), "ncclAllReduce(max)", err);
+    nvtxRangePop();
+    return ok;
 }
 
 int comm_nccl_version() {

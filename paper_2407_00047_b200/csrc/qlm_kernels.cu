@@ -11,6 +11,7 @@
 //   mc_sample_kernel     a10: Philox sampling of per-group output tokens
 //   mc_count_kernel      a11: per-trial Eq. 10 walk + violation counts
 #include <atomic>
+#include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -786,6 +787,21 @@ int env_cached(const char *name, int dflt) {
     return r;
 }
 
+int log_level() {
+    static const int lvl = env_cached("QLM_LOG", 0);
+    return lvl;
+}
+
+void qlog(int level, const char *fmt, ...) {
+    if (log_level() < level) return;
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    fprintf(stderr, "[qlm] %s\n", buf);
+}
+
 static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 static int env_int(const char *name, int dflt) { return env_cached(name, dflt); }
@@ -887,6 +903,8 @@ static cudaError_t launch_scan_t(ScanParams p, cudaStream_t st) {
     if (grid > maxg) grid = maxg;
     if (grid > p.max_blocks) grid = p.max_blocks;
     if (grid < 1) grid = 1;
+    qlog(1, "scan_kernel<kind=%d,tok=%zu,out=%d,score=%d> count=%lld grid=%lld block=%d smem=%zu",
+         KIND, sizeof(TOK), OUT, (int)SCORE, (long long)p.cd.count, (long long)grid, best_blk, best_smem);
     kern<<<(unsigned)grid, best_blk, best_smem, st>>>(p);
     ++g_launches;
     return cudaGetLastError();

@@ -48,6 +48,11 @@ extern std::atomic<int64_t> g_override_ilv_cap;
 inline bool override_on(uint32_t bit) { return (g_override_flags.load(std::memory_order_relaxed) & bit) != 0; }
 int sm_count();                                 // of the current device (cached per device)
 int env_cached(const char *name, int dflt);     // tuning/test overrides, read once per process
+// Host logging (QLM_LOG=1: entry points and the kernel each call launches,
+// with its grid and shared memory; QLM_LOG=2 adds per-launch argument detail),
+// to stderr with a "[qlm]" prefix.  Off by default; read once per process.
+int log_level();
+void qlog(int level, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
 
 cudaError_t launch_build(const Dims &dm, const qlm_group *g, const qlm_queue *q,
                          const double *theta, const double *prefill, const double *eps,

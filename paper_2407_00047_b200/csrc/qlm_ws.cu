@@ -606,6 +606,9 @@ static cudaError_t launch_ws_rs(WsParams &w, size_t smem, int W, cudaStream_t st
     if (grid > need) grid = need;
     if (grid > w.p.max_blocks) grid = w.p.max_blocks;
     if (grid < 1) grid = 1;
+    qlog(1, "ws_kernel<kind=%d,tok=%zu,score=%d,rs=%d,tier=%d> count=%lld pairs=%d grid=%lld smem=%zu tma=%d",
+         KIND, sizeof(TOK), (int)SCORE, RS, (int)TIER, (long long)w.p.cd.count, W, (long long)grid, smem,
+         w.use_tma);
     kern<<<(unsigned)grid, w.spread ? 512 : 64 * W, smem, st>>>(w);
     ++g_launches;
     return cudaGetLastError();

@@ -730,6 +730,8 @@ static cudaError_t launch_t(const ScanParams &p0, cudaStream_t st) {
     if (grid > need) grid = need;
     if (grid > p0.max_blocks) grid = p0.max_blocks;
     if (grid < 1) grid = 1;
+    qlog(1, "ws2_kernel<kind=%d,GS=%d,score=%d> count=%lld pairs=%d grid=%lld smem=%zu tma=%d", KIND, GS,
+         SCORE, (long long)p0.cd.count, W, (long long)grid, smem, w.use_tma);
     kern<<<(unsigned)grid, (WS2_SPREAD && W == 6) ? 512 : 64 * W, smem, st>>>(w);
     ++g_launches;
     return cudaGetLastError();

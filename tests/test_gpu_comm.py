@@ -93,3 +93,24 @@ def test_local_search_sharded_by_the_library():
     ba, ia = a.local_search(start, moves=2, per_iter=4096, iters=6, seed=11)
     bb, ib = b.local_search(start, moves=2, per_iter=4096, iters=6, seed=11)
     assert torch.equal(ba, bb) and torch.equal(ia, ib)
+
+
+def test_local_search_graph_equals_direct_launches():
+    # qlm_local_search captures its launches into a CUDA graph on a real
+    # stream; the direct launches (override) give the same row and record,
+    # and a second call (graph updated in place, new seed) matches too
+    from paper_2407_00047_b200 import RwtEstimator, kernel_overrides
+    p = make_config("C3")
+    e = RwtEstimator(p, device=0)
+    start = np.arange(p.T)
+    s = torch.cuda.Stream()
+    for stream in (s, torch.cuda.default_stream()):     # a side stream; the legacy default stream
+      with torch.cuda.stream(stream):
+        for seed in (5, 6):
+            kernel_overrides()
+            g_row, g_inc = e.local_search(start, moves=2, per_iter=8192, iters=12, seed=seed)
+            kernel_overrides(no_graph=True)
+            d_row, d_inc = e.local_search(start, moves=2, per_iter=8192, iters=12, seed=seed)
+            kernel_overrides()
+            torch.cuda.synchronize()
+            assert torch.equal(g_row, d_row) and torch.equal(g_inc, d_inc)

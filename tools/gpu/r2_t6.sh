@@ -1,0 +1,3 @@
+python tools/kernel_suite.py > gpurun_out/suite.json 2> gpurun_out/suite.err
+grep "Error\|error" gpurun_out/suite.err | tail -3
+python -c "import json; [print(x['config'], x['name'][:60], '%.4g'%x['value'], '%.4f'%x['ms']) for x in json.load(open('gpurun_out/suite.json'))]"

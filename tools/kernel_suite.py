@@ -107,6 +107,36 @@ def items():
                 r"wide_kernel|fy_rows_kernel|scan_kernel"
         return setup
 
+    def c2_step(graph):
+        def setup():
+            p = make_config("C2")
+            e = RwtEstimator(p)
+            n = 100_000
+            cand = e.random(0, n, seed=1)
+            out = {k: torch.empty((p.G, n), device="cuda") for k in ("wt", "sd", "v")}
+            rec = torch.empty(2, dtype=torch.int64, device="cuda")
+
+            def step():
+                e.score_estimate(cand, out=out, scores=False, rec=rec)
+                e.decode(e.from_record(rec, seed=1))
+            if not graph:
+                return step, n, "orderings/s", n * 12 * p.G, r"ws2_kernel<1, 32|row_warp_kernel"
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                step()                                   # warm-up (opt-ins, tensor maps)
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            keep = (e, cand, out, rec)                   # the graph replays into these: keep them alive
+
+            def replay():
+                g.replay()
+                return keep
+            return replay, n, "orderings/s", n * 12 * p.G, r"ws2_kernel<1, 32|row_warp_kernel"
+        return setup
+
     def c3_search():
         p = make_config("C3")
         e = RwtEstimator(p)
@@ -126,6 +156,8 @@ def items():
         ("tiered_score_estimate RANDOM bulk + argmin", "C5h", bulk("C5h", 100_000, tiered=True)),
         ("tiered_score_estimate RANDOM bulk + argmin (ws kernel, TIER)", "C3", bulk("C3", 1_000_000, tiered=True)),
         ("local_search 64 x 65536 NEIGHBOR (2 moves)", "C3", c3_search),
+        ("step: score_estimate 1e5 + winner decode, direct launches", "C2", c2_step(False)),
+        ("step: score_estimate 1e5 + winner decode, CUDA graph replay", "C2", c2_step(True)),
     ]
 
 
@@ -143,6 +175,7 @@ def run(reps=20, hbm_peak=None, clk_mhz=1965.0, once=False):
     counts = _ncu_counts()
     ipeak = 148 * 4 * clk_mhz * 1e6
     for name, cfg, setup in items():
+        print(f"# {cfg} {name}", file=sys.stderr, flush=True)
         fn, units, unit, nbytes, kre = setup()
         if once:
             fn()
@@ -232,6 +265,8 @@ def items_meta():
         ("tiered_score_estimate RANDOM bulk + argmin", "C5h", r"tier_warp_kernel|tier_kernel|big_kernel"),
         ("tiered_score_estimate RANDOM bulk + argmin (ws kernel, TIER)", "C3", r"ws_kernel<1, unsigned char, 1, \d, 1>"),
         ("local_search 64 x 65536 NEIGHBOR (2 moves)", "C3", r"scan_kernel<[03], unsigned char|adopt_kernel"),
+        ("step: score_estimate 1e5 + winner decode, direct launches", "C2", r"ws2_kernel<1, 32|row_warp_kernel"),
+        ("step: score_estimate 1e5 + winner decode, CUDA graph replay", "C2", r"ws2_kernel<1, 32|row_warp_kernel"),
     ]
 
 
