@@ -1035,6 +1035,7 @@ int qlm_tiered_score_estimate(qlm_ctx *ctx, const qlm_candidates *cand, float *w
     p.t_mem = reinterpret_cast<const int32_t *>(t);
     p.t_cap = reinterpret_cast<const int32_t *>(t + o_cap);
     p.t_load = reinterpret_cast<const double *>(t + o_load);
+    attach_ilv(ctx, p);                                  // large-T RANDOM: two-phase row chunks
     cudaError_t e = launch_tier(p, st);
     if (e != cudaSuccess) return cuda_fail(e, "tier kernel");
     return rec ? global_record(ctx, rec, st) : QLM_OK;

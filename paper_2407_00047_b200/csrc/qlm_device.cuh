@@ -41,6 +41,10 @@ struct Tables {             // device pointers, one allocation
     double *den;            // [1] sum_i n_i
 };
 
+// Internal candidate kind: rows materialised word-interleaved by fy_rows_kernel
+// (word w of chunk-local candidate l at rows[(w * stride + l) * 4]).
+constexpr int KIND_ILV = 7;
+
 struct Cand {               // device view of qlm_candidates
     int kind, tb;
     const uint8_t *rows;
@@ -466,6 +470,13 @@ __device__ __forceinline__ void warp_gen_row(const Cand &cd, int T, uint64_t c, 
                 ti = (j == i + 1) ? ti : nx;
                 j = jn;
             }
+        }
+    } else if (cd.kind == KIND_ILV) {                     // rows made by fy_rows_kernel (u16 pairs)
+        const uint32_t *r32 = reinterpret_cast<const uint32_t *>(cd.rows);
+        for (int w = lane; w < (T + 1) / 2; w += 32) {
+            const uint32_t v = __ldg(r32 + (size_t)w * cd.stride + loc);
+            srow[2 * w] = (uint16_t)v;
+            if (2 * w + 1 < T) srow[2 * w + 1] = (uint16_t)(v >> 16);
         }
     } else if (cd.kind == QLM_CAND_ENUM) {
         if (lane == 0) {

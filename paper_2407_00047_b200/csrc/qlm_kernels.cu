@@ -392,8 +392,40 @@ __global__ void __launch_bounds__(32) fy_rows_kernel(Cand cd, int T, uint32_t *o
     uint32_t raw1 = ld16(1), rj = ld16(j);
     uint32_t fin = 0;
     uint32_t *op = o;                                  // word (i >> 1) of this lane's row
-    for (int i0 = 0; i0 < T - 1; i0 += 4) {
-        // the next Philox block is independent of this one's steps: issue it first
+    // one step i: forward the pending values, store row[j_i] = row[i], pack the
+    // final row[i] and advance the two-deep pipeline (jn = j_{i+1}, raw2 =
+    // mem[i+2] and rjn = mem[j_{i+1}] were loaded before this step's store)
+    auto step = [&](int i, int jn, uint32_t raw2, uint32_t rjn) {
+        const uint32_t tj = (jm == j) ? t1m : rj;              // value at j_i before step i
+        st16(j, t0);                                           // row[j_i] = row[i]
+        if (i & 1) {
+            fin |= tj << 16;
+            if (act) __stcs(op, fin);
+            op += ld;
+        } else {
+            fin = tj;
+        }
+        // value at position i+1 before step i+1 (raw1 misses stores i-1 and i)
+        const uint32_t t1 = (j == i + 1) ? t0 : ((jm == i + 1) ? t1m : raw1);
+        t1m = t0; jm = j;
+        t0 = t1; j = jn;
+        raw1 = raw2; rj = rjn;
+    };
+    int i0 = 0;
+    // main body: whole Philox blocks whose steps all have i + 2 < T (no bounds
+    // checks); the next block is independent of this one's steps: issue it first
+    for (; i0 + 4 <= T - 3; i0 += 4) {
+        const uint4 wn = philox10(make_uint4((uint32_t)((i0 >> 2) + 1), clo, chi, kRowTag), key);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k;
+            const int jn = k < 3 ? jof(wd, k + 1, i + 1) : jof(wn, 0, i + 1);
+            step(i, jn, ld16(i + 2), ld16(jn));
+        }
+        wd = wn;
+    }
+    // tail: the last steps, with bounds
+    for (; i0 < T - 1; i0 += 4) {
         const uint4 wn = i0 + 4 < T - 1 ? philox10(make_uint4((uint32_t)((i0 >> 2) + 1), clo, chi, kRowTag), key)
                                         : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
@@ -401,23 +433,8 @@ __global__ void __launch_bounds__(32) fy_rows_kernel(Cand cd, int T, uint32_t *o
             const int i = i0 + k;
             if (i >= T - 1) break;
             const int jn = i + 1 < T - 1 ? (k < 3 ? jof(wd, k + 1, i + 1) : jof(wn, 0, i + 1)) : 0;
-            // loads for the next steps, issued before this step's store
             const uint32_t raw2 = i + 2 < T ? ld16(i + 2) : 0u;   // mem[i+2]: misses stores i, i+1
-            const uint32_t rjn = ld16(jn);                         // mem[j_{i+1}]: misses store i
-            const uint32_t tj = (jm == j) ? t1m : rj;              // value at j_i before step i
-            st16(j, t0);                                           // row[j_i] = row[i]
-            if (k & 1) {
-                fin |= tj << 16;
-                if (act) __stcs(op, fin);
-                op += ld;
-            } else {
-                fin = tj;
-            }
-            // value at position i+1 before step i+1 (raw1 misses stores i-1 and i)
-            const uint32_t t1 = (j == i + 1) ? t0 : ((jm == i + 1) ? t1m : raw1);
-            t1m = t0; jm = j;
-            t0 = t1; j = jn;
-            raw1 = raw2; rj = rjn;
+            step(i, jn, raw2, ld16(jn));                           // mem[j_{i+1}]: misses store i
         }
         wd = wn;
     }
@@ -946,19 +963,25 @@ static bool wide_first(const ScanParams &p) {
 // fy_rows_kernel (cheap, latency-bound) and scored by the scan kernel reading
 // them with coalesced loads at full occupancy.  Argmin is carried across
 // chunks in chunk_recs[0].
-static cudaError_t launch_two_phase(const ScanParams &p0, cudaStream_t st) {
-    const int64_t count = p0.cd.count, cap = p0.ilv_cap;
-    const size_t fy_smem = (size_t)p0.dm.T * 32 * 2;
+cudaError_t launch_fy_rows(const Cand &g, int T, uint32_t *out, int64_t n, cudaStream_t st) {
+    const size_t fy_smem = (size_t)T * 32 * 2;
     cudaError_t e = prep(fy_rows_kernel, fy_smem);
     if (e != cudaSuccess) return e;
+    qlog(1, "fy_rows_kernel T=%d rows=%lld", T, (long long)n);
+    fy_rows_kernel<<<(unsigned)((n + 31) / 32), 32, fy_smem, st>>>(g, T, out, n);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+static cudaError_t launch_two_phase(const ScanParams &p0, cudaStream_t st) {
+    const int64_t count = p0.cd.count, cap = p0.ilv_cap;
+    cudaError_t e;
     for (int64_t c0 = 0; c0 < count; c0 += cap) {
         const int64_t n = count - c0 < cap ? count - c0 : cap;
         Cand g = p0.cd;
         g.first = p0.cd.first + c0;
         g.count = n;
-        fy_rows_kernel<<<(unsigned)((n + 31) / 32), 32, fy_smem, st>>>(g, p0.dm.T, p0.ilv, n);
-        ++g_launches;
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = launch_fy_rows(g, p0.dm.T, p0.ilv, n, st)) != cudaSuccess) return e;
         ScanParams p = p0;
         p.cd.kind = KIND_ILV;
         p.cd.tb = 2;

@@ -37,9 +37,6 @@ struct ScanParams {
     int slo_hi_only;           // every slo_s has a zero low 32-bit word (qlm_ws2.cu records)
 };
 
-// Internal candidate kind: rows materialised word-interleaved by fy_rows_kernel
-// (word w of chunk-local candidate l at rows[(w * stride + l) * 4]).
-constexpr int KIND_ILV = 7;
 
 extern std::atomic<int64_t> g_launches;
 // qlm_set_kernel_overrides (tests: compare kernel paths on one process)
@@ -69,6 +66,9 @@ cudaError_t launch_big_tier(const ScanParams &p, cudaStream_t st);  // same, two
 cudaError_t launch_req(const ScanParams &p, const qlm_group *groups, float *frac, float *s1r,
                        cudaStream_t st);                            // request-level (R19)
 cudaError_t launch_tier(const ScanParams &p, cudaStream_t st);     // two-tier swapping (R20)
+// large-T RANDOM rows of candidates [g.first, g.first + n), word-interleaved
+// into `out` (word w of candidate l at out[w * n + l]); fy_rows_kernel
+cudaError_t launch_fy_rows(const Cand &g, int T, uint32_t *out, int64_t n, cudaStream_t st);
 cudaError_t launch_form_groups(int n, int dims, int M, const int32_t *k_host, int limit, int max_iter,
                                const int32_t *model, const double *slo, const int32_t *out,
                                const int32_t *feat, int32_t *label, int32_t *group_of,

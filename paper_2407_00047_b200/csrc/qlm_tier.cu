@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, cons
     const float alpha = p.alpha;
     const double den = *p.tb.den;
     float *const gout[3] = {p.wt, p.sd, p.vo};
+    const int64_t ldo = p.ld_out ? p.ld_out : count;           // chunked launches write into the full range
     const bool bulk = p.wt || p.sd || p.vo;
     uint64_t bkey = ~0ull;
     int64_t bidx = -1;
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, cons
             for (int i = tid; i < 3 * G * kTwWarps; i += 256) {
                 const int r = i >> 3, k = i & 7;
                 const int a = r / G, g = r - a * G;
-                if (gout[a] && k < nv) gout[a][(int64_t)g * count + c0 + k] = tile[((size_t)a * G + g) * kTwPad + k];
+                if (gout[a] && k < nv) gout[a][(int64_t)g * ldo + c0 + k] = tile[((size_t)a * G + g) * kTwPad + k];
             }
             __syncthreads();
         }
@@ -445,9 +446,52 @@ static cudaError_t launch_tier_warp(const ScanParams &p, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Large-T RANDOM under tiers: rows generated per chunk by fy_rows_kernel (one
+// lane per row, 32 rows per warp) instead of one lane of the scoring warp, then
+// scored by the lane-per-queue kernel reading them; argmin carried across
+// chunks like launch_two_phase.
+static cudaError_t launch_tier_two_phase(const ScanParams &p0, cudaStream_t st) {
+    const int64_t count = p0.cd.count, cap = p0.ilv_cap;
+    cudaError_t e;
+    for (int64_t c0 = 0; c0 < count; c0 += cap) {
+        const int64_t n = count - c0 < cap ? count - c0 : cap;
+        Cand g = p0.cd;
+        g.first = p0.cd.first + c0;
+        g.count = n;
+        if ((e = launch_fy_rows(g, p0.dm.T, p0.ilv, n, st)) != cudaSuccess) return e;
+        ScanParams p = p0;
+        p.cd.kind = KIND_ILV;
+        p.cd.tb = 2;
+        p.cd.rows = reinterpret_cast<const uint8_t *>(p0.ilv);
+        p.cd.stride = n;
+        p.cd.first = g.first;
+        p.cd.count = n;
+        p.ld_out = count;
+        if (p.s1) p.s1 += c0;
+        if (p.s2) p.s2 += c0;
+        if (p.n_over) p.n_over += c0;
+        if (p.wt) p.wt += c0;
+        if (p.sd) p.sd += c0;
+        if (p.vo) p.vo += c0;
+        if (p0.out_rec) p.out_rec = p0.chunk_recs + (c0 ? 1 : 0);
+        if ((e = launch_tier_warp(p, st)) != cudaSuccess) return e;
+        if (p0.out_rec && c0) {
+            if ((e = launch_reduce_records(p0.chunk_recs, 2, p0.chunk_recs, st)) != cudaSuccess) return e;
+        }
+    }
+    return p0.out_rec ? launch_reduce_records(p0.chunk_recs, 1, p0.out_rec, st) : cudaSuccess;
+}
+
 cudaError_t launch_tier(const ScanParams &p, cudaStream_t st) {
     const cudaError_t ws = launch_ws_tier(p, st);            // warp-specialised fast path
     if (ws != cudaErrorNotSupported) return ws;
+    if (p.dm.G > 256 && p.cd.kind == QLM_CAND_RANDOM && p.dm.T > 256 && p.ilv && p.ilv_cap >= 32 &&
+        p.chunk_recs && !p.cd.first_from && p.cd.count >= 4096 && !override_on(QLM_OVERRIDE_NO_TIER_WARP) &&
+        !override_on(QLM_OVERRIDE_NO_TWO_PHASE)) {
+        const cudaError_t w = launch_tier_two_phase(p, st);
+        if (w != cudaErrorNotSupported) return w;
+        cudaGetLastError();
+    }
     if (p.dm.G > 256 && !override_on(QLM_OVERRIDE_NO_TIER_WARP)) {   // large G: lane per queue
         const cudaError_t w = launch_tier_warp(p, st);
         if (w != cudaErrorNotSupported) return w;

@@ -146,3 +146,37 @@ def test_calls_restore_the_current_device():
         a = ests[0].best_ordering_async(ests[0].random(0, 8192, seed=1)).cpu()
         b = ests[1].best_ordering_async(ests[1].random(0, 8192, seed=1)).cpu()
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("cap", [0, 4096])
+def test_tiered_large_T_two_phase_equals_direct(cap):
+    # tiered RANDOM scoring with T > 256 and G > 256 generates its rows per chunk
+    # with fy_rows_kernel (two-phase); it must equal the lane-per-queue kernel
+    # generating rows itself bit for bit, across chunks, and match the oracle
+    from paper_2407_00047_b200 import RwtEstimator, kernel_overrides
+    from workloads.synth import make_tiers
+    from tests.parity import check_estimates, check_scores
+    p = make_config("C5h")
+    t = make_tiers(dev_rows=(0, 1))
+    n = 9000
+    res = {}
+    for mode in ("direct", "two_phase"):
+        kernel_overrides(no_two_phase=mode == "direct", ilv_cap=cap)
+        e = RwtEstimator(p, device=0)
+        e.set_tiers(t)
+        cand = e.random(123, n, seed=1)
+        out = {k: torch.empty((p.G, n), device="cuda") for k in ("wt", "sd", "v")}
+        rec = torch.empty(2, dtype=torch.int64, device="cuda")
+        r = e.tiered_score_estimate(cand, out=out, rec=rec)
+        torch.cuda.synchronize()
+        res[mode] = (r, rec.clone())
+        kernel_overrides()
+    (a, ra), (b, rb) = res["direct"], res["two_phase"]
+    for k in ("wt", "sd", "v", "s1", "s2"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(ra, rb)
+    o = O.Oracle(p)
+    lo, cnt = n - 40, 40
+    ref = o.tiered_range(t, O.RANDOM, 123 + lo, cnt, seed=1)
+    check_estimates({k: b[k][:, lo:lo + cnt] for k in ("wt", "sd", "v")}, ref)
+    check_scores(b["s1"][lo:].cpu().numpy(), b["s2"][lo:].cpu().numpy(), ref, p)
