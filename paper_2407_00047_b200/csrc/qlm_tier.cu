@@ -391,11 +391,19 @@ __global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, cons
             __syncthreads();
             const int nv = (int)min((int64_t)kTwWarps, count - c0);
             // 8 consecutive lanes write one row's 8 floats: each store instruction
-            // covers 4 whole 32-B sectors (no partial-sector writes)
-            for (int i = tid; i < 3 * G * kTwWarps; i += 256) {
-                const int r = i >> 3, k = i & 7;
-                const int a = r / G, g = r - a * G;
-                if (gout[a] && k < nv) gout[a][(int64_t)g * ldo + c0 + k] = tile[((size_t)a * G + g) * kTwPad + k];
+            // covers 4 whole 32-B sectors (no partial-sector writes); thread t
+            // takes column t mod 8 of rows t/8, t/8 + 32, ... (no divisions)
+            const int k = tid & 7;
+            if (k < nv) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    float *const base = gout[a];
+                    if (!base) continue;
+                    float *dst = base + c0 + k + (int64_t)(tid >> 3) * ldo;
+                    const float *src = tile + (size_t)a * G * kTwPad + k + (tid >> 3) * kTwPad;
+                    const int64_t dstep = 32 * ldo;
+                    for (int g = tid >> 3; g < G; g += 32, dst += dstep, src += 32 * kTwPad) __stcs(dst, *src);
+                }
             }
             __syncthreads();
         }
