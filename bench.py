@@ -285,14 +285,18 @@ def run_ours(args, rank, world, local_rank):
         ev_s.record(side)
         g = global_best(rec, est.reduce_records, est=est)        # a8 (in the library when attached)
         win = est.from_record(g, seed=CANDIDATE_SEED)
-        qo, po = est.decode(win)                                 # a9
+        if out_host is None:
+            est.decode(win)                                      # a9
+        else:
+            # a9 through the C ABI with the D2H of the step's result: qlm_winner
+            # decodes (and scores) the global record's candidate and copies
+            # (index, S1, S2, n_over, queue/position per group) into the
+            # pinned host buffers on the stream
+            est.winner(win, out_host)
         stream.wait_event(ev_s)
         est.mc_count(win, MC_TRIALS, counts=counts)              # a11
         sum_counts(counts, est=est)                              # a12 (in the library when attached)
-        if out_host is not None:                                 # D2H of the step's result
-            out_host["rec"].copy_(g, non_blocking=True)
-            out_host["qo"].copy_(qo.view(-1), non_blocking=True)
-            out_host["po"].copy_(po.view(-1), non_blocking=True)
+        if out_host is not None:
             out_host["cnt"].copy_(counts.view(-1), non_blocking=True)
         return g
 
@@ -334,7 +338,7 @@ def run_ours(args, rank, world, local_rank):
         g_np = groups_array(p.model, p.n_req, p.slo, p.mu, p.var, p.dist)
         groups_host = torch.from_numpy(g_np.view(np.uint8).copy()).pin_memory()
         def host_out():
-            return {"rec": torch.empty(2, dtype=torch.int64).pin_memory(),
+            return {"best": torch.empty(24, dtype=torch.uint8).pin_memory(),
                     "qo": torch.empty(G, dtype=torch.int32).pin_memory(),
                     "po": torch.empty(G, dtype=torch.int32).pin_memory(),
                     "cnt": torch.empty(G, dtype=torch.int32).pin_memory()}
@@ -356,9 +360,9 @@ def run_ours(args, rank, world, local_rank):
             done[k % 2].record(stream)
             if k > 0:
                 done[(k - 1) % 2].synchronize()
-                _ = int(outs[(k - 1) % 2]["rec"][1])              # the host reads the result
+                _ = RwtEstimator.best_of(outs[(k - 1) % 2]["best"])["index"]   # the host reads the result
         done[(Ke - 1) % 2].synchronize()
-        _ = int(outs[(Ke - 1) % 2]["rec"][1])
+        _ = RwtEstimator.best_of(outs[(Ke - 1) % 2]["best"])["index"]
         x1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([x0.elapsed_time(x1) / Ke], dtype=torch.float64, device=dev)
@@ -368,9 +372,10 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(groups_host.numel()),
                "d2h_bytes_per_step": int(sum(v.numel() * v.element_size() for v in out_host.values())),
                "ms_per_step": te.item(),
-               "note": "per step: pinned H2D of the 64 group records + table rebuild, the whole "
-                       "step, D2H of (record, decoded ordering, MC counts) and a host read of the "
-                       "result; pipelined one step deep (the host reads step k-1 while step k runs)"}
+               "note": "per step: pinned H2D of the 64 group records through qlm_update_groups + "
+                       "table rebuild, the whole step, D2H of the winner (index, S1, S2, n_over, "
+                       "decoded ordering) through qlm_winner plus the MC counts, and a host read of "
+                       "the result; pipelined one step deep (the host reads step k-1 while step k runs)"}
 
     if rank == 0:
         peaks = {}

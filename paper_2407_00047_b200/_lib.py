@@ -104,6 +104,7 @@ SIGNATURES = {
     "qlm_comm_detach": (C.c_int, [_vp]),
     "qlm_comm_info": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "qlm_set_kernel_overrides": (C.c_int, [C.c_uint32, _i64]),
+    "qlm_winner": (C.c_int, [_vp, C.POINTER(Candidates), _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

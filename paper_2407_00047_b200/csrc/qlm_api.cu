@@ -660,6 +660,35 @@ int qlm_decode(qlm_ctx *ctx, const qlm_candidates *cand, int32_t *queue_of_group
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "decode kernel");
 }
 
+int qlm_winner(qlm_ctx *ctx, const qlm_candidates *one, qlm_best *out, int32_t *queue_of_group,
+               int32_t *pos_of_group, void *stream) {
+    DevGuard dg_;
+    NvtxRange nv_("qlm_winner");
+    if (!ctx || !one || !out) return fail(QLM_EINVAL, "ctx, one or out is NULL");
+    if (one->count != 1 || !one->first_from)
+        return fail(QLM_EINVAL, "qlm_winner needs cand.count == 1 and cand.first_from = the device record");
+    int rc = check_cand(ctx, one);
+    if (rc || (rc = check_dev(ctx))) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int G = ctx->dm.G;
+    // the record's candidate scored and decoded on the device (no host sync),
+    // then one D2H copy per result field into the caller's host buffers
+    float *d_s = reinterpret_cast<float *>(ctx->d_rec + 1);
+    int32_t *d_no = reinterpret_cast<int32_t *>(ctx->d_rec + 2);
+    if ((rc = qlm_score_orderings(ctx, one, d_s, d_s + 1, d_no, stream))) return rc;
+    if ((rc = qlm_decode(ctx, one, ctx->d_dec_out, ctx->d_dec_out + G, stream))) return rc;
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(&out->index, &one->first_from->index, sizeof(int64_t), cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpyAsync(&out->s1, d_s, 2 * sizeof(float), cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpyAsync(&out->n_over, d_no, sizeof(int32_t), cudaMemcpyDeviceToHost, st)) ||
+        (queue_of_group && (e = cudaMemcpyAsync(queue_of_group, ctx->d_dec_out, G * sizeof(int32_t),
+                                                cudaMemcpyDeviceToHost, st))) ||
+        (pos_of_group && (e = cudaMemcpyAsync(pos_of_group, ctx->d_dec_out + G, G * sizeof(int32_t),
+                                              cudaMemcpyDeviceToHost, st))))
+        return cuda_fail(e, "winner readback");
+    return QLM_OK;
+}
+
 int qlm_rows(qlm_ctx *ctx, const qlm_candidates *cand, uint16_t *rows_out, void *stream) {
     DevGuard dg_;
     NvtxRange nv_("qlm_rows");

@@ -286,6 +286,21 @@ class RwtEstimator:
         return dict(index=b.index, s1=b.s1, s2=b.s2, n_over=b.n_over, queue_of_group=qo,
                     pos_of_group=po)
 
+    def winner(self, one: Cand, host: dict, stream=None):
+        """qlm_winner: the record's candidate scored and decoded on the stream and
+        copied into host tensors (pinned recommended): host["best"] a uint8[24]
+        qlm_best image, host["qo"] / host["po"] int32[G].  Asynchronous."""
+        L.check(L.lib().qlm_winner(self._h, C.byref(one.c()), host["best"].data_ptr(),
+                                   host["qo"].data_ptr() if "qo" in host else None,
+                                   host["po"].data_ptr() if "po" in host else None,
+                                   self._stream(stream)), "qlm_winner")
+
+    @staticmethod
+    def best_of(best_bytes: torch.Tensor) -> dict:
+        """Decode a host qlm_best image (qlm_winner) into a dict."""
+        b = L.Best.from_buffer_copy(bytes(best_bytes.numpy().tobytes()))
+        return dict(index=b.index, s1=b.s1, s2=b.s2, n_over=b.n_over)
+
     def rwt_estimate(self, cand: Cand, want=("wt", "sd", "v"), out=None, stream=None):
         """Per-(group, candidate) expected wait, its std and violation probability.
 

@@ -114,3 +114,24 @@ def test_local_search_graph_equals_direct_launches():
             kernel_overrides()
             torch.cuda.synchronize()
             assert torch.equal(g_row, d_row) and torch.equal(g_inc, d_inc)
+
+
+def test_winner_reads_the_record_into_host_buffers():
+    # qlm_winner: the record's candidate scored + decoded on the stream, copied
+    # into host buffers -- equal to the synchronous qlm_best_ordering
+    from paper_2407_00047_b200 import RwtEstimator
+    p = make_config("C3")
+    e = RwtEstimator(p, device=0)
+    cand = e.random(0, 50_000, seed=2)
+    rec = e.best_ordering_async(cand)
+    host = {"best": torch.empty(24, dtype=torch.uint8).pin_memory(),
+            "qo": torch.empty(p.G, dtype=torch.int32).pin_memory(),
+            "po": torch.empty(p.G, dtype=torch.int32).pin_memory()}
+    e.winner(e.from_record(rec, seed=2), host)
+    torch.cuda.synchronize()
+    got = RwtEstimator.best_of(host["best"])
+    ref = e.best_ordering(cand)
+    assert got["index"] == ref["index"] and got["s1"] == ref["s1"] and got["s2"] == ref["s2"]
+    assert got["n_over"] == ref["n_over"]
+    assert np.array_equal(host["qo"].numpy(), ref["queue_of_group"])
+    assert np.array_equal(host["po"].numpy(), ref["pos_of_group"])
