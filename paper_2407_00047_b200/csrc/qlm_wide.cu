@@ -99,15 +99,20 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
     const Dims dm = p.dm;
     const int G = dm.G, Q = dm.Q, T = dm.T, M = dm.M;
     // tables (no replication): group records, per-device work, transitions, queues
+    // group records and per-device work replicated 1 << rs times (lane l reads
+    // copy l mod 2^rs: fewer bank conflicts on the random per-lane lookups);
+    // transitions replicated 16 times
+    const int rs = p.rep_shift;
     GRec *sg = reinterpret_cast<GRec *>(smem + p.off_grec);
-    for (int i = tid; i < G; i += 256) sg[i] = p.tb.grec[i];
+    for (int i = tid; i < (G << rs); i += 256) sg[i] = p.tb.grec[i >> rs];
     double2 *sab = reinterpret_cast<double2 *>(smem + p.off_ab);
-    for (int i = tid; i < dm.D * G; i += 256) sab[i] = p.tb.ab[i];
+    for (int i = tid; i < ((dm.D * G) << rs); i += 256) sab[i] = p.tb.ab[i >> rs];
     QRec *sq = reinterpret_cast<QRec *>(smem + p.off_q);
     for (int i = tid; i < Q; i += 256) sq[i] = p.tb.qrec[i];
     double *str = reinterpret_cast<double *>(smem + p.off_tr);
-    for (int i = tid; i < dm.D * 2 * M * M; i += 256) {
-        const int m = i % M, pp = (i / M) % (2 * M), d = i / (2 * M * M);
+    for (int i = tid; i < (dm.D * 2 * M * M) << 4; i += 256) {
+        const int e = i >> 4;
+        const int m = e % M, pp = (e / M) % (2 * M), d = e / (2 * M * M);
         const int from = pp < M ? pp : pp - M;
         const double sw = p.tb.swap[(d * M + from) * M + m];
         const double tl = (pp < M && m != pp) ? p.tb.tail[d * M + pp] : 0.0;
@@ -119,7 +124,7 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
     __syncthreads();
     SlotTables tab;
     tab.sg = sg; tab.sab = sab; tab.str = str; tab.sq = sq;
-    tab.G = G; tab.Q = Q; tab.M = M; tab.rs = 0; tab.rl = 0; tab.trs = 0; tab.trl = 0;
+    tab.G = G; tab.Q = Q; tab.M = M; tab.rs = rs; tab.rl = lane & ((1 << rs) - 1); tab.trs = 4; tab.trl = lane & 15;
 
     const Cand cd = p.cd;
     const int64_t count = cd.count;
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
             int prev_model = 0;
             if (p0 > 0 && p0 < T) {
                 const int tb_ = row[p0 - 1];
-                if (tb_ < G) { fresh = false; prev_model = sg[tb_].model; }
+                if (tb_ < G) { fresh = false; prev_model = sg[tb_ << rs].model; }
             }
             auto enter = [&](ScanState &s) {
                 if (fresh) {
@@ -277,15 +282,18 @@ static size_t a16w(size_t x) { return (x + 15) & ~size_t(15); }
 template <int KIND, bool SCORE>
 static cudaError_t launch_wide_t(ScanParams p, cudaStream_t st) {
     const Dims &dm = p.dm;
-    size_t off = 0;
-    p.off_grec = (int)off; off = a16w(off + (size_t)dm.G * sizeof(GRec));
-    p.off_ab = (int)off;   off = a16w(off + (size_t)dm.D * dm.G * sizeof(double2));
-    p.off_q = (int)off;    off = a16w(off + (size_t)dm.Q * sizeof(QRec));
-    p.off_tr = (int)off;   off = a16w(off + (size_t)dm.D * 2 * dm.M * dm.M * sizeof(double));
-    p.off_scratch = (int)off; off = a16w(off + (size_t)kWideCands * ((dm.T + 7) & ~7) * 2);
-    p.off_stage = (int)off;
-    const bool any_out = p.wt || p.sd || p.vo;
-    if (any_out) off += (size_t)3 * dm.G * kWidePad * 4;
+    auto plan = [&](int rs) {
+        size_t off = 0;
+        p.rep_shift = rs;
+        p.off_grec = (int)off; off = a16w(off + ((size_t)dm.G << rs) * sizeof(GRec));
+        p.off_ab = (int)off;   off = a16w(off + ((size_t)dm.D * dm.G << rs) * sizeof(double2));
+        p.off_q = (int)off;    off = a16w(off + (size_t)dm.Q * sizeof(QRec));
+        p.off_tr = (int)off;   off = a16w(off + ((size_t)dm.D * 2 * dm.M * dm.M << 4) * sizeof(double));
+        p.off_scratch = (int)off; off = a16w(off + (size_t)kWideCands * ((dm.T + 7) & ~7) * 2);
+        p.off_stage = (int)off;
+        if (p.wt || p.sd || p.vo) off += (size_t)3 * dm.G * kWidePad * 4;
+        return off;
+    };
     auto kern = wide_kernel<KIND, SCORE>;
     int optin = 0, dev = 0;
     cudaGetDevice(&dev);
@@ -293,6 +301,15 @@ static cudaError_t launch_wide_t(ScanParams p, cudaStream_t st) {
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
+    // the most replication that fits (env QLM_WIDE_RS pins it for A/B timing)
+    const int env_rs = env_cached("QLM_WIDE_RS", -1);
+    size_t off = 0;
+    int rs = env_rs >= 0 ? env_rs : 0;   // replication measured: no gain (latency-bound), so none by default
+    for (; rs >= 0; --rs) {
+        off = plan(rs);
+        if (off + fa.sharedSizeBytes <= (size_t)optin || env_rs >= 0) break;
+    }
+    if (rs < 0) rs = 0, off = plan(0);
     if (off + fa.sharedSizeBytes > (size_t)optin) return cudaErrorNotSupported;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off)) != cudaSuccess)
         return e;
