@@ -59,6 +59,7 @@ cudaError_t launch_scan(ScanParams p, cudaStream_t st);
 cudaError_t launch_ws(ScanParams p, cudaStream_t st);      // warp-specialised fast path
 cudaError_t launch_ws2(const ScanParams &p, cudaStream_t st);  // same, D = 1 / byte rows (qlm_ws2.cu)
 cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st); // same, two-tier swapping (R20)
+cudaError_t launch_ws2_tier(const ScanParams &p, cudaStream_t st);  // ws2 with R20 (D = 1 / byte rows)
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st);   // ws, else scan
 cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per candidate (large G)
 cudaError_t launch_big(const ScanParams &p, cudaStream_t st);       // very large G: global tables

@@ -672,6 +672,11 @@ static cudaError_t launch_ws_k(ScanParams &p, cudaStream_t st) {
 cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st) {
     if (p.cd.first_from || p.cd.count < 4096 || override_on(QLM_OVERRIDE_NO_WS)) return cudaErrorNotSupported;
     if (!(p.wt || p.sd || p.vo) || p.dm.M > 32) return cudaErrorNotSupported;
+    if (!override_on(QLM_OVERRIDE_NO_WS2)) {
+        const cudaError_t e = launch_ws2_tier(p, st);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
     if ((size_t)3 * (p.dm.G + 1) * 32 * 4 * 2 > 200 * 1024) return cudaErrorNotSupported;
     switch (p.cd.kind) {
     case QLM_CAND_RANDOM:

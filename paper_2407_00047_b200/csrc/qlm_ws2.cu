@@ -43,6 +43,9 @@ namespace ws2 {
 
 constexpr int kRep = 8;      // record replicas: lane l reads replica l & 7
 constexpr int kTrRep = 16;   // transition replicas: lane l reads replica l & 15
+// Two-tier swapping (R20) keeps two transition tables (warm, cold) in the same
+// space with 8 replicas each, and a 16-byte second record half.
+template <bool TIER> __host__ __device__ constexpr int tr_rep() { return TIER ? 8 : kTrRep; }
 #ifndef WS2_PIPE
 #define WS2_PIPE 0
 #endif
@@ -69,8 +72,8 @@ constexpr int kTrRep = 16;   // transition replicas: lane l reads replica l & 15
 #endif
 constexpr int kWordsPerCheck = 2;
 constexpr int kPend = 4 + 4 * kWordsPerCheck;   // deferred-slot FIFO depth per lane
-constexpr int kRecStride = 2 * kRep * 16;
-constexpr int kNeutral = 8;  // neutral records T .. T+7 (row padding, see load_word)   // bytes per token value: [2 halves][8 replicas][16 B]
+constexpr int kRecStride = 2 * kRep * 16;   // bytes per token value: [2 halves][8 replicas][16 B]
+constexpr int kNeutral = 8;  // neutral records T .. T+7 (row padding, see load_word)
 
 struct alignas(64) Params {
     CUtensorMap tmap[3];     // wt, sd, v: fp32 [G][count], box {32, G}
@@ -292,8 +295,18 @@ struct WordData {
     int ix[4], kh[4], sidx[4];
 };
 
+// R20 state of the queue being walked: bit of the model in memory, targets
+// seen / warm, CPU memory taken, the queue's CPU memory (-1 once a target did
+// not fit: later targets are cold, the warm set is a strict prefix)
+struct TierState {
+    uint32_t pbit, seen, warm;
+    int cum, capd;
+};
+
+template <bool TIER>
 __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb, uint32_t rb1, uint32_t tb,
-                                          uint32_t &prow, int &gq, WordData &d) {
+                                          uint32_t cold_off, uint32_t &prow, int &gq, TierState &ts,
+                                          WordData &d) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int tok = (int)__byte_perm(wd, 0u, 0x4440u + k);
@@ -306,18 +319,47 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
             : "=r"(d.ix[k]), "=r"(d.kh[k]), "=r"(d.sidx[k]), "+r"(gq) : "r"(tok), "r"(G));
         const uint32_t ra = (uint32_t)d.ix[k] * kRecStride;
         const float4 r0 = lds128(rb + ra);               // {a, slo hi, n}
-        const float2 r1 = lds64v(rb1 + ra);              // {b, 128 * state}
         d.aw[k] = __hiloint2double(__float_as_int(r0.y), __float_as_int(r0.x));
         d.slo[k] = __hiloint2double(__float_as_int(r0.z), 0);
         d.nf[k] = r0.w;
-        d.b[k] = r1.x;
+        uint32_t xs;
+        if constexpr (TIER) {
+            // {b, transition state, CPU memory (group: its model's; separator:
+            // its queue's), model bit (separator: the resident's)}
+            const float4 r1 = lds128(rb1 + ra);
+            d.b[k] = r1.x;
+            xs = (uint32_t)__float_as_int(r1.y);
+            const int mem = __float_as_int(r1.z);
+            const uint32_t bit = (uint32_t)__float_as_int(r1.w);
+            const bool sep = d.kh[k] == 0;
+            // R20, in the order of qlm_ws.cu's tier walk: the first transition
+            // into a model makes it warm while it fits the CPU memory
+            const bool trn = !sep && bit != ts.pbit;
+            const bool first = trn && !(ts.seen & bit);
+            const int need = ts.cum + mem;
+            const bool fits = need <= ts.capd;
+            ts.seen |= first ? bit : 0u;
+            ts.warm |= (first && fits) ? bit : 0u;
+            ts.cum = (first && fits) ? need : ts.cum;
+            ts.capd = (first && !fits) ? -1 : ts.capd;
+            const bool cold = trn && !(ts.warm & bit);
+            ts.pbit = bit;                                 // separator: its queue's resident
+            ts.capd = sep ? mem : ts.capd;
+            ts.seen = sep ? 0u : ts.seen;
+            ts.warm = sep ? 0u : ts.warm;
+            ts.cum = sep ? 0 : ts.cum;
+            d.tr[k] = lds64f(prow + xs + (cold ? cold_off : 0u));
+        } else {
+            const float2 r1 = lds64v(rb1 + ra);          // {b, 128 * state}
+            d.b[k] = r1.x;
 #if WS2_XNODEP
-        const uint32_t xs = (uint32_t)(tok & 3) * 128u;            // timing experiment: no record dependency
+            xs = (uint32_t)(tok & 3) * 128u;             // timing experiment: no record dependency
 #else
-        const uint32_t xs = (uint32_t)__float_as_int(r1.y);
+            xs = (uint32_t)__float_as_int(r1.y);
 #endif
-        d.tr[k] = lds64f(prow + xs);                               // row of the state before
-        prow = tb + xs * R;                                        // row of this slot's state
+            d.tr[k] = lds64f(prow + xs);                 // row of the state before
+        }
+        prow = tb + xs * R;                              // row of this slot's state
     }
 }
 
@@ -402,7 +444,7 @@ __device__ __forceinline__ void flush(uint32_t pq0, uint32_t rb, uint32_t sb, fl
     a.pq = pq0;
 }
 
-template <int KIND, int GS, int SCORE>
+template <int KIND, int GS, int SCORE, bool TIER>
 __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Params w) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const ScanParams &p = w.p;
@@ -420,41 +462,57 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
     // resident r with nothing running (R4).  A group's state is its model, a
     // separator's the start state of its queue (a declared backlog starts in
     // the resident's model state, R12).
+    constexpr int TRR = tr_rep<TIER>();
+    int summem = 0;
+    if constexpr (TIER)
+        for (int m = 0; m < M; ++m) summem += p.t_mem[m];
     for (int i = tid; i < (T + kNeutral) * kTrRep; i += blockDim.x) {
         const int ix = i / kTrRep, r = i % kTrRep;
         double aw, slo;
         float b, nf;
-        int st;
+        int st, mem = 0;
+        uint32_t bit = 0;
         if (ix < G) {
             const GRec g = p.tb.grec[ix];
             const double2 ab = p.tb.ab[ix];                       // device row 0 (D = 1)
             slo = g.slo; aw = ab.x; b = (float)ab.y; nf = (float)g.n; st = g.model;
+            if constexpr (TIER) { mem = p.t_mem[g.model]; bit = 1u << g.model; }
         } else if (ix >= T) {                                    // neutral padding token
             slo = 1e30; aw = 0.0; b = 0.0f; nf = 0.0f; st = 0;
         } else {
             const QRec q = p.tb.qrec[ix - G + 1];
             slo = 1e30; aw = q.bmean; b = (float)q.bvar; nf = 0.0f;
             st = q.backlog ? q.r : M + q.r;
+            if constexpr (TIER) { mem = min(p.t_cap[q.d], summem); bit = 1u << q.r; }
         }
         uint8_t *e = smem + w.off_rec + ix * kRecStride;
         if (r < kRep)
             *reinterpret_cast<float4 *>(e + r * 16) =
                 make_float4(__int_as_float(__double2loint(aw)), __int_as_float(__double2hiint(aw)),
                             __int_as_float(__double2hiint(slo)), nf);
-        *reinterpret_cast<float2 *>(e + kRep * 16 + r * 8) = make_float2(b, __int_as_float(st * 128));
+        if constexpr (TIER) {
+            if (r < kRep)
+                *reinterpret_cast<float4 *>(e + kRep * 16 + r * 16) =
+                    make_float4(b, __int_as_float(st * TRR * 8), __int_as_float(mem), __int_as_float((int)bit));
+        } else {
+            *reinterpret_cast<float2 *>(e + kRep * 16 + r * 8) = make_float2(b, __int_as_float(st * TRR * 8));
+        }
     }
-    // transitions [2M][2M][16 replicas] f64, row = state before the slot, column
-    // = the slot's state: tail of the model ahead on a change (R1) + swap, one
-    // fp64 term (R2); columns >= M (separators) are never used (keep = 0)
+    // transitions [2M][2M][TRR replicas] f64, row = state before the slot,
+    // column = the slot's state: tail of the model ahead on a change (R1) +
+    // swap, one fp64 term (R2); columns >= M (separators) are never used (keep
+    // = 0).  Tiered: a second (cold) table follows, + the storage -> CPU load of
+    // a model that changes (R20)
     const int R = 2 * M;
-    for (int i = tid; i < R * R * kTrRep; i += blockDim.x) {
-        const int e = i / kTrRep, col = e % R, row = e / R;
+    const int ntr = R * R * TRR;
+    for (int i = tid; i < (TIER ? 2 : 1) * ntr; i += blockDim.x) {
+        const int e = (i % ntr) / TRR, col = e % R, row = e / R;
         double v = 0.0;
         if (col < M) {
             const int from = row < M ? row : row - M;
             const double sw = p.tb.swap[from * M + col];
             const double tl = (row < M && col != row) ? p.tb.tail[row] : 0.0;
-            v = __dadd_rn(tl, sw);
+            v = i < ntr ? __dadd_rn(tl, sw) : __dadd_rn(tl, __dadd_rn(sw, col != from ? p.t_load[col] : 0.0));
         }
         reinterpret_cast<double *>(smem + w.off_tr)[i] = v;
     }
@@ -525,8 +583,9 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
     } else {           // ---------------- consumer
         const int pair = role_pair;
         const uint32_t rb = su32(smem + w.off_rec) + (lane & (kRep - 1)) * 16;
-        const uint32_t rb1 = su32(smem + w.off_rec) + kRep * 16 + (lane & (kTrRep - 1)) * 8;
-        const uint32_t tb = su32(smem + w.off_tr) + (lane & (kTrRep - 1)) * 8;
+        const uint32_t rb1 = su32(smem + w.off_rec) + kRep * 16 + (TIER ? (lane & 7) * 16 : (lane & 15) * 8);
+        const uint32_t tb = su32(smem + w.off_tr) + (lane & (TRR - 1)) * 8;
+        const uint32_t cold_off = (uint32_t)ntr * 8u;
         const uint32_t st0 = su32(smem + w.off_stage) + (uint32_t)pair * (3 * (GS + 1) * 128);
         const uint32_t sb = st0 + lane * 4;
         const uint32_t pq0 = su32(smem + w.off_pend) + (uint32_t)pair * (kPend * 256) + lane * 8;
@@ -537,6 +596,8 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
         const double q0mean = q0.bmean;
         const float q0var = (float)q0.bvar;
         const int q0st = q0.backlog ? q0.r : M + q0.r;
+        const uint32_t q0bit = 1u << q0.r;
+        const int q0cap = TIER ? min(p.t_cap[q0.d], summem) : 0;
         const int nw = (T + 3) >> 2;                               // row words (padded)
         for (int j = 0;; ++j) {
             const int s = 2 * pair + (j & 1);
@@ -556,23 +617,25 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             Acc a;
             a.A = q0mean; a.B = q0var;
             a.S2 = 0.0; a.acc2 = 0.0; a.acc1 = 0.0f; a.over = 0.0f; a.pq = pq0;
-            uint32_t prow = tb + (uint32_t)q0st * 128u * R;   // queue 0 start row
+            uint32_t prow = tb + (uint32_t)q0st * (TRR * 8u) * R;   // queue 0 start row
             int gq = G;
+            TierState ts;
+            ts.pbit = q0bit; ts.seen = 0u; ts.warm = 0u; ts.cum = 0; ts.capd = q0cap;
             uint32_t cur = ld_u32(ra);
             int wi = 0;
             for (; wi + 1 < nw; wi += 2) {
                 const uint32_t nxt = ld_u32(ra + (wi + 1) * 128);
                 WordData d;
-                load_word(cur, G, R, rb, rb1, tb, prow, gq, d);
+                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d);
                 compute_word<GS, SCORE>(d, sb, zc, oc, a);
                 cur = ld_u32(ra + (wi + 2 < nw ? wi + 2 : wi + 1) * 128);
-                load_word(nxt, G, R, rb, rb1, tb, prow, gq, d);
+                load_word<TIER>(nxt, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d);
                 compute_word<GS, SCORE>(d, sb, zc, oc, a);
                 if (__any_sync(0xFFFFFFFFu, a.pq > pqlim)) flush<GS, SCORE>(pq0, rb, sb, alpha, a);
             }
             if (wi < nw) {
                 WordData d;
-                load_word(cur, G, R, rb, rb1, tb, prow, gq, d);
+                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d);
                 compute_word<GS, SCORE>(d, sb, zc, oc, a);
             }
             flush<GS, SCORE>(pq0, rb, sb, alpha, a);
@@ -653,10 +716,10 @@ static bool make_map(CUtensorMap *tm, float *ptr, int64_t count, int G) {
 static size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 static size_t a1k(size_t x) { return (x + 1023) & ~size_t(1023); }
 
-static size_t plan(Params &w, int W, int GS) {
+static size_t plan(Params &w, int W, int GS, bool tier) {
     const Dims &dm = w.p.dm;
     size_t off = 0;
-    w.off_tr = (int)off;    off = a16(off + (size_t)4 * dm.M * dm.M * kTrRep * 8);
+    w.off_tr = (int)off;    off = a16(off + (size_t)4 * dm.M * dm.M * kTrRep * 8);   // tiered: 2 x 8 replicas
     w.off_rec = (int)off;   off = a16(off + (size_t)(dm.T + kNeutral) * kRecStride);
     w.tw = (dm.T + 3) / 4;
     off = a1k(off);         // slot bases 1 KB aligned (the producer ORs byte offsets in)
@@ -693,9 +756,9 @@ static size_t opt_in(K kern) {
     return m;
 }
 
-template <int KIND, int GS, int SCORE>
+template <int KIND, int GS, int SCORE, bool TIER>
 static cudaError_t launch_t(const ScanParams &p0, cudaStream_t st) {
-    auto kern = ws2_kernel<KIND, GS, SCORE>;
+    auto kern = ws2_kernel<KIND, GS, SCORE, TIER>;
     const size_t lim = opt_in(kern);
     if (!lim) return cudaErrorNotSupported;
     Params w;
@@ -705,12 +768,12 @@ static cudaError_t launch_t(const ScanParams &p0, cudaStream_t st) {
     size_t smem = 0;
     for (int cand = 8; cand >= 2; --cand) {
         Params t = w;
-        const size_t sm = plan(t, cand, GS);
+        const size_t sm = plan(t, cand, GS, TIER);
         if (sm <= lim) { W = cand; smem = sm; break; }
     }
     if (W < 2) return cudaErrorNotSupported;
     if (W > 6) W = 6;                       // 12 warps: 3 per scheduler
-    smem = plan(w, W, GS);
+    smem = plan(w, W, GS, TIER);
     const Dims &dm = p0.dm;
     w.zc = p0.zc;
     w.oc = 1.0f > p0.alpha ? 1.0f : 0.0f;
@@ -730,27 +793,27 @@ static cudaError_t launch_t(const ScanParams &p0, cudaStream_t st) {
     if (grid > need) grid = need;
     if (grid > p0.max_blocks) grid = p0.max_blocks;
     if (grid < 1) grid = 1;
-    qlog(1, "ws2_kernel<kind=%d,GS=%d,score=%d> count=%lld pairs=%d grid=%lld smem=%zu tma=%d", KIND, GS,
-         SCORE, (long long)p0.cd.count, W, (long long)grid, smem, w.use_tma);
+    qlog(1, "ws2_kernel<kind=%d,GS=%d,score=%d,tier=%d> count=%lld pairs=%d grid=%lld smem=%zu tma=%d", KIND,
+         GS, SCORE, (int)TIER, (long long)p0.cd.count, W, (long long)grid, smem, w.use_tma);
     kern<<<(unsigned)grid, (WS2_SPREAD && W == 6) ? 512 : 64 * W, smem, st>>>(w);
     ++g_launches;
     return cudaGetLastError();
 }
 
-template <int KIND, int SCORE>
+template <int KIND, int SCORE, bool TIER>
 static cudaError_t launch_g(const ScanParams &p, cudaStream_t st) {
     const int G = p.dm.G;
-    if (G <= 32) return launch_t<KIND, 32, SCORE>(p, st);
-    if (G <= 64) return launch_t<KIND, 64, SCORE>(p, st);
-    if (G <= 128) return launch_t<KIND, 128, SCORE>(p, st);
+    if (G <= 32) return launch_t<KIND, 32, SCORE, TIER>(p, st);
+    if (G <= 64) return launch_t<KIND, 64, SCORE, TIER>(p, st);
+    if (G <= 128) return launch_t<KIND, 128, SCORE, TIER>(p, st);
     return cudaErrorNotSupported;
 }
 
-template <int KIND>
+template <int KIND, bool TIER = false>
 static cudaError_t launch_k(const ScanParams &p, cudaStream_t st) {
-    if (p.n_over) return launch_g<KIND, 2>(p, st);
-    if (p.s1 || p.s2 || p.out_rec) return launch_g<KIND, 1>(p, st);
-    return launch_g<KIND, 0>(p, st);
+    if (p.n_over) return launch_g<KIND, 2, TIER>(p, st);
+    if (p.s1 || p.s2 || p.out_rec) return launch_g<KIND, 1, TIER>(p, st);
+    return launch_g<KIND, 0, TIER>(p, st);
 }
 
 }  // namespace ws2
@@ -768,6 +831,21 @@ cudaError_t launch_ws2(const ScanParams &p, cudaStream_t st) {
     case QLM_CAND_EXPLICIT: return p.cd.tb == 1 ? ws2::launch_k<QLM_CAND_EXPLICIT>(p, st) : cudaErrorNotSupported;
     case QLM_CAND_NEIGHBOR: return p.cd.tb == 1 ? ws2::launch_k<QLM_CAND_NEIGHBOR>(p, st) : cudaErrorNotSupported;
     case QLM_CAND_ENUM: return ws2::launch_k<QLM_CAND_ENUM>(p, st);
+    default: return cudaErrorNotSupported;
+    }
+}
+
+// The same kernel with two-tier swapping (R20): warm / cold transition tables
+// and the per-queue tier walk in the consumer.  Model sizes and capacities
+// travel as 32-bit ints in the records (set_tiers bounds them by 2^24).
+cudaError_t launch_ws2_tier(const ScanParams &p, cudaStream_t st) {
+    if (p.dm.D != 1 || p.dm.T > 256 || p.dm.G > 128 || p.dm.M > 6 || !p.slo_hi_only || p.cd.first_from ||
+        p.cd.count < 4096 || p.cd.count > ((int64_t)1 << 31) - 64 || !p.t_mem || !p.t_cap || !p.t_load)
+        return cudaErrorNotSupported;
+    if (!(p.wt || p.sd || p.vo)) return cudaErrorNotSupported;
+    switch (p.cd.kind) {
+    case QLM_CAND_RANDOM: return ws2::launch_k<QLM_CAND_RANDOM, true>(p, st);
+    case QLM_CAND_EXPLICIT: return p.cd.tb == 1 ? ws2::launch_k<QLM_CAND_EXPLICIT, true>(p, st) : cudaErrorNotSupported;
     default: return cudaErrorNotSupported;
     }
 }

@@ -793,6 +793,43 @@ def test_tiers_random_problems_all_kinds(seed):
         assert ok
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_tiers_ws_random_problems_vs_thread_kernel(seed):
+    # the warp-specialised tier walks (ws2_kernel: D = 1, G <= 128, M <= 6;
+    # ws_kernel otherwise) on random problems and tier tables -- tight caps,
+    # backlogs, sigma = 0 -- equal the thread-per-candidate tier kernel bit
+    # for bit over >= 4096 candidates and the oracle on a ragged tail
+    from workloads.synth import make_random_tiers
+    rng = np.random.default_rng(900 + seed)
+    D = 1 if seed < 4 else 2
+    G, Q, M = int(rng.integers(3, 120)), int(rng.integers(1, 9)), int(rng.integers(2, 7))
+    p = make_random_problem(rng, G, Q, M, D, backlog=bool(seed % 2), sigma_zero=seed == 2)
+    if D == 1:   # SLOs with a zero low word: the D = 1 byte-row kernel (ws2) takes these
+        p.slo = (p.slo.view(np.uint64) & np.uint64(0xFFFFFFFF00000000)).view(np.float64)
+    tiers = make_random_tiers(rng, M, D)
+    e = est_of(p)
+    e.set_tiers(tiers)
+    n = 4096 + 37
+    for kind in ("random", "explicit"):
+        if kind == "random":
+            cand, kw = e.random(11, n, seed=4), dict(kind=O.RANDOM, first=11, seed=4)
+        else:
+            rows = np.stack([O.random_row(5, c, p.T) for c in range(n)])
+            cand, kw = e.explicit(rows_tensor(rows)), dict(kind=O.EXPLICIT, first=0, rows=rows.astype(np.uint8))
+        ws, rws = _tier_out(e, cand)
+        kernel_overrides(no_ws=True)
+        th, rth = _tier_out(e, cand)
+        kernel_overrides()
+        for k in ("wt", "sd", "v", "s1", "s2", "n_over"):
+            assert torch.equal(ws[k], th[k]), (kind, k)
+        assert torch.equal(rws, rth)
+        lo = n - 50
+        ref = O.Oracle(p).tiered_range(tiers, kw["kind"], kw["first"] + lo, 50, seed=kw.get("seed", 0),
+                                       rows=kw["rows"][lo:] if "rows" in kw else None)
+        check_estimates({k: ws[k][:, lo:] for k in ("wt", "sd", "v")}, ref)
+        assert np.array_equal(ws["n_over"][lo:].cpu().numpy(), ref["n_over"])
+
+
 def test_tiers_enum_brute_force_and_edges():
     from tests.handmade import hand_problem
     p = hand_problem([1, 2, 1, 3, 0], 25, 200.0, 0.0, 150.0, theta=1000.0, prefill=0.5, eps=1.0,
@@ -820,11 +857,12 @@ def test_tiers_enum_brute_force_and_edges():
         e.tiered_score_estimate(e.random(0, 10, seed=1))
 
 
-@pytest.mark.parametrize("cfg", ["C3", "C4"])
-def test_tiers_ws_path_bit_identical_to_thread_kernel(cfg, monkeypatch):
-    # count >= 4096 takes the warp-specialised kernel (TIER variant); QLM_NO_WS
-    # forces the thread-per-candidate tier kernel.  Both add in the oracle's
-    # order and share the S1 accumulator split: outputs must be identical.
+@pytest.mark.parametrize("cfg,ws", [("C3", "ws2"), ("C3", "ws"), ("C4", "ws")])
+def test_tiers_ws_path_bit_identical_to_thread_kernel(cfg, ws, monkeypatch):
+    # count >= 4096 takes a warp-specialised kernel (TIER variant: ws2_kernel
+    # for D = 1 byte rows, else ws_kernel); no_ws forces the thread-per-
+    # candidate tier kernel.  All add in the oracle's order and share the S1
+    # accumulator split: outputs must be identical.
     from workloads.synth import make_tiers
     p = make_config(cfg)
     t = make_tiers()
@@ -832,6 +870,7 @@ def test_tiers_ws_path_bit_identical_to_thread_kernel(cfg, monkeypatch):
     e.set_tiers(t)
     n = 8192 + 64
     cand = e.random(31, n, seed=1)
+    kernel_overrides(no_ws2=ws == "ws")
     ws, rws = _tier_out(e, cand)
     kernel_overrides(no_ws=True)
     th, rth = _tier_out(e, cand)

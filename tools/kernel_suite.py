@@ -154,7 +154,7 @@ def items():
         ("mc_count 1221 trials of one ordering", "C4", c4_mc_count),
         ("score_estimate RANDOM bulk + argmin (wide_kernel)", "C5", bulk("C5", 100_000)),
         ("tiered_score_estimate RANDOM bulk + argmin", "C5h", bulk("C5h", 100_000, tiered=True)),
-        ("tiered_score_estimate RANDOM bulk + argmin (ws kernel, TIER)", "C3", bulk("C3", 1_000_000, tiered=True)),
+        ("tiered_score_estimate RANDOM bulk + argmin (ws2 kernel, TIER)", "C3", bulk("C3", 1_000_000, tiered=True)),
         ("local_search 64 x 65536 NEIGHBOR (2 moves)", "C3", c3_search),
         ("step: score_estimate 1e5 + winner decode, direct launches", "C2", c2_step(False)),
         ("step: score_estimate 1e5 + winner decode, CUDA graph replay", "C2", c2_step(True)),
@@ -263,7 +263,7 @@ def items_meta():
         ("mc_count 1221 trials of one ordering", "C4", r"mc_count_kernel"),
         ("score_estimate RANDOM bulk + argmin (wide_kernel)", "C5", r"fy_rows_kernel|wide_kernel|reduce_records"),
         ("tiered_score_estimate RANDOM bulk + argmin", "C5h", r"tier_warp_kernel|tier_kernel|big_kernel"),
-        ("tiered_score_estimate RANDOM bulk + argmin (ws kernel, TIER)", "C3", r"ws_kernel<1, unsigned char, 1, \d, 1>"),
+        ("tiered_score_estimate RANDOM bulk + argmin (ws2 kernel, TIER)", "C3", r"ws2_kernel<1, \d+, \d, (true|1)>|ws_kernel<1, unsigned char, 1, \d, 1>"),
         ("local_search 64 x 65536 NEIGHBOR (2 moves)", "C3", r"scan_kernel<[03], unsigned char|adopt_kernel"),
         ("step: score_estimate 1e5 + winner decode, direct launches", "C2", r"ws2_kernel<1, 32|row_warp_kernel"),
         ("step: score_estimate 1e5 + winner decode, CUDA graph replay", "C2", r"ws2_kernel<1, 32|row_warp_kernel"),
