@@ -180,3 +180,31 @@ def test_tiered_large_T_two_phase_equals_direct(cap):
     ref = o.tiered_range(t, O.RANDOM, 123 + lo, cnt, seed=1)
     check_estimates({k: b[k][:, lo:lo + cnt] for k in ("wt", "sd", "v")}, ref)
     check_scores(b["s1"][lo:].cpu().numpy(), b["s2"][lo:].cpu().numpy(), ref, p)
+
+
+
+@pytest.mark.parametrize("G,Q", [(250, 8), (300, 33), (1024, 32), (1990, 11), (3500, 2)])
+def test_large_T_two_phase_rows_equal_direct_scan(G, Q):
+    # large-T RANDOM: rows materialised by fy_rows_kernel and scored from the
+    # interleaved scratch (two-phase) equal the scan kernel generating rows
+    # itself, bit for bit -- every candidate's scores and the argmin -- and the
+    # oracle on a ragged tail (T = 257 .. 3501)
+    from paper_2407_00047_b200 import RwtEstimator, kernel_overrides
+    from tests.parity import check_scores
+    from workloads.synth import make_random_problem
+    p = make_random_problem(np.random.default_rng(G + Q), G, Q, 4)
+    n = 4096 + 77
+    res = {}
+    for direct in (False, True):
+        kernel_overrides(no_two_phase=direct, no_wide=True)
+        e = RwtEstimator(p, device=0)
+        rec = torch.empty(2, dtype=torch.int64, device="cuda")
+        out = e.score_estimate(e.random(5, n, seed=3), rec=rec)
+        torch.cuda.synchronize()
+        res[direct] = (out["s1"].clone(), out["s2"].clone(), rec.clone())
+        kernel_overrides()
+    for a, b in zip(res[False], res[True]):
+        assert torch.equal(a, b)
+    lo, cnt = n - 12, 12
+    ref = O.Oracle(p).score_range(O.RANDOM, 5 + lo, cnt, seed=3)
+    check_scores(res[False][0][lo:].cpu().numpy(), res[False][1][lo:].cpu().numpy(), ref, p)
