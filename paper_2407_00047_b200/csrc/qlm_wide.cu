@@ -92,8 +92,35 @@ __device__ __forceinline__ void wide_stage_rows(const Cand &cd, int T, int64_t c
     }
 }
 
+// Word-interleaved rows, software-pipelined: the next batch's words are
+// loaded into registers (kWidePf per thread) before the current batch is
+// scored and stored to shared memory after it, so the global-load latency
+// hides behind the passes (the synchronous staging left the warps waiting on
+// it: long-scoreboard stalls were the largest share).
+constexpr int kWidePf = 24;                   // words per thread in flight (8 * nw <= 256 * kWidePf)
+
+__device__ __forceinline__ void wide_pf_load(const Cand &cd, int nw, int64_t c0, int nv, uint32_t (&v)[kWidePf]) {
+    const uint32_t *r32 = reinterpret_cast<const uint32_t *>(cd.rows);
+    const int n = nw * kWideCands;
+#pragma unroll
+    for (int u = 0; u < kWidePf; ++u) {
+        const int i = threadIdx.x + u * 256, w = i >> 3, k = i & 7;
+        v[u] = (i < n && k < nv) ? __ldcs(r32 + (size_t)w * cd.stride + c0 + k) : 0u;
+    }
+}
+
+__device__ __forceinline__ void wide_pf_store(int nw, const uint32_t (&v)[kWidePf], uint16_t *srow, int ldr) {
+    uint32_t *s32 = reinterpret_cast<uint32_t *>(srow);
+    const int ldw = ldr >> 1, n = nw * kWideCands;
+#pragma unroll
+    for (int u = 0; u < kWidePf; ++u) {
+        const int i = threadIdx.x + u * 256, w = i >> 3, k = i & 7;
+        if (i < n) s32[k * ldw + w] = v[u];
+    }
+}
+
 template <int KIND, bool SCORE>
-__global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
+__global__ void __launch_bounds__(256, 2) wide_kernel(const ScanParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const Dims dm = p.dm;
@@ -138,11 +165,26 @@ __global__ void __launch_bounds__(256) wide_kernel(const ScanParams p) {
     uint64_t bkey = ~0ull;
     int64_t bidx = -1;
     const int64_t nbatch = (count + kWideCands - 1) / kWideCands;
+    const int nw = (T + 1) >> 1;
+    constexpr bool kIlv = KIND == KIND_ILV;
+    const bool pf = kIlv && nw * kWideCands <= 256 * kWidePf;
+    uint32_t pfv[kWidePf];
+    if (kIlv && pf && blockIdx.x < nbatch)
+        wide_pf_load(cd, nw, (int64_t)blockIdx.x * kWideCands,
+                     (int)min((int64_t)kWideCands, count - (int64_t)blockIdx.x * kWideCands), pfv);
     for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
         const int64_t c0 = bt * kWideCands;
         const int64_t loc = c0 + warp;
-        wide_stage_rows<KIND>(cd, T, c0, (int)min((int64_t)kWideCands, count - c0), srows, ldr);
-        __syncthreads();
+        if (kIlv && pf) {
+            wide_pf_store(nw, pfv, srows, ldr);
+            __syncthreads();
+            const int64_t bn = bt + gridDim.x;                 // next batch: loads in flight now
+            if (bn < nbatch)
+                wide_pf_load(cd, nw, bn * kWideCands, (int)min((int64_t)kWideCands, count - bn * kWideCands), pfv);
+        } else {
+            wide_stage_rows<KIND>(cd, T, c0, (int)min((int64_t)kWideCands, count - c0), srows, ldr);
+            __syncthreads();
+        }
         const uint16_t *row = srows + warp * ldr;
         if (loc < count) {
             // ---- entry state of this lane's chunk (from the row itself)
