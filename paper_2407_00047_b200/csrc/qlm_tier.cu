@@ -248,13 +248,14 @@ static cudaError_t launch_tier_t(const ScanParams &p, cudaStream_t st) {
 // a [3][G][9] tile and leave as full 32-B rows of the group-major arrays.
 constexpr int kTwWarps = 8;
 constexpr int kTwPad = kTwWarps + 1;
+constexpr int kTwPf = 24;           // prefetched row words per lane (interleaved rows, T <= 1536)
 
 struct TierWarpSmem {
     int off_g, off_ab, off_q, off_trw, off_trc, off_mem, off_cap, off_tile, off_rows, off_qbeg;
     int ldr;
 };
 
-__global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, const TierWarpSmem L) {
+__global__ void __launch_bounds__(256, 1) tier_warp_kernel(const ScanParams p, const TierWarpSmem L) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const Dims dm = p.dm;
@@ -303,10 +304,35 @@ __global__ void __launch_bounds__(256) tier_warp_kernel(const ScanParams p, cons
     uint64_t bkey = ~0ull;
     int64_t bidx = -1;
     const int64_t nbatch = (count + kTwWarps - 1) / kTwWarps;
+    // interleaved rows (two-phase): the warp's next row is loaded into
+    // registers (kTwPf words per lane) before the current one is walked, so
+    // the strided global loads overlap the walk
+    const int nw = (T + 1) >> 1;
+    const bool pf = cd.kind == KIND_ILV && nw <= 32 * kTwPf;
+    const uint32_t *r32 = reinterpret_cast<const uint32_t *>(cd.rows);
+    uint32_t pfv[kTwPf];
+    auto pf_load = [&](int64_t l) {
+#pragma unroll
+        for (int u = 0; u < kTwPf; ++u) {
+            const int w = lane + 32 * u;
+            pfv[u] = (w < nw && l < count) ? __ldg(r32 + (size_t)w * cd.stride + l) : 0u;
+        }
+    };
+    if (pf) pf_load((int64_t)blockIdx.x * kTwWarps + warp);
     for (int64_t bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
         const int64_t c0 = bt * kTwWarps, loc = c0 + warp;
+        if (pf) {
+            uint32_t *s32 = reinterpret_cast<uint32_t *>(srow);   // srow is 4-B aligned (ldr even)
+#pragma unroll
+            for (int u = 0; u < kTwPf; ++u) {
+                const int w = lane + 32 * u;
+                if (w < nw) s32[w] = pfv[u];
+            }
+            __syncwarp();
+            pf_load((bt + gridDim.x) * kTwWarps + warp);
+        }
         if (loc < count) {                                    // warp-uniform
-            warp_gen_row(cd, T, (uint64_t)(first + loc), loc, srow, sJ);
+            if (!pf) warp_gen_row(cd, T, (uint64_t)(first + loc), loc, srow, sJ);
             // queue q covers row positions [qbeg[q], qbeg[q + 1] - 1)
             if (lane == 0) qbeg[0] = 0;
             int nsep = 0;
