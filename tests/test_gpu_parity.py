@@ -313,6 +313,25 @@ def test_mc_random_candidates_and_trial_offsets():
     assert torch.equal(a + b, cnt)
 
 
+def test_mc_sampler_request_chunks_and_reuse():
+    # a10 splits a group's requests into 64-request chunks summed with integer
+    # atomics (last chunk converts and resets the scratch): group sizes on
+    # both sides of every chunk / Philox-block boundary, trials not a multiple
+    # of 32, repeated calls (the scratch must come back zeroed) and a larger
+    # then smaller trial count (reallocation) -- all bit-exact to the oracle
+    rng = np.random.default_rng(23)
+    sizes = [1, 7, 8, 9, 63, 64, 65, 71, 72, 511, 512, 513, 4000, 3]
+    p = make_random_problem(rng, len(sizes), 3, 3, 2, with_tables=True)
+    p.n_req = np.array(sizes, np.int32)
+    e = est_of(p)
+    o = O.Oracle(p)
+    cand = e.random(3, 4, seed=5)
+    for nt, t0 in ((77, 0), (77, 0), (1500, 40), (33, 9)):
+        cnt = e.mc_estimate(cand, mc_seed=13, trials=nt, trial_first=t0)
+        ref = o.mc_count(O.RANDOM, 3, 4, o.mc_sample(13, t0, nt), seed=5)
+        np.testing.assert_array_equal(cnt.cpu().numpy().astype(np.uint32), ref)
+
+
 def test_mc_of_device_record_without_sync():
     p = make_config("C2")
     p.len_tables = make_config("C3").len_tables
