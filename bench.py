@@ -374,7 +374,7 @@ def run_ours(args, rank, world, local_rank):
                "ms_per_step": te.item(),
                "note": "per step: pinned H2D of the 64 group records through qlm_update_groups + "
                        "table rebuild, the whole step, D2H of the winner (index, S1, S2, n_over, "
-                       "decoded ordering) through qlm_winner plus the MC counts, and a host read of "
+                       "decoded ordering) written into pinned host buffers by qlm_winner, D2H of the MC counts, and a host read of "
                        "the result; pipelined one step deep (the host reads step k-1 while step k runs)"}
 
     if rank == 0:

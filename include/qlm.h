@@ -194,9 +194,10 @@ QLM_API int qlm_best_ordering(qlm_ctx *ctx, const qlm_candidates *cand, qlm_best
  * candidate named by a device record (`one`: count 1, first_from = the record,
  * a RANDOM / ENUM / NEIGHBOR description) is scored and decoded on `stream`,
  * then out->{index, s1, s2, n_over} and queue_of_group[G] / pos_of_group[G]
- * (nullable) are copied to the caller's host buffers.  Asynchronous: the host
- * values are valid once `stream` reaches this point (pinned buffers make the
- * copies truly asynchronous).  Typical use: the winner record of
+ * (nullable) reach the caller's host buffers: pinned (page-locked, mapped)
+ * buffers are written by the device directly with one kernel, pageable ones
+ * get one copy per field.  Asynchronous: the host values are valid once
+ * `stream` reaches this point.  Typical use: the winner record of
  * qlm_score_estimate / qlm_best_ordering_async (global once a communicator is
  * attached).  Errors: QLM_EINVAL (count != 1, no first_from, EXPLICIT).     */
 QLM_API int qlm_winner(qlm_ctx *ctx, const qlm_candidates *one, qlm_best *out, int32_t *queue_of_group,

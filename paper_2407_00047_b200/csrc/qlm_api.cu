@@ -660,6 +660,18 @@ int qlm_decode(qlm_ctx *ctx, const qlm_candidates *cand, int32_t *queue_of_group
     return e == cudaSuccess ? QLM_OK : cuda_fail(e, "decode kernel");
 }
 
+// The device address of a pinned host buffer (page-locked and mapped, as
+// cudaHostAlloc / cudaHostRegister memory is under unified addressing), or
+// nullptr for pageable memory.
+static void *mapped_host(void *h) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 int qlm_winner(qlm_ctx *ctx, const qlm_candidates *one, qlm_best *out, int32_t *queue_of_group,
                int32_t *pos_of_group, void *stream) {
     DevGuard dg_;
@@ -678,6 +690,15 @@ int qlm_winner(qlm_ctx *ctx, const qlm_candidates *one, qlm_best *out, int32_t *
     if ((rc = qlm_score_orderings(ctx, one, d_s, d_s + 1, d_no, stream))) return rc;
     if ((rc = qlm_decode(ctx, one, ctx->d_dec_out, ctx->d_dec_out + G, stream))) return rc;
     cudaError_t e;
+    // pinned (device-mapped) host buffers: the device writes the result fields
+    // straight into them with one small kernel; otherwise one copy per field
+    void *m_out = mapped_host(out), *m_qo = queue_of_group ? mapped_host(queue_of_group) : nullptr,
+         *m_po = pos_of_group ? mapped_host(pos_of_group) : nullptr;
+    if (m_out && (m_qo || !queue_of_group) && (m_po || !pos_of_group)) {
+        e = launch_winner_out(one->first_from, d_s, d_no, ctx->d_dec_out, G, static_cast<qlm_best *>(m_out),
+                              static_cast<int32_t *>(m_qo), static_cast<int32_t *>(m_po), st);
+        return e == cudaSuccess ? QLM_OK : cuda_fail(e, "winner readback");
+    }
     if ((e = cudaMemcpyAsync(&out->index, &one->first_from->index, sizeof(int64_t), cudaMemcpyDeviceToHost, st)) ||
         (e = cudaMemcpyAsync(&out->s1, d_s, 2 * sizeof(float), cudaMemcpyDeviceToHost, st)) ||
         (e = cudaMemcpyAsync(&out->n_over, d_no, sizeof(int32_t), cudaMemcpyDeviceToHost, st)) ||

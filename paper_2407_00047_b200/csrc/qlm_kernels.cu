@@ -443,6 +443,34 @@ __global__ void __launch_bounds__(32) fy_rows_kernel(Cand cd, int T, uint32_t *o
     if (act) __stcs(op, fin);
 }
 
+// qlm_winner's result, written by the device straight into the caller's
+// pinned (device-mapped) host buffers: one launch instead of five D2H copies.
+__global__ void __launch_bounds__(256) winner_out_kernel(const qlm_record *rec, const float *s12,
+                                                         const int32_t *n_over, const int32_t *dec, int G,
+                                                         qlm_best *out, int32_t *qo, int32_t *po) {
+    if (threadIdx.x == 0) {
+        qlm_best b;
+        b.index = rec->index;
+        b.s1 = s12[0];
+        b.s2 = s12[1];
+        b.n_over = *n_over;
+        b.reserved = 0;
+        *out = b;
+    }
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        if (qo) qo[g] = dec[g];
+        if (po) po[g] = dec[G + g];
+    }
+}
+
+cudaError_t launch_winner_out(const qlm_record *rec, const float *s12, const int32_t *n_over,
+                              const int32_t *dec, int G, qlm_best *out, int32_t *qo, int32_t *po,
+                              cudaStream_t st) {
+    winner_out_kernel<<<1, 256, 0, st>>>(rec, s12, n_over, dec, G, out, qo, po);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 // =============================================================================
 // a9: rows / decode (thread per candidate, same generators as the scan)
 // =============================================================================

@@ -77,6 +77,10 @@ cudaError_t launch_form_groups(int n, int dims, int M, const int32_t *k_host, in
                                int32_t *n_bad, cudaStream_t st);  // Alg. 1 (R21)
 cudaError_t launch_adopt(const Dims &dm, const Cand &cd, const qlm_record *rec, qlm_record *inc,
                          cudaStream_t st);                          // local-search step (R18)
+// qlm_winner's fields into device-mapped host buffers (qo / po nullable)
+cudaError_t launch_winner_out(const qlm_record *rec, const float *s12, const int32_t *n_over,
+                              const int32_t *dec, int G, qlm_best *out, int32_t *qo, int32_t *po,
+                              cudaStream_t st);
 cudaError_t launch_rows(const ScanParams &p, uint16_t *rows, int32_t *qo, int32_t *po,
                         cudaStream_t st);
 cudaError_t launch_reduce_records(const qlm_record *recs, int n, qlm_record *out,

@@ -288,7 +288,8 @@ class RwtEstimator:
 
     def winner(self, one: Cand, host: dict, stream=None):
         """qlm_winner: the record's candidate scored and decoded on the stream and
-        copied into host tensors (pinned recommended): host["best"] a uint8[24]
+        written into host tensors (pinned: by the device directly, one kernel;
+        pageable: one copy per field): host["best"] a uint8[24]
         qlm_best image, host["qo"] / host["po"] int32[G].  Asynchronous."""
         L.check(L.lib().qlm_winner(self._h, C.byref(one.c()), host["best"].data_ptr(),
                                    host["qo"].data_ptr() if "qo" in host else None,

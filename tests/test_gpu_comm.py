@@ -116,17 +116,20 @@ def test_local_search_graph_equals_direct_launches():
             assert torch.equal(g_row, d_row) and torch.equal(g_inc, d_inc)
 
 
-def test_winner_reads_the_record_into_host_buffers():
-    # qlm_winner: the record's candidate scored + decoded on the stream, copied
-    # into host buffers -- equal to the synchronous qlm_best_ordering
+@pytest.mark.parametrize("pinned", [True, False])
+def test_winner_reads_the_record_into_host_buffers(pinned):
+    # qlm_winner: the record's candidate scored + decoded on the stream, written
+    # into host buffers (pinned: by the device directly; pageable: copies) --
+    # equal to the synchronous qlm_best_ordering
     from paper_2407_00047_b200 import RwtEstimator
     p = make_config("C3")
     e = RwtEstimator(p, device=0)
     cand = e.random(0, 50_000, seed=2)
     rec = e.best_ordering_async(cand)
-    host = {"best": torch.empty(24, dtype=torch.uint8).pin_memory(),
-            "qo": torch.empty(p.G, dtype=torch.int32).pin_memory(),
-            "po": torch.empty(p.G, dtype=torch.int32).pin_memory()}
+    mk = (lambda t: t.pin_memory()) if pinned else (lambda t: t)
+    host = {"best": mk(torch.full((24,), 0xAB, dtype=torch.uint8)),
+            "qo": mk(torch.full((p.G,), -7, dtype=torch.int32)),
+            "po": mk(torch.full((p.G,), -7, dtype=torch.int32))}
     e.winner(e.from_record(rec, seed=2), host)
     torch.cuda.synchronize()
     got = RwtEstimator.best_of(host["best"])
