@@ -400,6 +400,71 @@ def test_warp_specialised_and_fallback_kernels_agree(cfg, n, kind, monkeypatch):
     check_estimates({k: b[k][:, :m] for k in ("wt", "sd", "v")}, est)
 
 
+@pytest.mark.parametrize("seed", range(9))
+def test_bulk_kernel_paths_agree_random_problems(seed):
+    """Random D = 1 problems (SLOs with a zero low word) across ws2_kernel's
+    group buckets (G <= 32 / 64 / 128), M up to 6, backlogs and sigma = 0,
+    for RANDOM, EXPLICIT, NEIGHBOR and ENUM candidate sets of >= 4096: the
+    D = 1 kernel (ws2), the general warp-specialised kernel (no_ws2) and the
+    thread-per-candidate scan (no_ws) give identical bits -- wt, sd, v, S1,
+    S2, n_over and the argmin record -- and match the oracle on a ragged tail."""
+    rng = np.random.default_rng(4200 + seed)
+    lo, hi = [(3, 32), (33, 64), (65, 128)][seed % 3]
+    G = int(rng.integers(lo, hi + 1))
+    Q, M = int(rng.integers(1, 10)), int(rng.integers(2, 7))
+    kinds = ["random", "explicit", "neighbor"]
+    if seed == 0:
+        G, Q, kinds = 5, 4, ["enum"]                    # T = 8: 8! = 40320 orderings
+    p = make_random_problem(rng, G, Q, M, 1, backlog=bool(seed % 2), sigma_zero=seed == 4)
+    p.slo = (p.slo.view(np.uint64) & np.uint64(0xFFFFFFFF00000000)).view(np.float64)
+    e = est_of(p)
+    o = O.Oracle(p)
+    n = 4096 + 97 if seed else 40320
+    for kind in kinds:
+        ref_kw = {}
+        if kind == "random":
+            cand, ref_kw = e.random(7, n, seed=9), dict(kind=O.RANDOM, first=7, seed=9)
+        elif kind == "enum":
+            cand, ref_kw = e.enum(0, n), dict(kind=O.ENUM, first=0)
+        elif kind == "explicit":
+            rows = np.stack([O.random_row(2, c, p.T) for c in range(n)])
+            cand, ref_kw = e.explicit(rows_tensor(rows)), dict(kind=O.EXPLICIT, first=0, rows=rows.astype(np.uint8))
+        else:
+            base_np = O.random_row(6, 1, p.T)
+            mv = int(rng.integers(1, 4))
+            cand = e.neighbor(e.row_buffer(base_np), 3, n, seed=8, moves=mv)
+            ref_kw = dict(kind=O.NEIGHBOR, first=3, seed=8, rows=base_np, moves=mv)
+        res = {}
+        for path in ("ws2", "ws", "scan"):
+            kernel_overrides(no_ws2=path == "ws", no_ws=path == "scan")
+            rec = torch.empty(2, dtype=torch.int64, device="cuda")
+            bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+            bufs["n_over"] = torch.empty(n, dtype=torch.int32, device="cuda")
+            res[path] = (e.score_estimate(cand, out=bufs, rec=rec), rec)
+            kernel_overrides()
+        torch.cuda.synchronize()
+        (a, ra) = res["ws2"]
+        for path in ("ws", "scan"):
+            b, rb = res[path]
+            for k in ("wt", "sd", "v", "s1", "s2", "n_over"):
+                assert torch.equal(a[k], b[k]), (kind, path, k)
+            assert torch.equal(ra, rb), (kind, path)
+        m = 40
+        t0 = n - m
+        kw = dict(ref_kw)
+        k_, first = kw.pop("kind"), kw.pop("first")
+        if k_ == O.EXPLICIT:
+            kw["rows"] = kw["rows"][t0:]
+            first_ref = 0
+        else:
+            first_ref = first + t0
+        ref = o.score_range(k_, first_ref, m, **kw)
+        est = o.estimate_range(k_, first_ref, m, **kw)
+        check_scores(a["s1"][t0:].cpu().numpy(), a["s2"][t0:].cpu().numpy(), ref, p)
+        check_estimates({k: a[k][:, t0:] for k in ("wt", "sd", "v")}, est)
+        assert np.array_equal(a["n_over"][t0:].cpu().numpy(), ref["n_over"])
+
+
 def test_mc_split_sample_count_on_two_streams():
     p = make_config("C3")
     e = est_of(p)
