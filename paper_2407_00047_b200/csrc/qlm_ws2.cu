@@ -67,13 +67,26 @@ template <bool TIER> __host__ __device__ constexpr int tr_rep() { return TIER ? 
 #ifndef WS2_XNOPROD
 #define WS2_XNOPROD 0
 #endif
+#ifndef WS2_WMAX
+#define WS2_WMAX 7
+#endif
+#ifndef WS2_XW5
+#define WS2_XW5 0
+#endif
 #ifndef WS2_CHAIN1
 #define WS2_CHAIN1 0
+#endif
+#ifndef WS2_PHXPIPE
+#define WS2_PHXPIPE 1     // producer: Philox block b + 1 computed alongside block b's swaps
+#endif
+#ifndef WS2_LATEWAIT
+#define WS2_LATEWAIT 1    // consumer: wait for the previous tile's TMA read after word 0's loads
 #endif
 constexpr int kWordsPerCheck = 2;
 constexpr int kPend = 4 + 4 * kWordsPerCheck;   // deferred-slot FIFO depth per lane
 constexpr int kRecStride = 2 * kRep * 16;   // bytes per token value: [2 halves][8 replicas][16 B]
-constexpr int kNeutral = 8;  // neutral records T .. T+7 (row padding, see load_word)
+// neutral records T .. T + nneu - 1 for the row padding (see load_word)
+__host__ __device__ constexpr int neutral_count(int T) { return (-T) & 3; }
 
 struct alignas(64) Params {
     CUtensorMap tmap[3];     // wt, sd, v: fp32 [G][count], box {32, G}
@@ -196,8 +209,18 @@ __device__ __forceinline__ void produce_random(uint32_t cs, int T, uint64_t seed
         fin |= tj << ((i & 3) * 8);
     };
     int i0 = 0;
+#if WS2_PHXPIPE
+    // the Philox chain of block b + 1 is independent of block b's swaps: the
+    // scheduler interleaves the two latency chains
+    uint4 wn = philox10(make_uint4(0u, clo, chi, kRowTag), key);
+#endif
     for (int b = 0; b < nfull; ++b, i0 += 8) {
+#if WS2_PHXPIPE
+        const uint4 wd = wn;
+        wn = philox10(make_uint4((uint32_t)(b + 1), clo, chi, kRowTag), key);
+#else
         const uint4 wd = philox10(make_uint4((uint32_t)b, clo, chi, kRowTag), key);
+#endif
         const uint32_t pb = cs + (i0 << 5);             // word i0 / 4 of the lane's column
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -210,7 +233,11 @@ __device__ __forceinline__ void produce_random(uint32_t cs, int T, uint64_t seed
         }
     }
     if (i0 < T - 1) {                                   // last partial block
+#if WS2_PHXPIPE
+        const uint4 wd = wn;
+#else
         const uint4 wd = philox10(make_uint4((uint32_t)nfull, clo, chi, kRowTag), key);
+#endif
 #pragma unroll
         for (int k = 0; k < 7; ++k) {
             const int i = i0 + k;
@@ -292,7 +319,7 @@ struct Acc {
 struct WordData {
     double slo[4], aw[4], tr[4];
     float b[4], nf[4];
-    int ix[4], kh[4], sidx[4];
+    int ix[4], kh[4];
 };
 
 // R20 state of the queue being walked: bit of the model in memory, targets
@@ -311,12 +338,13 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
     for (int k = 0; k < 4; ++k) {
         const int tok = (int)__byte_perm(wd, 0u, 0x4440u + k);
         // one predicate for everything a separator changes: its label (the k-th
-        // separator -> G + k), keep (the A reset), the B reset and the trash row
-        // (gq is incremented last: the compiler may give G and gq one register
-        // when their values coincide, so no operand is read after the write)
-        asm("{\n.reg .pred p;\nsetp.ge.s32 p, %4, %5;\nselp.b32 %0, %3, %4, p;\n"
-            "selp.b32 %1, 0, 0x3FF00000, p;\nselp.b32 %2, %5, %4, p;\n@p add.s32 %3, %3, 1;\n}\n"
-            : "=r"(d.ix[k]), "=r"(d.kh[k]), "=r"(d.sidx[k]), "+r"(gq) : "r"(tok), "r"(G));
+        // separator -> G + k), keep (the A reset, the B reset and its staging
+        // stores, which are predicated off) (gq is incremented last: the compiler
+        // may give G and gq one register when their values coincide, so no
+        // operand is read after the write)
+        asm("{\n.reg .pred p;\nsetp.ge.s32 p, %3, %4;\nselp.b32 %0, %2, %3, p;\n"
+            "selp.b32 %1, 0, 0x3FF00000, p;\n@p add.s32 %2, %2, 1;\n}\n"
+            : "=r"(d.ix[k]), "=r"(d.kh[k]), "+r"(gq) : "r"(tok), "r"(G));
         const uint32_t ra = (uint32_t)d.ix[k] * kRecStride;
         const float4 r0 = lds128(rb + ra);               // {a, slo hi, n}
         d.aw[k] = __hiloint2double(__float_as_int(r0.y), __float_as_int(r0.x));
@@ -365,7 +393,7 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
 
 template <int GS, int SCORE>
 __device__ __forceinline__ void compute_word(const WordData &d, uint32_t sb, float zc, float oc, Acc &a) {
-    constexpr uint32_t ASTR = (GS + 1) * 128;            // staging array stride (row G = trash row)
+    constexpr uint32_t ASTR = GS * 128;                  // staging array stride
     double wt[4];
     float V[4];
     // Eq. 10 in the oracle's order: wt = A + (tail + swap); A' = wt + a.  A
@@ -407,32 +435,34 @@ __device__ __forceinline__ void compute_word(const WordData &d, uint32_t sb, flo
             a.S2 = __fma_rn(slack, -__hiloint2double(d.kh[k], 0), a.S2);   // S2 += wt - slo (groups only)
         }
         if (!clamped) {                                  // |z| < z_clamp: exact value at flush
-            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a.pq), "f"(sf), "f"(__int_as_float(d.ix[k])) : "memory");
-            a.pq += 32 * 8;
+            // the token goes to the lane's byte FIFO, the slack to the v row
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(a.pq), "r"(d.ix[k]) : "memory");
+            a.pq += 32;
         }
-        const uint32_t st = sb + (uint32_t)d.sidx[k] * 128u;   // separators -> trash row G
+        const uint32_t st = sb + (uint32_t)d.ix[k] * 128u;
         if (WS2_XNOSTORE) continue;
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(st), "f"((float)wt[k]) : "memory");
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + ASTR), "f"(sd) : "memory");
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(st + 2 * ASTR), "f"(v) : "memory");
+        // separators and padding (keep = 0) store nothing
+        asm volatile("{\n.reg .pred p;\nsetp.ne.s32 p, %4, 0;\n@p st.shared.f32 [%0], %1;\n"
+                     "@p st.shared.f32 [%0+%5], %2;\n@p st.shared.f32 [%0+%6], %3;\n}\n"
+                     ::"r"(st), "f"((float)wt[k]), "f"(sd), "f"(clamped ? v : sf), "r"(d.kh[k]),
+                     "n"(ASTR), "n"(2 * ASTR) : "memory");
     }
 }
 
 // Deferred slots: Phi-bar in FIFO (row) order; v overwrites the staged value.
 template <int GS, int SCORE>
 __device__ __forceinline__ void flush(uint32_t pq0, uint32_t rb, uint32_t sb, float alpha, Acc &a) {
-    const int n = (int)((a.pq - pq0) >> 8);
+    const int n = (int)((a.pq - pq0) >> 5);
     const int maxn = (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)n);
     for (int i = 0; i < maxn; ++i) {
         if (i < n) {
-            float sf, tf;
-            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(sf), "=f"(tf) : "r"(pq0 + i * 256));
-            const int ix = __float_as_int(tf);
+            const int ix = (int)ld_u8(pq0 + i * 32);
             const uint32_t s = sb + (uint32_t)ix * 128u;
-            float sd;
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(sd) : "r"(s + (GS + 1) * 128));
+            float sd, sf;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(sd) : "r"(s + GS * 128));
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(sf) : "r"(s + 2 * GS * 128));   // the slack
             const float v = phibar(sf * rcp_approx(sd));
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(s + 2 * (GS + 1) * 128), "f"(v) : "memory");
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(s + 2 * GS * 128), "f"(v) : "memory");
             if constexpr (SCORE > 0) {
                 float nf;
                 asm volatile("ld.shared.f32 %0, [%1];" : "=f"(nf) : "r"(rb + (uint32_t)ix * kRecStride + 12));
@@ -466,7 +496,7 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
     int summem = 0;
     if constexpr (TIER)
         for (int m = 0; m < M; ++m) summem += p.t_mem[m];
-    for (int i = tid; i < (T + kNeutral) * kTrRep; i += blockDim.x) {
+    for (int i = tid; i < (T + neutral_count(T)) * kTrRep; i += blockDim.x) {
         const int ix = i / kTrRep, r = i % kTrRep;
         double aw, slo;
         float b, nf;
@@ -498,17 +528,18 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             *reinterpret_cast<float2 *>(e + kRep * 16 + r * 8) = make_float2(b, __int_as_float(st * TRR * 8));
         }
     }
-    // transitions [2M][2M][TRR replicas] f64, row = state before the slot,
-    // column = the slot's state: tail of the model ahead on a change (R1) +
-    // swap, one fp64 term (R2); columns >= M (separators) are never used (keep
-    // = 0).  Tiered: a second (cold) table follows, + the storage -> CPU load of
-    // a model that changes (R20)
-    const int R = 2 * M;
-    const int ntr = R * R * TRR;
+    // transitions [2M][M][TRR replicas] f64 + M zero entries, row = state
+    // before the slot, column = the slot's state: tail of the model ahead on a
+    // change (R1) + swap, one fp64 term (R2).  A separator's column (its start
+    // state, >= M) reads the next row's entries or the zero padding: finite
+    // values that keep = 0 discards.  Tiered: a second (cold) table follows,
+    // + the storage -> CPU load of a model that changes (R20)
+    const int R = M;                                       // row stride in entries
+    const int ntr = M * (2 * M + 1) * TRR;
     for (int i = tid; i < (TIER ? 2 : 1) * ntr; i += blockDim.x) {
-        const int e = (i % ntr) / TRR, col = e % R, row = e / R;
+        const int e = (i % ntr) / TRR, col = e % M, row = e / M;
         double v = 0.0;
-        if (col < M) {
+        if (row < 2 * M) {
             const int from = row < M ? row : row - M;
             const double sw = p.tb.swap[from * M + col];
             const double tl = (row < M && col != row) ? p.tb.tail[row] : 0.0;
@@ -540,8 +571,19 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
     // 8, 9, 12, 13 idle
     int role_pair = warp < W ? warp : warp - W;
     bool is_prod = warp >= W, idle = false;
-    if (WS2_SPREAD && W == 6) {
+    if (WS2_SPREAD && W == 7) {
+        // 16-warp block, warp w on scheduler w % 4: consumers 0-6 (schedulers
+        // 0,1,2,3,0,1,2), producers 7-11, 14, 15, warps 12, 13 idle
+        const int pmap[16] = {0, 1, 2, 3, 4, 5, 6, 0, 1, 2, 3, 4, -1, -1, 5, 6};
+        role_pair = pmap[warp];
+        is_prod = warp >= 7;
+        idle = role_pair < 0;
+    } else if (WS2_SPREAD && W == 6) {
+#if WS2_XW5   // timing experiment: pair 5 idle (five consumers, same placement)
+        const int pmap[16] = {0, 1, 2, 3, 4, -1, 0, 1, -1, -1, 2, 3, -1, -1, 4, -1};
+#else
         const int pmap[16] = {0, 1, 2, 3, 4, 5, 0, 1, -1, -1, 2, 3, -1, -1, 4, 5};
+#endif
         role_pair = pmap[warp];
         is_prod = warp >= 6;
         idle = role_pair < 0;
@@ -586,10 +628,10 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
         const uint32_t rb1 = su32(smem + w.off_rec) + kRep * 16 + (TIER ? (lane & 7) * 16 : (lane & 15) * 8);
         const uint32_t tb = su32(smem + w.off_tr) + (lane & (TRR - 1)) * 8;
         const uint32_t cold_off = (uint32_t)ntr * 8u;
-        const uint32_t st0 = su32(smem + w.off_stage) + (uint32_t)pair * (3 * (GS + 1) * 128);
+        const uint32_t st0 = su32(smem + w.off_stage) + (uint32_t)pair * (3 * GS * 128);
         const uint32_t sb = st0 + lane * 4;
-        const uint32_t pq0 = su32(smem + w.off_pend) + (uint32_t)pair * (kPend * 256) + lane * 8;
-        const uint32_t pqlim = pq0 + (kPend - 4 * kWordsPerCheck) * 256;   // room until the next check
+        const uint32_t pq0 = su32(smem + w.off_pend) + (uint32_t)pair * (kPend * 32) + lane;
+        const uint32_t pqlim = pq0 + (kPend - 4 * kWordsPerCheck) * 32;    // room until the next check
         const float zc = w.zc, oc = w.oc, alpha = p.alpha;
         const double den = *p.tb.den;
         const QRec q0 = p.tb.qrec[0];                              // queue 0 start (R4 / R12)
@@ -604,10 +646,13 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             mbar_wait(&full[s], (j >> 1) & 1);
             const int64_t b = slot_b[s];
             if (b >= nbatch) break;
-            if (j > 0 && w.use_tma) {
-                if (lane == 0) bulk_wait_read0();                  // previous tile read out
+            const bool tile_busy = j > 0 && w.use_tma;           // previous tile not yet read out
+#if !WS2_LATEWAIT
+            if (tile_busy) {
+                if (lane == 0) bulk_wait_read0();
                 __syncwarp();
             }
+#endif
             const int64_t c0 = b << 5, loc = c0 + lane;
             // row words; the slot has one spare word so the prefetch never leaves it
             uint32_t ra = su32(smem + w.off_rows) + (uint32_t)s * tw * 128 + 4 * lane;
@@ -623,6 +668,20 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             ts.pbit = q0bit; ts.seen = 0u; ts.warm = 0u; ts.cum = 0; ts.capd = q0cap;
             uint32_t cur = ld_u32(ra);
             int wi = 0;
+#if WS2_LATEWAIT
+            {   // word 0 peeled: its table loads run before the wait for the TMA
+                // engine to finish reading the previous tile out of the staging
+                WordData d;
+                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d);
+                cur = ld_u32(ra + (nw > 1 ? 1 : 0) * 128);
+                if (tile_busy) {
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+                }
+                compute_word<GS, SCORE>(d, sb, zc, oc, a);
+                wi = 1;
+            }
+#endif
             for (; wi + 1 < nw; wi += 2) {
                 const uint32_t nxt = ld_u32(ra + (wi + 1) * 128);
                 WordData d;
@@ -639,6 +698,32 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
                 compute_word<GS, SCORE>(d, sb, zc, oc, a);
             }
             flush<GS, SCORE>(pq0, rb, sb, alpha, a);
+            mbar_arrive(&empty[s]);                                 // row slot free
+            if (w.use_tma) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if (p.wt) tma_store_2d(&w.tmap[0], st0, (int)c0, 0);
+                    if (p.sd) tma_store_2d(&w.tmap[1], st0 + GS * 128, (int)c0, 0);
+                    if (p.vo) tma_store_2d(&w.tmap[2], st0 + 2 * GS * 128, (int)c0, 0);
+                    bulk_commit();
+                }
+            } else {
+                __syncwarp();
+                if (loc < count) {
+                    const float *stf = reinterpret_cast<const float *>(smem + w.off_stage) +
+                                       (size_t)pair * 3 * GS * 32 + lane;
+                    const int64_t ld = p.ld_out ? p.ld_out : count;
+                    for (int g = 0; g < G; ++g) {
+                        const int64_t o = (int64_t)g * ld + loc;
+                        if (p.wt) p.wt[o] = stf[g * 32];
+                        if (p.sd) p.sd[o] = stf[(GS + g) * 32];
+                        if (p.vo) p.vo[o] = stf[(2 * GS + g) * 32];
+                    }
+                }
+                __syncwarp();
+            }
+            // scores after the tile's TMA store is issued (they need no staging)
             if (loc < count) {
                 if constexpr (SCORE > 0) {
                     const float s1 = (float)(((double)a.acc1 + a.acc2) / den);   // R11
@@ -650,31 +735,6 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
                     const int64_t c = first + loc;
                     if (better(key, c, bkey, bidx)) { bkey = key; bidx = c; }
                 }
-            }
-            mbar_arrive(&empty[s]);                                 // row slot free
-            if (w.use_tma) {
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    if (p.wt) tma_store_2d(&w.tmap[0], st0, (int)c0, 0);
-                    if (p.sd) tma_store_2d(&w.tmap[1], st0 + (GS + 1) * 128, (int)c0, 0);
-                    if (p.vo) tma_store_2d(&w.tmap[2], st0 + 2 * (GS + 1) * 128, (int)c0, 0);
-                    bulk_commit();
-                }
-            } else {
-                __syncwarp();
-                if (loc < count) {
-                    const float *stf = reinterpret_cast<const float *>(smem + w.off_stage) +
-                                       (size_t)pair * 3 * (GS + 1) * 32 + lane;
-                    const int64_t ld = p.ld_out ? p.ld_out : count;
-                    for (int g = 0; g < G; ++g) {
-                        const int64_t o = (int64_t)g * ld + loc;
-                        if (p.wt) p.wt[o] = stf[g * 32];
-                        if (p.sd) p.sd[o] = stf[(GS + 1 + g) * 32];
-                        if (p.vo) p.vo[o] = stf[(2 * GS + 2 + g) * 32];
-                    }
-                }
-                __syncwarp();
             }
         }
         if (w.use_tma && lane == 0) bulk_wait0();
@@ -714,20 +774,21 @@ static bool make_map(CUtensorMap *tm, float *ptr, int64_t count, int G) {
 }
 
 static size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
-static size_t a1k(size_t x) { return (x + 1023) & ~size_t(1023); }
+
+static size_t a128(size_t x) { return (x + 127) & ~size_t(127); }
 
 static size_t plan(Params &w, int W, int GS, bool tier) {
     const Dims &dm = w.p.dm;
+    (void)tier;                                            // tiered: 2 tables x 8 replicas, same bytes
     size_t off = 0;
-    w.off_tr = (int)off;    off = a16(off + (size_t)4 * dm.M * dm.M * kTrRep * 8);   // tiered: 2 x 8 replicas
-    w.off_rec = (int)off;   off = a16(off + (size_t)(dm.T + kNeutral) * kRecStride);
     w.tw = (dm.T + 3) / 4;
-    off = a1k(off);         // slot bases 1 KB aligned (the producer ORs byte offsets in)
-    w.off_rows = (int)off;  off = a16(off + (size_t)2 * W * w.tw * 128);
+    w.off_rows = (int)off;  off = a16(off + (size_t)2 * W * w.tw * 128);   // 1 KB aligned (the smem base)
+    w.off_tr = (int)off;    off = a16(off + (size_t)dm.M * (2 * dm.M + 1) * kTrRep * 8);
+    w.off_rec = (int)off;   off = a16(off + (size_t)(dm.T + neutral_count(dm.T)) * kRecStride);
     w.off_bar = (int)off;   off = a16(off + (size_t)6 * W * 8 + 8);
-    w.off_pend = (int)off;  off = a16(off + (size_t)W * kPend * 256);
-    off = a1k(off);
-    w.off_stage = (int)off; off += (size_t)W * 3 * (GS + 1) * 128;
+    w.off_pend = (int)off;  off = a16(off + (size_t)W * kPend * 32);
+    off = a128(off);        // TMA source tiles: 128-byte aligned
+    w.off_stage = (int)off; off += (size_t)W * 3 * GS * 128;
     w.pairs = W;
     return off;
 }
@@ -772,7 +833,7 @@ static cudaError_t launch_t(const ScanParams &p0, cudaStream_t st) {
         if (sm <= lim) { W = cand; smem = sm; break; }
     }
     if (W < 2) return cudaErrorNotSupported;
-    if (W > 6) W = 6;                       // 12 warps: 3 per scheduler
+    if (W > WS2_WMAX) W = WS2_WMAX;         // 7: 14 of 16 warps (the spread map)
     smem = plan(w, W, GS, TIER);
     const Dims &dm = p0.dm;
     w.zc = p0.zc;
@@ -795,7 +856,7 @@ static cudaError_t launch_t(const ScanParams &p0, cudaStream_t st) {
     if (grid < 1) grid = 1;
     qlog(1, "ws2_kernel<kind=%d,GS=%d,score=%d,tier=%d> count=%lld pairs=%d grid=%lld smem=%zu tma=%d", KIND,
          GS, SCORE, (int)TIER, (long long)p0.cd.count, W, (long long)grid, smem, w.use_tma);
-    kern<<<(unsigned)grid, (WS2_SPREAD && W == 6) ? 512 : 64 * W, smem, st>>>(w);
+    kern<<<(unsigned)grid, (WS2_SPREAD && W >= 6) ? 512 : 64 * W, smem, st>>>(w);
     ++g_launches;
     return cudaGetLastError();
 }
