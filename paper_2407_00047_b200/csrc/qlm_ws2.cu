@@ -67,6 +67,9 @@ template <bool TIER> __host__ __device__ constexpr int tr_rep() { return TIER ? 
 #ifndef WS2_XNOPROD
 #define WS2_XNOPROD 0
 #endif
+#ifndef WS2_PRELABEL
+#define WS2_PRELABEL 0    // 1: producers relabel separators in the final row words (measured +2 %, off)
+#endif
 #ifndef WS2_WMAX
 #define WS2_WMAX 7
 #endif
@@ -184,13 +187,35 @@ __device__ __forceinline__ uint32_t ld_u32(uint32_t a) {
     return v;
 }
 
+// Separator relabelling in row order: the k-th token >= G of a row becomes
+// G + k (the start of queue k + 1; padding bytes continue past T - 1 into the
+// neutral records).  `gns` = G + separators seen so far.  With WS2_PRELABEL
+// the producers apply it to every final row word, so the consumer reads labels.
+__device__ __forceinline__ uint32_t relabel_word(uint32_t w, uint32_t G, uint32_t &gns) {
+#if WS2_PRELABEL
+    uint32_t out = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        uint32_t t = __byte_perm(w, 0u, 0x4440u + k);
+        const bool sep = t >= G;
+        t = sep ? gns : t;
+        gns += sep ? 1u : 0u;
+        out |= t << (8 * k);
+    }
+    return out;
+#else
+    return w;
+#endif
+}
+
 // RANDOM (R10, T <= 256: two 16-bit swap indices per Philox word, 8 per block):
 // forward Fisher-Yates in the lane's column (shared address `cs` = slot + 4
 // lane; byte of token i at cs + (i mod 4) + 128 (i / 4)).  Position i is final
 // after step i (later steps touch positions > i), so finals are packed in a
 // register and leave as whole words.
-__device__ __forceinline__ void produce_random(uint32_t cs, int T, uint64_t seed, uint64_t c) {
+__device__ __forceinline__ void produce_random(uint32_t cs, int T, uint32_t G, uint64_t seed, uint64_t c) {
     const int tw = (T + 3) >> 2;
+    uint32_t gns = G;
     for (int w = 0; w < tw; ++w) st_u32(cs + w * 128, 0x03020100u + 0x04040404u * (uint32_t)w);
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     const uint32_t clo = (uint32_t)c, chi = (uint32_t)(c >> 32);
@@ -227,7 +252,7 @@ __device__ __forceinline__ void produce_random(uint32_t cs, int T, uint64_t seed
             const uint32_t w = pick4(wd, k >> 1);
             step(i0 + k, (k & 1) ? (w & 0xFFFF0000u) : (w << 16), pb + ((k >> 2) << 7) + (k & 3));
             if ((k & 3) == 3) {
-                st_u32(pb + ((k >> 2) << 7), fin);
+                st_u32(pb + ((k >> 2) << 7), relabel_word(fin, G, gns));
                 fin = 0;
             }
         }
@@ -245,7 +270,7 @@ __device__ __forceinline__ void produce_random(uint32_t cs, int T, uint64_t seed
             const uint32_t w = pick4(wd, k >> 1);
             step(i, (k & 1) ? (w & 0xFFFF0000u) : (w << 16), cs + (i & 3) + ((i >> 2) << 7));
             if ((i & 3) == 3) {
-                st_u32(cs + ((i >> 2) << 7), fin);
+                st_u32(cs + ((i >> 2) << 7), relabel_word(fin, G, gns));
                 fin = 0;
             }
         }
@@ -253,26 +278,27 @@ __device__ __forceinline__ void produce_random(uint32_t cs, int T, uint64_t seed
     {   // position T-1 holds whatever the last swap left there
         const int i = T - 1;
         fin |= ld_u8(cs + (i & 3) + ((i >> 2) << 7)) << ((i & 3) * 8);
-        st_u32(cs + ((i >> 2) << 7), fin | pad_mask(T));   // neutral padding past T-1
+        st_u32(cs + ((i >> 2) << 7), relabel_word(fin | pad_mask(T), G, gns));   // neutral padding past T-1
     }
 }
 
 // EXPLICIT byte rows: 16-byte loads of the lane's own row, word stores (the
 // caller's padding bytes past T-1 are replaced by neutral tokens).
-__device__ __forceinline__ void produce_explicit(uint32_t cs, int T, int tw, const uint8_t *row) {
+__device__ __forceinline__ void produce_explicit(uint32_t cs, int T, uint32_t G, int tw, const uint8_t *row) {
     const uint32_t pad = pad_mask(T);
+    uint32_t gns = G;
     for (int w = 0; w < tw; w += 4) {
         const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row + 4 * w));
         const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (w + k < tw) st_u32(cs + (w + k) * 128, w + k == tw - 1 ? x[k] | pad : x[k]);
+            if (w + k < tw) st_u32(cs + (w + k) * 128, relabel_word(w + k == tw - 1 ? x[k] | pad : x[k], G, gns));
     }
 }
 
 // NEIGHBOR over a byte base row (R18): base words (a broadcast load), the
 // candidate's transpositions in the lane's column, then relabelling.
-__device__ __forceinline__ void produce_neighbor(uint32_t cs, int T, int tw, const Cand &cd, uint64_t c) {
+__device__ __forceinline__ void produce_neighbor(uint32_t cs, int T, uint32_t G, int tw, const Cand &cd, uint64_t c) {
     const uint32_t *b32 = reinterpret_cast<const uint32_t *>(cd.rows);
     for (int w = 0; w < tw; ++w) st_u32(cs + w * 128, __ldg(b32 + w) | (w == tw - 1 ? pad_mask(T) : 0u));
     int mi[QLM_MAX_MOVES], mj[QLM_MAX_MOVES];
@@ -284,16 +310,21 @@ __device__ __forceinline__ void produce_neighbor(uint32_t cs, int T, int tw, con
         st_u8(ai, ld_u8(aj));
         st_u8(aj, t);
     }
+#if WS2_PRELABEL
+    uint32_t gns = G;
+    for (int w = 0; w < tw; ++w) st_u32(cs + w * 128, relabel_word(ld_u32(cs + w * 128), G, gns));
+#endif
 }
 
 // ENUM (Lehmer unranking, lexicographic).
-__device__ __forceinline__ void produce_enum(uint32_t cs, int T, uint64_t c) {
+__device__ __forceinline__ void produce_enum(uint32_t cs, int T, uint32_t G, uint64_t c) {
     int s = 0;
+    uint32_t gns = G;
     uint32_t fin = 0;
     tokens_enum(c, T, [&](int tok) {
         fin |= (uint32_t)tok << ((s & 3) * 8);
         if ((s & 3) == 3 || s == T - 1) {
-            st_u32(cs + (s >> 2) * 128, s == T - 1 ? fin | pad_mask(T) : fin);
+            st_u32(cs + (s >> 2) * 128, relabel_word(s == T - 1 ? fin | pad_mask(T) : fin, G, gns));
             fin = 0;
         }
         ++s;
@@ -342,9 +373,15 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
         // stores, which are predicated off) (gq is incremented last: the compiler
         // may give G and gq one register when their values coincide, so no
         // operand is read after the write)
+#if WS2_PRELABEL
+        (void)gq;                                        // the producer relabelled the row
+        d.ix[k] = tok;
+        d.kh[k] = tok >= G ? 0 : 0x3FF00000;
+#else
         asm("{\n.reg .pred p;\nsetp.ge.s32 p, %3, %4;\nselp.b32 %0, %2, %3, p;\n"
             "selp.b32 %1, 0, 0x3FF00000, p;\n@p add.s32 %2, %2, 1;\n}\n"
             : "=r"(d.ix[k]), "=r"(d.kh[k]), "+r"(gq) : "r"(tok), "r"(G));
+#endif
         const uint32_t ra = (uint32_t)d.ix[k] * kRecStride;
         const float4 r0 = lds128(rb + ra);               // {a, slo hi, n}
         d.aw[k] = __hiloint2double(__float_as_int(r0.y), __float_as_int(r0.x));
@@ -611,14 +648,15 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             const int64_t loc = (b << 5) + lane;
             const uint32_t sl = su32(smem + w.off_rows) + (uint32_t)s * tw * 128;
             if (loc < count && !(WS2_XNOPROD && j >= 2)) {
-                if constexpr (KIND == QLM_CAND_RANDOM) produce_random(sl + 4 * lane, T, cd.seed, (uint64_t)(first + loc));
-                else if constexpr (KIND == QLM_CAND_EXPLICIT) produce_explicit(sl + 4 * lane, T, tw, cd.rows + loc * cd.stride);
-                else if constexpr (KIND == QLM_CAND_NEIGHBOR) produce_neighbor(sl + 4 * lane, T, tw, cd, (uint64_t)(first + loc));
-                else produce_enum(sl + 4 * lane, T, (uint64_t)(first + loc));
+                if constexpr (KIND == QLM_CAND_RANDOM) produce_random(sl + 4 * lane, T, G, cd.seed, (uint64_t)(first + loc));
+                else if constexpr (KIND == QLM_CAND_EXPLICIT) produce_explicit(sl + 4 * lane, T, G, tw, cd.rows + loc * cd.stride);
+                else if constexpr (KIND == QLM_CAND_NEIGHBOR) produce_neighbor(sl + 4 * lane, T, G, tw, cd, (uint64_t)(first + loc));
+                else produce_enum(sl + 4 * lane, T, G, (uint64_t)(first + loc));
             } else {                                          // past the range: a valid row
+                uint32_t gns = G;
                 for (int wd = 0; wd < tw; ++wd)
-                    st_u32(sl + 4 * lane + wd * 128, (0x03020100u + 0x04040404u * (uint32_t)wd) |
-                                                         (wd == tw - 1 ? pad_mask(T) : 0u));
+                    st_u32(sl + 4 * lane + wd * 128,
+                           relabel_word((0x03020100u + 0x04040404u * (uint32_t)wd) | (wd == tw - 1 ? pad_mask(T) : 0u), G, gns));
             }
             mbar_arrive(&full[s]);
         }
