@@ -424,7 +424,8 @@ QLM_API int64_t qlm_kernel_launches(void);   /* kernels launched by this process
 #define QLM_OVERRIDE_NO_WIDE 8u        /* no warp-per-candidate large-G bulk kernel           */
 #define QLM_OVERRIDE_NO_TIER_WARP 16u  /* no lane-per-queue tiered kernel                     */
 #define QLM_OVERRIDE_NO_GRAPH 32u      /* qlm_local_search launches directly (no CUDA graph)   */
-#define QLM_OVERRIDE_ALL 63u
+#define QLM_OVERRIDE_NO_LARGE 64u      /* no D = 1 thread-per-candidate large-T scorer (qlm_large.cu) */
+#define QLM_OVERRIDE_ALL 127u
 QLM_API int qlm_set_kernel_overrides(uint32_t flags, int64_t ilv_cap);
 QLM_API int qlm_abi_version(void);
 

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("QLM_LIB_PATH") or os.path.join(os.path.dirname(os.pat
 
 QLM_OK, QLM_EINVAL, QLM_ENOMEM, QLM_ECUDA, QLM_ENCCL, QLM_EBADORDER, QLM_ERANGE = 0, 1, 2, 3, 4, 5, 6
 COMM_ID_BYTES = 128
-OVERRIDE = {"no_ws": 1, "no_ws2": 2, "no_two_phase": 4, "no_wide": 8, "no_tier_warp": 16, "no_graph": 32}
+OVERRIDE = {"no_ws": 1, "no_ws2": 2, "no_two_phase": 4, "no_wide": 8, "no_tier_warp": 16, "no_graph": 32, "no_large": 64}
 CAND_EXPLICIT, CAND_RANDOM, CAND_ENUM, CAND_NEIGHBOR = 0, 1, 2, 3
 MAX_MOVES = 8
 

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libqlm.so")
 OBJ_DIR = os.path.join(ROOT, "build", "lib_objs")
-SOURCES = [os.path.join(PKG, "csrc", n) for n in ("qlm_api.cu", "qlm_kernels.cu", "qlm_ws.cu", "qlm_ws2.cu", "qlm_wide.cu", "qlm_req.cu", "qlm_tier.cu", "qlm_group.cu", "qlm_big.cu", "qlm_comm.cu")]
+SOURCES = [os.path.join(PKG, "csrc", n) for n in ("qlm_api.cu", "qlm_kernels.cu", "qlm_ws.cu", "qlm_ws2.cu", "qlm_wide.cu", "qlm_req.cu", "qlm_tier.cu", "qlm_group.cu", "qlm_big.cu", "qlm_comm.cu", "qlm_large.cu")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
 LDFLAGS = ARCH + ["-shared", "-ldl"]

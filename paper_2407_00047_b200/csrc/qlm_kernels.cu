@@ -1025,7 +1025,7 @@ static cudaError_t launch_two_phase(const ScanParams &p0, cudaStream_t st) {
         if (p.sd) p.sd += c0;
         if (p.vo) p.vo += c0;
         if (p0.out_rec) p.out_rec = p0.chunk_recs + (c0 ? 1 : 0);
-        e = wide_first(p) ? launch_wide(p, st) : cudaErrorNotSupported;
+        e = wide_first(p) ? launch_wide(p, st) : launch_large(p, st);
         if (e == cudaErrorNotSupported) {
             cudaGetLastError();
             e = launch_scan_k<KIND_ILV, uint16_t>(p, st);

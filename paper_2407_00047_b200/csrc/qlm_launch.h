@@ -62,6 +62,7 @@ cudaError_t launch_ws_tier(ScanParams p, cudaStream_t st); // same, two-tier swa
 cudaError_t launch_ws2_tier(const ScanParams &p, cudaStream_t st);  // ws2 with R20 (D = 1 / byte rows)
 cudaError_t launch_any_scan(const ScanParams &p, cudaStream_t st);   // ws, else scan
 cudaError_t launch_wide(const ScanParams &p, cudaStream_t st);      // warp per candidate (large G)
+cudaError_t launch_large(const ScanParams &p, cudaStream_t st);     // D = 1 score-only over 16-bit ILV rows
 cudaError_t launch_big(const ScanParams &p, cudaStream_t st);       // very large G: global tables
 cudaError_t launch_big_tier(const ScanParams &p, cudaStream_t st);  // same, two-tier swapping (R20)
 cudaError_t launch_req(const ScanParams &p, const qlm_group *groups, float *frac, float *s1r,

@@ -68,11 +68,11 @@ def queues_array(device, resident, backlog_mean=None, backlog_var=None) -> np.nd
 
 
 def kernel_overrides(no_ws=False, no_ws2=False, no_two_phase=False, no_wide=False, no_tier_warp=False,
-                     no_graph=False, ilv_cap=0):
+                     no_graph=False, no_large=False, ilv_cap=0):
     """Testing: restrict the library's kernel choice process-wide
     (qlm_set_kernel_overrides); call with no arguments to restore the default."""
     kw = dict(no_ws=no_ws, no_ws2=no_ws2, no_two_phase=no_two_phase, no_wide=no_wide,
-              no_tier_warp=no_tier_warp, no_graph=no_graph)
+              no_tier_warp=no_tier_warp, no_graph=no_graph, no_large=no_large)
     flags = sum(L.OVERRIDE[k] for k, v in kw.items() if v)
     L.check(L.lib().qlm_set_kernel_overrides(flags, int(ilv_cap)), "qlm_set_kernel_overrides")
 
