@@ -23,7 +23,6 @@
 #include "qlm_device.cuh"
 #include "qlm_launch.h"
 
-#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -315,10 +314,10 @@ static cudaError_t launch_t(const ScanParams &p0, cudaStream_t st) {
     w.p = p0;
     w.oc = 1.0f > p0.alpha ? 1.0f : 0.0f;
     // replicas of the record halves: the most that fit next to 16 warps'
-    // FIFOs (QLM_LARGE_REP = "r0,r1" pins them for A/B timing)
+    // FIFOs (QLM_LARGE_R0 / _R1 = log2 replicas, read once per process, pin
+    // them for A/B timing; measured: 4 x 4 and 8 x 4 within 1 %)
     const int warps = 16;
-    int r0 = 3, r1 = 4;
-    if (const char *s = getenv("QLM_LARGE_REP")) sscanf(s, "%d,%d", &r0, &r1);
+    int r0 = env_cached("QLM_LARGE_R0", 3), r1 = env_cached("QLM_LARGE_R1", 4);
     size_t smem = plan(w, warps, r0, r1);
     while (smem > lim && (r0 > 0 || r1 > 0)) {
         if (r1 >= r0 && r1 > 0) --r1; else --r0;

@@ -69,7 +69,7 @@ def items():
             cand = e.random(0, n, seed=1)
             rec = torch.empty(2, dtype=torch.int64, device="cuda")
             return (lambda: e.best_ordering_async(cand, rec)), n, "orderings/s", None, \
-                r"scan_kernel|fy_rows_kernel"
+                r"scan_kernel|fy_rows_kernel|large_kernel"
         return setup
 
     def c4_mc():
@@ -149,7 +149,7 @@ def items():
         ("rwt_estimate EXPLICIT u8 rows (ws2_kernel, bulk only)", "C3", c3_explicit),
         ("best_ordering_async RANDOM (score + argmin only)", "C2", score_only("C2", 1_000_000)),
         ("best_ordering_async RANDOM (score + argmin only)", "C3", score_only("C3", 1_000_000)),
-        ("best_ordering_async RANDOM (two-phase: fy_rows + scan)", "C5", score_only("C5", 1_000_000)),
+        ("best_ordering_async RANDOM (two-phase: fy_rows + large_kernel)", "C5", score_only("C5", 1_000_000)),
         ("mc_sample 1221 trials (Philox + length tables)", "C4", c4_mc),
         ("mc_count 1221 trials of one ordering", "C4", c4_mc_count),
         ("score_estimate RANDOM bulk + argmin (wide_kernel)", "C5", bulk("C5", 100_000)),
@@ -258,7 +258,7 @@ def items_meta():
         ("rwt_estimate EXPLICIT u8 rows (ws2_kernel, bulk only)", "C3", r"ws2_kernel<0,"),
         ("best_ordering_async RANDOM (score + argmin only)", "C2", r"scan_kernel<1, unsigned char"),
         ("best_ordering_async RANDOM (score + argmin only)", "C3", r"scan_kernel<1, unsigned char"),
-        ("best_ordering_async RANDOM (two-phase: fy_rows + scan)", "C5", r"fy_rows_kernel|scan_kernel<7|reduce_records"),
+        ("best_ordering_async RANDOM (two-phase: fy_rows + large_kernel)", "C5", r"fy_rows_kernel|large_kernel|scan_kernel<7|reduce_records"),
         ("mc_sample 1221 trials (Philox + length tables)", "C4", r"mc_sample_kernel"),
         ("mc_count 1221 trials of one ordering", "C4", r"mc_count_kernel"),
         ("score_estimate RANDOM bulk + argmin (wide_kernel)", "C5", r"fy_rows_kernel|wide_kernel|reduce_records"),

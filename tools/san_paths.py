@@ -1,6 +1,7 @@
 """Small launches of the bulk kernels for compute-sanitizer (memcheck /
 racecheck / synccheck): ws2_kernel (plain and tiered), wide_kernel and
-tier_warp_kernel on the two-phase rows."""
+tier_warp_kernel on the two-phase rows, and the score-only large-T path
+(fy_rows_kernel + large_kernel)."""
 import sys
 
 sys.path.insert(0, ".")
@@ -23,8 +24,18 @@ def run(cfg, n, tiered):
     print(cfg, n, "tiered" if tiered else "plain", rec.tolist())
 
 
+def score_only(cfg, n):
+    p = make_config(cfg)
+    e = RwtEstimator(p)
+    s1, s2, nov = e.score_orderings(e.random(0, n, seed=1))
+    rec = e.best_ordering_async(e.random(0, n, seed=1))
+    torch.cuda.synchronize()
+    print(cfg, n, "score-only", rec.tolist())
+
+
 if __name__ == "__main__":
     run("C3", 8192, False)
     run("C3", 8192, True)
     run("C5", 4096, False)
     run("C5h", 4096, True)
+    score_only("C5", 4096 + 77)
