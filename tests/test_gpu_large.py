@@ -96,3 +96,58 @@ def test_large_kernel_is_chosen_for_C5():
                        env=dict(os.environ, QLM_LOG="1"), timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "large_kernel<score=" in r.stderr, r.stderr[-2000:]
+
+
+def unclamped_problem(G, Q, M, seed):
+    """A D = 1 problem where most slots have |z| < z_clamp: large output
+    variance and each SLO at the median waiting time of its group over a
+    sample of orderings, so the deferred-Phi-bar FIFOs of ws2_kernel /
+    large_kernel fill and flush many times per row (R8/R9)."""
+    rng = np.random.default_rng(seed)
+    p = make_random_problem(rng, G, Q, M, backlog=True)
+    p.n_req = rng.integers(1, 4, G).astype(np.int32)         # few requests: sd ~ mean per group
+    p.var = (3.0 * p.mu) ** 2
+    p.q_backlog_var = np.maximum(p.q_backlog_var, 4.0)      # sd > 0 at every queue head
+    p.dtok, p.prefill, p.swap = p.dtok * 1e-3, p.prefill * 1e-3, p.swap * 1e-3   # small fixed terms
+    wt = O.Oracle(p).estimate_range(O.RANDOM, 0, 64, seed=11)["wt"]   # [count][G]
+    p.slo = np.median(wt, axis=0) * rng.uniform(0.9, 1.1, G)
+    return hi_only(p)
+
+
+@pytest.mark.parametrize("G,Q,seed", [(60, 5, 1), (120, 9, 2), (300, 7, 3)])
+def test_deferred_fifo_stress(G, Q, seed):
+    # most slots unclamped: ws2 (T <= 256) / large_kernel (T > 256) equal the
+    # general kernels bit for bit (bulk for ws2, scores for both) and the
+    # oracle on a tail; S1 is dominated by the FIFO's Phi-bar terms
+    from paper_2407_00047_b200 import RwtEstimator, kernel_overrides
+    p = unclamped_problem(G, Q, 4, seed)
+    n = 4096 + 61
+    o = O.Oracle(p)
+    ref = o.score_range(O.RANDOM, 3 + n - 24, 24, seed=4)
+    est = o.estimate_range(O.RANDOM, 3 + n - 24, 24, seed=4)
+    frac_open = np.mean(np.abs(p.slo[None, :] - est["wt"]) < 8.0 * est["sd"])   # |z| < z_clamp
+    assert frac_open > 0.5, frac_open                  # the stress is real
+    res = {}
+    for path in ("fast", "general"):
+        kernel_overrides(no_ws2=path == "general", no_large=path == "general", no_wide=True)
+        try:
+            e = RwtEstimator(p, device=0)
+            cand = e.random(3, n, seed=4)
+            rec = torch.empty(2, dtype=torch.int64, device="cuda")
+            if p.T <= 256:
+                bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+                bufs["n_over"] = torch.empty(n, dtype=torch.int32, device="cuda")
+                out = e.score_estimate(cand, out=bufs, rec=rec)
+                res[path] = [out[k].clone() for k in ("wt", "sd", "v", "s1", "s2", "n_over")] + [rec.clone()]
+            else:
+                s1, s2, nov = e.score_orderings(cand)
+                rec = e.best_ordering_async(cand, rec)
+                res[path] = [s1.clone(), s2.clone(), nov.clone(), rec.clone()]
+            torch.cuda.synchronize()
+        finally:
+            kernel_overrides()
+    for a, b in zip(res["fast"], res["general"]):
+        assert torch.equal(a, b)
+    s1 = res["fast"][3 if p.T <= 256 else 0]
+    s2 = res["fast"][4 if p.T <= 256 else 1]
+    check_scores(s1[n - 24:].cpu().numpy(), s2[n - 24:].cpu().numpy(), ref, p)
