@@ -350,9 +350,15 @@ class RwtEstimator:
                                      self._stream(stream)), "qlm_mc_count")
         return counts
 
-    def decode(self, cand: Cand, stream=None):
-        qo = self._empty((cand.count, self.G), torch.int32)
-        po = self._empty((cand.count, self.G), torch.int32)
+    def decode(self, cand: Cand, stream=None, out=None):
+        """qlm_decode: queue and position of every group (int32 [count][G] each);
+        `out` = (qo, po) preallocated on the device (e.g. for another stream)."""
+        if out is not None:
+            qo, po = out
+            assert qo.shape == (cand.count, self.G) and po.shape == qo.shape and qo.dtype == po.dtype == torch.int32
+        else:
+            qo = self._empty((cand.count, self.G), torch.int32)
+            po = self._empty((cand.count, self.G), torch.int32)
         L.check(L.lib().qlm_decode(self._h, C.byref(cand.c()), qo.data_ptr(), po.data_ptr(),
                                    self._stream(stream)), "qlm_decode")
         return qo, po
