@@ -234,3 +234,17 @@ def test_qlm_create_without_gpu_is_a_named_error(lib):
     from workloads.synth import make_config
     with pytest.raises(L.QlmError, match="CUDA device|sm_"):
         RwtEstimator(make_config("C1"))
+
+
+def test_kernel_override_flags_match_header(lib):
+    # every QLM_OVERRIDE_* bit of qlm.h is named in the Python binding, ALL is
+    # their union, and an unknown bit is a named error (host-only call)
+    src = open(HEADER).read()
+    bits = {m.group(1).lower(): int(m.group(2)) for m in
+            re.finditer(r"#define QLM_OVERRIDE_(\w+) (\d+)u", src) if m.group(1) != "ALL"}
+    assert bits == L.OVERRIDE
+    every = int(re.search(r"#define QLM_OVERRIDE_ALL (\d+)u", src).group(1))
+    assert every == sum(bits.values())
+    assert lib.qlm_set_kernel_overrides(every + 1, 0) != 0
+    assert lib.qlm_set_kernel_overrides(every, 0) == 0
+    assert lib.qlm_set_kernel_overrides(0, 0) == 0
