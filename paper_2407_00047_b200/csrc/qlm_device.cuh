@@ -9,6 +9,22 @@
 
 #include "qlm.h"
 
+// Debug bounds checks (build with -DQLM_BOUNDS, tools/gpu/s3_bounds.sh): a
+// failed check prints its condition and traps, so the calling test fails.
+#ifdef QLM_BOUNDS
+#include <cstdio>
+#define QLM_CHECK(c)                                                                          \
+    do {                                                                                      \
+        if (!(c)) {                                                                           \
+            printf("QLM_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,     \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                                   \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
+#else
+#define QLM_CHECK(c) do { } while (0)
+#endif
+
 namespace qlm {
 
 // ---- derived tables in HBM (built on the device by build_tables_kernel) ----

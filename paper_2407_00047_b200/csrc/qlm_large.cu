@@ -75,6 +75,8 @@ struct Ctx {
     uint32_t s0, s1;         // record strides (bytes per token)
     int G, R;                // groups, transition row stride (entries)
     float zc, oc;
+    int T;                   // QLM_BOUNDS limits: record entries, transition table end,
+    uint32_t tr_hi, pq_hi;   // end of the lane's FIFO
 };
 
 // One slot (R1-R9, R11, R22), token `tok` of the row in row order.
@@ -84,9 +86,11 @@ __device__ __forceinline__ void slot(const Ctx &c, int tok, uint32_t &prow, int 
     asm("{\n.reg .pred p;\nsetp.ge.s32 p, %3, %4;\nselp.b32 %0, %2, %3, p;\n"
         "selp.b32 %1, 0, 0x3FF00000, p;\n@p add.s32 %2, %2, 1;\n}\n"
         : "=r"(ix), "=r"(kh), "+r"(gq) : "r"(tok), "r"(c.G));
+    QLM_CHECK(ix >= 0 && ix < c.T);
     const float4 r0 = lds128(c.rb0 + (uint32_t)ix * c.s0);      // {a, hi word of slo, n}
     const float2 r1 = lds64v(c.rb1 + (uint32_t)ix * c.s1);      // {b, 128 * state}
     const uint32_t xs = (uint32_t)__float_as_int(r1.y);
+    QLM_CHECK(prow + xs + 8 <= c.tr_hi);
     const double tr = lds64f(prow + xs);                         // row of the state before
     prow = c.tb + xs * (uint32_t)c.R;
     const double aw = __hiloint2double(__float_as_int(r0.y), __float_as_int(r0.x));
@@ -110,6 +114,7 @@ __device__ __forceinline__ void slot(const Ctx &c, int tok, uint32_t &prow, int 
     }
     a.S2 = __fma_rn(slack, -keep, a.S2);                         // S2 += wt - slo (groups only)
     if (!clamped) {                                              // exact Phi-bar at the flush
+        QLM_CHECK(a.pq < c.pq_hi);
         asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a.pq), "f"(sf), "f"(sd), "f"(r0.w),
                      "f"(0.0f) : "memory");
         a.pq += 32 * 16;
@@ -202,6 +207,8 @@ __global__ void __launch_bounds__(512, 1) large_kernel(const __grid_constant__ P
     c.R = M;
     c.zc = p.zc;
     c.oc = w.oc;
+    c.T = T;
+    c.tr_hi = su32(smem + w.off_tr) + (uint32_t)ntr * 8u;
     const float alpha = p.alpha;
     const double den = *p.tb.den;
     const QRec q0 = p.tb.qrec[0];
@@ -210,6 +217,7 @@ __global__ void __launch_bounds__(512, 1) large_kernel(const __grid_constant__ P
     const uint32_t prow0 = c.tb + (uint32_t)(q0.backlog ? q0.r : M + q0.r) * (kTrRep * 8u) * (uint32_t)M;
     const uint32_t pq0 = su32(smem + w.off_pend) + (uint32_t)(tid >> 5) * (kPend * 512u) + lane * 16u;
     const uint32_t pqlim = pq0 + (kPend - 2 * kWPC) * 512u;    // room until the next check
+    c.pq_hi = pq0 + kPend * 512u;
     const int nw = (T + 1) >> 1, nfull = T >> 1;
     const int64_t ld = cd.stride;                                // words are [nw][stride] u32
     uint64_t bkey = ~0ull;

@@ -228,6 +228,7 @@ __device__ __forceinline__ void produce_random(uint32_t cs, int T, uint32_t G, u
         asm("{\n.reg .u64 t;\nmul.wide.u32 t, %1, %2;\nmov.b64 {_, %0}, t;\n}\n"
             : "=r"(jd) : "r"(u16hi), "r"((uint32_t)(T - i)));
         const uint32_t j = (uint32_t)i + jd;
+        QLM_CHECK(j < (uint32_t)T && j >= (uint32_t)i);
         const uint32_t aj = (j >> 2) * 124u + (cs + j);
         const uint32_t ti = ld_u8(ai), tj = ld_u8(aj);
         st_u8(aj, ti);
@@ -361,10 +362,17 @@ struct TierState {
     int cum, capd;
 };
 
+// Address limits for the QLM_BOUNDS build (unused otherwise).
+struct Bounds {
+    int ntok;                 // record entries (tokens + neutral padding)
+    uint32_t tr_lo, tr_hi;    // transition table(s), shared addresses
+    uint32_t pq_hi;           // end of the lane's FIFO
+};
+
 template <bool TIER>
 __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb, uint32_t rb1, uint32_t tb,
                                           uint32_t cold_off, uint32_t &prow, int &gq, TierState &ts,
-                                          WordData &d) {
+                                          WordData &d, const Bounds &bd) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int tok = (int)__byte_perm(wd, 0u, 0x4440u + k);
@@ -382,6 +390,7 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
             "selp.b32 %1, 0, 0x3FF00000, p;\n@p add.s32 %2, %2, 1;\n}\n"
             : "=r"(d.ix[k]), "=r"(d.kh[k]), "+r"(gq) : "r"(tok), "r"(G));
 #endif
+        QLM_CHECK(d.ix[k] >= 0 && d.ix[k] < bd.ntok);
         const uint32_t ra = (uint32_t)d.ix[k] * kRecStride;
         const float4 r0 = lds128(rb + ra);               // {a, slo hi, n}
         d.aw[k] = __hiloint2double(__float_as_int(r0.y), __float_as_int(r0.x));
@@ -413,6 +422,7 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
             ts.seen = sep ? 0u : ts.seen;
             ts.warm = sep ? 0u : ts.warm;
             ts.cum = sep ? 0 : ts.cum;
+            QLM_CHECK(prow + xs + (cold ? cold_off : 0u) >= bd.tr_lo && prow + xs + (cold ? cold_off : 0u) + 8 <= bd.tr_hi);
             d.tr[k] = lds64f(prow + xs + (cold ? cold_off : 0u));
         } else {
             const float2 r1 = lds64v(rb1 + ra);          // {b, 128 * state}
@@ -422,6 +432,7 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
 #else
             xs = (uint32_t)__float_as_int(r1.y);
 #endif
+            QLM_CHECK(prow + xs >= bd.tr_lo && prow + xs + 8 <= bd.tr_hi);
             d.tr[k] = lds64f(prow + xs);                 // row of the state before
         }
         prow = tb + xs * R;                              // row of this slot's state
@@ -429,7 +440,8 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
 }
 
 template <int GS, int SCORE>
-__device__ __forceinline__ void compute_word(const WordData &d, uint32_t sb, float zc, float oc, Acc &a) {
+__device__ __forceinline__ void compute_word(const WordData &d, uint32_t sb, float zc, float oc, Acc &a,
+                                             const Bounds &bd) {
     constexpr uint32_t ASTR = GS * 128;                  // staging array stride
     double wt[4];
     float V[4];
@@ -473,10 +485,12 @@ __device__ __forceinline__ void compute_word(const WordData &d, uint32_t sb, flo
         }
         if (!clamped) {                                  // |z| < z_clamp: exact value at flush
             // the token goes to the lane's byte FIFO, the slack to the v row
+            QLM_CHECK(a.pq < bd.pq_hi);
             asm volatile("st.shared.u8 [%0], %1;" ::"r"(a.pq), "r"(d.ix[k]) : "memory");
             a.pq += 32;
         }
         const uint32_t st = sb + (uint32_t)d.ix[k] * 128u;
+        QLM_CHECK(d.kh[k] == 0 || d.ix[k] < GS);              // stores only for groups
         if (WS2_XNOSTORE) continue;
         // separators and padding (keep = 0) store nothing
         asm volatile("{\n.reg .pred p;\nsetp.ne.s32 p, %4, 0;\n@p st.shared.f32 [%0], %1;\n"
@@ -494,6 +508,7 @@ __device__ __forceinline__ void flush(uint32_t pq0, uint32_t rb, uint32_t sb, fl
     for (int i = 0; i < maxn; ++i) {
         if (i < n) {
             const int ix = (int)ld_u8(pq0 + i * 32);
+            QLM_CHECK(ix < GS);                                  // only groups are deferred
             const uint32_t s = sb + (uint32_t)ix * 128u;
             float sd, sf;
             asm volatile("ld.shared.f32 %0, [%1];" : "=f"(sd) : "r"(s + GS * 128));
@@ -679,6 +694,11 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
         const uint32_t q0bit = 1u << q0.r;
         const int q0cap = TIER ? min(p.t_cap[q0.d], summem) : 0;
         const int nw = (T + 3) >> 2;                               // row words (padded)
+        Bounds bd;
+        bd.ntok = T + neutral_count(T);
+        bd.tr_lo = su32(smem + w.off_tr);
+        bd.tr_hi = bd.tr_lo + (uint32_t)(TIER ? 2 : 1) * (uint32_t)ntr * 8u;
+        bd.pq_hi = pq0 + kPend * 32u;
         for (int j = 0;; ++j) {
             const int s = 2 * pair + (j & 1);
             mbar_wait(&full[s], (j >> 1) & 1);
@@ -710,30 +730,30 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             {   // word 0 peeled: its table loads run before the wait for the TMA
                 // engine to finish reading the previous tile out of the staging
                 WordData d;
-                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d);
+                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d, bd);
                 cur = ld_u32(ra + (nw > 1 ? 1 : 0) * 128);
                 if (tile_busy) {
                     if (lane == 0) bulk_wait_read0();
                     __syncwarp();
                 }
-                compute_word<GS, SCORE>(d, sb, zc, oc, a);
+                compute_word<GS, SCORE>(d, sb, zc, oc, a, bd);
                 wi = 1;
             }
 #endif
             for (; wi + 1 < nw; wi += 2) {
                 const uint32_t nxt = ld_u32(ra + (wi + 1) * 128);
                 WordData d;
-                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d);
-                compute_word<GS, SCORE>(d, sb, zc, oc, a);
+                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d, bd);
+                compute_word<GS, SCORE>(d, sb, zc, oc, a, bd);
                 cur = ld_u32(ra + (wi + 2 < nw ? wi + 2 : wi + 1) * 128);
-                load_word<TIER>(nxt, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d);
-                compute_word<GS, SCORE>(d, sb, zc, oc, a);
+                load_word<TIER>(nxt, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d, bd);
+                compute_word<GS, SCORE>(d, sb, zc, oc, a, bd);
                 if (__any_sync(0xFFFFFFFFu, a.pq > pqlim)) flush<GS, SCORE>(pq0, rb, sb, alpha, a);
             }
             if (wi < nw) {
                 WordData d;
-                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d);
-                compute_word<GS, SCORE>(d, sb, zc, oc, a);
+                load_word<TIER>(cur, G, R, rb, rb1, tb, cold_off, prow, gq, ts, d, bd);
+                compute_word<GS, SCORE>(d, sb, zc, oc, a, bd);
             }
             flush<GS, SCORE>(pq0, rb, sb, alpha, a);
             mbar_arrive(&empty[s]);                                 // row slot free
