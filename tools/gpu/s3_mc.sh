@@ -1,0 +1,18 @@
+QLM_LIB_PATH=build/variants/libqlm_mcw.so timeout 900 python -m pytest tests -q -m gpu -k "mc or MC or smoke or bench_step" -x 2>&1 | tail -3
+for v in mcb mcw mcb mcw; do echo "$v"; QLM_LIB_PATH=build/variants/libqlm_$v.so python tools/step_parts.py 2>&1 | grep -E "full|no count|scan only"; done
+for v in mcb mcw; do echo "$v C4"; QLM_LIB_PATH=build/variants/libqlm_$v.so python - <<'PY'
+import sys, torch; sys.path.insert(0, ".")
+import __graft_entry__; __graft_entry__.build()
+from paper_2407_00047_b200 import RwtEstimator
+from workloads.synth import make_config
+for cfg in ("C3", "C4"):
+    e = RwtEstimator(make_config(cfg))
+    for _ in range(3): e.mc_sample(2, 1221)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(20): e.mc_sample(2, 1221)
+    b.record(); torch.cuda.synchronize()
+    print(cfg, "mc_sample us", a.elapsed_time(b) / 20 * 1000)
+PY
+done
