@@ -151,3 +151,32 @@ def test_deferred_fifo_stress(G, Q, seed):
     s1 = res["fast"][3 if p.T <= 256 else 0]
     s2 = res["fast"][4 if p.T <= 256 else 1]
     check_scores(s1[n - 24:].cpu().numpy(), s2[n - 24:].cpu().numpy(), ref, p)
+
+
+@pytest.mark.parametrize("G,Q,M", [(40, 150, 3), (100, 157, 6), (9, 200, 2)])
+def test_ws2_many_queues(G, Q, M):
+    # byte rows near T = 256 with many separators (T = 189, 256 -- no padding
+    # byte -- and 208): the seven-pair plan shrinks to fewer pairs; ws2 equals
+    # the general warp-specialised kernel and the scan bit for bit, and the oracle
+    from paper_2407_00047_b200 import RwtEstimator, kernel_overrides
+    p = hi_only(make_random_problem(np.random.default_rng(G + Q + M), G, Q, M, backlog=True))
+    assert p.T <= 256
+    n = 4096 + 33
+    res = {}
+    for path in ("ws2", "ws", "scan"):
+        kernel_overrides(no_ws2=path == "ws", no_ws=path == "scan")
+        try:
+            e = RwtEstimator(p, device=0)
+            rec = torch.empty(2, dtype=torch.int64, device="cuda")
+            bufs = {k: torch.empty((p.G, n), dtype=torch.float32, device="cuda") for k in ("wt", "sd", "v")}
+            bufs["n_over"] = torch.empty(n, dtype=torch.int32, device="cuda")
+            out = e.score_estimate(e.random(1, n, seed=2), out=bufs, rec=rec)
+            torch.cuda.synchronize()
+            res[path] = [out[k].clone() for k in ("wt", "sd", "v", "s1", "s2", "n_over")] + [rec.clone()]
+        finally:
+            kernel_overrides()
+    for path in ("ws", "scan"):
+        for a, b in zip(res["ws2"], res[path]):
+            assert torch.equal(a, b), path
+    ref = O.Oracle(p).score_range(O.RANDOM, 1 + n - 16, 16, seed=2)
+    check_scores(res["ws2"][3][n - 16:].cpu().numpy(), res["ws2"][4][n - 16:].cpu().numpy(), ref, p)
