@@ -70,6 +70,9 @@ template <bool TIER> __host__ __device__ constexpr int tr_rep() { return TIER ? 
 #ifndef WS2_PRELABEL
 #define WS2_PRELABEL 0    // 1: producers relabel separators in the final row words (measured +2 %, off)
 #endif
+#ifndef WS2_P6
+#define WS2_P6 0          // 1: six producers feed seven consumers (balanced schedulers; measured +10 %, off)
+#endif
 #ifndef WS2_WMAX
 #define WS2_WMAX 7
 #endif
@@ -135,6 +138,18 @@ __device__ __forceinline__ bool mbar_test(uint64_t *b, unsigned parity) {
         : "memory");
     return ok != 0;
 }
+// Per-slot consumption counters of the six-producer hand-off: several
+// producers fill one slot in turn, so the "slot free" signal is a count (an
+// mbarrier parity wait would let a producer two uses ahead pass early).
+__device__ __forceinline__ uint32_t ld_acquire_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *tm, uint32_t src, int x, int y) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
                  ::"l"(reinterpret_cast<uint64_t>(tm)), "r"(src), "r"(x), "r"(y)
@@ -603,9 +618,13 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
     uint64_t *empty = full + 2 * W;
     int64_t *slot_b = reinterpret_cast<int64_t *>(empty + 2 * W);
     unsigned long long *next_b = reinterpret_cast<unsigned long long *>(slot_b + 2 * W);
+    // six producers for seven consumers (16-warp spread map): static task
+    // rotation, "slot free" as a consumption count in empty[s]'s first word
+    const bool p6 = WS2_P6 && WS2_SPREAD && W == 7;
     if (tid < 2 * W) {
         mbar_init(&full[tid], 32);
-        mbar_init(&empty[tid], 32);
+        if (p6) *reinterpret_cast<volatile uint32_t *>(&empty[tid]) = 0u;
+        else mbar_init(&empty[tid], 32);
     }
     if (tid == 0) *next_b = 0ull;
     __syncthreads();
@@ -627,7 +646,9 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
         // 16-warp block, warp w on scheduler w % 4: consumers 0-6 (schedulers
         // 0,1,2,3,0,1,2), producers 7-11, 14, 15, warps 12, 13 idle
         const int pmap[16] = {0, 1, 2, 3, 4, 5, 6, 0, 1, 2, 3, 4, -1, -1, 5, 6};
-        role_pair = pmap[warp];
+        // p6: producers 7-11, 15 (one on schedulers 0-2, three on 3)
+        const int pmap6[16] = {0, 1, 2, 3, 4, 5, 6, 0, 1, 2, 3, 4, -1, -1, -1, 5};
+        role_pair = p6 ? pmap6[warp] : pmap[warp];
         is_prod = warp >= 7;
         idle = role_pair < 0;
     } else if (WS2_SPREAD && W == 6) {
@@ -644,13 +665,28 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
     } else if (is_prod) {   // ---------------- producer
         const int pair = role_pair;
         for (int j = 0;; ++j) {
-            const int s = 2 * pair + (j & 1);
+            int s;
+            int64_t b = 0;
+            if (p6) {
+                // task t = pair + 6 j of this block: batch blockIdx + t * grid,
+                // row k = t / 7 of consumer t mod 7
+                const int64_t t = pair + 6 * (int64_t)j;
+                b = blockIdx.x + t * grid;
+                if (b >= nbatch) break;
+                const int kk = (int)(t / 7);
+                s = 2 * (int)(t % 7) + (kk & 1);
+                const uint32_t ca = su32(&empty[s]);
+                if (lane == 0)
+                    while (ld_acquire_u32(ca) < (uint32_t)(kk >> 1)) __nanosleep(32);
+                __syncwarp();
+                if (lane == 0) slot_b[s] = b;
+            } else {
+            s = 2 * pair + (j & 1);
 #if WS2_SLEEP
             while (!mbar_test(&empty[s], ((j >> 1) & 1) ^ 1)) __nanosleep(WS2_SLEEP);
 #else
             mbar_wait(&empty[s], ((j >> 1) & 1) ^ 1);
 #endif
-            int64_t b = 0;
             if (lane == 0) {
                 b = blockIdx.x + (int64_t)atomicAdd(next_b, 1ull) * grid;
                 slot_b[s] = b;                                  // published by the arrive below
@@ -659,6 +695,7 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             if (b >= nbatch) {
                 mbar_arrive(&full[s]);
                 break;
+            }
             }
             const int64_t loc = (b << 5) + lane;
             const uint32_t sl = su32(smem + w.off_rows) + (uint32_t)s * tw * 128;
@@ -701,9 +738,16 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
         bd.pq_hi = pq0 + kPend * 32u;
         for (int j = 0;; ++j) {
             const int s = 2 * pair + (j & 1);
-            mbar_wait(&full[s], (j >> 1) & 1);
-            const int64_t b = slot_b[s];
-            if (b >= nbatch) break;
+            int64_t b;
+            if (p6) {
+                b = blockIdx.x + (pair + 7 * (int64_t)j) * grid;   // task pair + 7 j
+                if (b >= nbatch) break;
+                mbar_wait(&full[s], (j >> 1) & 1);
+            } else {
+                mbar_wait(&full[s], (j >> 1) & 1);
+                b = slot_b[s];
+                if (b >= nbatch) break;
+            }
             const bool tile_busy = j > 0 && w.use_tma;           // previous tile not yet read out
 #if !WS2_LATEWAIT
             if (tile_busy) {
@@ -756,7 +800,12 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
                 compute_word<GS, SCORE>(d, sb, zc, oc, a, bd);
             }
             flush<GS, SCORE>(pq0, rb, sb, alpha, a);
-            mbar_arrive(&empty[s]);                                 // row slot free
+            if (p6) {                                               // row slot free
+                __syncwarp();
+                if (lane == 0) st_release_u32(su32(&empty[s]), (uint32_t)((j >> 1) + 1));
+            } else {
+                mbar_arrive(&empty[s]);
+            }
             if (w.use_tma) {
                 fence_proxy_async_smem();
                 __syncwarp();
