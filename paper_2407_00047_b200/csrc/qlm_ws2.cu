@@ -369,11 +369,11 @@ struct WordData {
     int ix[4], kh[4];
 };
 
-// R20 state of the queue being walked: bit of the model in memory, targets
-// seen / warm, CPU memory taken, the queue's CPU memory (-1 once a target did
-// not fit: later targets are cold, the warm set is a strict prefix)
+// R20 state of the queue being walked: bit of the model in memory, warm
+// targets, CPU memory taken, the queue's CPU memory (-1 once a target did not
+// fit: later targets are cold, the warm set is a strict prefix)
 struct TierState {
-    uint32_t pbit, seen, warm;
+    uint32_t pbit, warm;
     int cum, capd;
 };
 
@@ -422,19 +422,21 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
             const uint32_t bit = (uint32_t)__float_as_int(r1.w);
             const bool sep = d.kh[k] == 0;
             // R20, in the order of qlm_ws.cu's tier walk: the first transition
-            // into a model makes it warm while it fits the CPU memory
+            // into a model makes it warm while it fits the CPU memory.  No
+            // "seen" set is needed: a model whose first transition did not fit
+            // left the queue exhausted (capd = -1), so testing it again can
+            // only fail again -- a transition is cold iff its model is not warm
+            // after the test
             const bool trn = !sep && bit != ts.pbit;
-            const bool first = trn && !(ts.seen & bit);
+            const bool test = trn && !(ts.warm & bit);   // first transition (or a failed one)
             const int need = ts.cum + mem;
             const bool fits = need <= ts.capd;
-            ts.seen |= first ? bit : 0u;
-            ts.warm |= (first && fits) ? bit : 0u;
-            ts.cum = (first && fits) ? need : ts.cum;
-            ts.capd = (first && !fits) ? -1 : ts.capd;
-            const bool cold = trn && !(ts.warm & bit);
+            ts.warm |= (test && fits) ? bit : 0u;
+            ts.cum = (test && fits) ? need : ts.cum;
+            const bool cold = test && !fits;
+            ts.capd = cold ? -1 : ts.capd;
             ts.pbit = bit;                                 // separator: its queue's resident
             ts.capd = sep ? mem : ts.capd;
-            ts.seen = sep ? 0u : ts.seen;
             ts.warm = sep ? 0u : ts.warm;
             ts.cum = sep ? 0 : ts.cum;
             QLM_CHECK(prow + xs + (cold ? cold_off : 0u) >= bd.tr_lo && prow + xs + (cold ? cold_off : 0u) + 8 <= bd.tr_hi);
@@ -767,7 +769,7 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             uint32_t prow = tb + (uint32_t)q0st * (TRR * 8u) * R;   // queue 0 start row
             int gq = G;
             TierState ts;
-            ts.pbit = q0bit; ts.seen = 0u; ts.warm = 0u; ts.cum = 0; ts.capd = q0cap;
+            ts.pbit = q0bit; ts.warm = 0u; ts.cum = 0; ts.capd = q0cap;
             uint32_t cur = ld_u32(ra);
             int wi = 0;
 #if WS2_LATEWAIT
