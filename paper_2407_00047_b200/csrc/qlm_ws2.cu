@@ -370,11 +370,11 @@ struct WordData {
 };
 
 // R20 state of the queue being walked: bit of the model in memory, warm
-// targets, CPU memory taken, the queue's CPU memory (-1 once a target did not
-// fit: later targets are cold, the warm set is a strict prefix)
+// targets, the queue's CPU memory not yet taken by them (-1 once a target did
+// not fit: later targets are cold, the warm set is a strict prefix)
 struct TierState {
     uint32_t pbit, warm;
-    int cum, capd;
+    int rem;
 };
 
 // Address limits for the QLM_BOUNDS build (unused otherwise).
@@ -427,18 +427,18 @@ __device__ __forceinline__ void load_word(uint32_t wd, int G, int R, uint32_t rb
             // left the queue exhausted (capd = -1), so testing it again can
             // only fail again -- a transition is cold iff its model is not warm
             // after the test
+            // `rem` = the queue's CPU memory minus what its warm models take
+            // (the walk's cum + mem <= capd is mem <= rem), -1 once exhausted
             const bool trn = !sep && bit != ts.pbit;
             const bool test = trn && !(ts.warm & bit);   // first transition (or a failed one)
-            const int need = ts.cum + mem;
-            const bool fits = need <= ts.capd;
+            const bool fits = mem <= ts.rem;
             ts.warm |= (test && fits) ? bit : 0u;
-            ts.cum = (test && fits) ? need : ts.cum;
+            ts.rem = (test && fits) ? ts.rem - mem : ts.rem;
             const bool cold = test && !fits;
-            ts.capd = cold ? -1 : ts.capd;
+            ts.rem = cold ? -1 : ts.rem;
             ts.pbit = bit;                                 // separator: its queue's resident
-            ts.capd = sep ? mem : ts.capd;
+            ts.rem = sep ? mem : ts.rem;
             ts.warm = sep ? 0u : ts.warm;
-            ts.cum = sep ? 0 : ts.cum;
             QLM_CHECK(prow + xs + (cold ? cold_off : 0u) >= bd.tr_lo && prow + xs + (cold ? cold_off : 0u) + 8 <= bd.tr_hi);
             d.tr[k] = lds64f(prow + xs + (cold ? cold_off : 0u));
         } else {
@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(512, 1) ws2_kernel(const __grid_constant__ Par
             uint32_t prow = tb + (uint32_t)q0st * (TRR * 8u) * R;   // queue 0 start row
             int gq = G;
             TierState ts;
-            ts.pbit = q0bit; ts.warm = 0u; ts.cum = 0; ts.capd = q0cap;
+            ts.pbit = q0bit; ts.warm = 0u; ts.rem = q0cap;
             uint32_t cur = ld_u32(ra);
             int wi = 0;
 #if WS2_LATEWAIT
